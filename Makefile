@@ -1,0 +1,23 @@
+# Builds libomni.so (sm_100a kernels + C-ABI) in-tree, plus the C oracle helper.
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+SRC_DIR := paper_1606_04487_b200/csrc
+BUILD := build
+SRCS := $(wildcard $(SRC_DIR)/*.cu)
+OBJS := $(patsubst $(SRC_DIR)/%.cu,$(BUILD)/%.o,$(SRCS))
+LIB := paper_1606_04487_b200/libomni.so
+
+all: $(LIB)
+
+$(BUILD)/%.o: $(SRC_DIR)/%.cu $(SRC_DIR)/common.cuh include/omni.h
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/$*.ptxas.log || (cat $(BUILD)/$*.ptxas.log; exit 1)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+
+clean:
+	rm -rf $(BUILD) $(LIB)
+
+.PHONY: all clean

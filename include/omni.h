@@ -1,0 +1,156 @@
+/*
+ * omni.h -- C-ABI of libomni.so, the sm_100a (B200) kernels behind the
+ * omnisim-compatible Python API in paper_1606_04487_b200/.
+ *
+ * The reference (omnisim 0.1.0, /root/reference/pkg/src/omnisim) is pure
+ * Python/NumPy and has no FFI; each entry point below replaces one NumPy op
+ * site on the data-parallel CNN training hot path and cites it.  The binding
+ * a maintainer adds on the reference side is ctypes.
+ *
+ * ABI rules
+ *   - every entry point returns 0 on success, a negative OMNI_E* status
+ *     otherwise; omni_last_error() returns a message for the calling thread;
+ *   - all launches are asynchronous on the caller's stream (a cudaStream_t
+ *     passed as void*; NULL = legacy default stream);
+ *   - the library never allocates persistent device memory: callers pass
+ *     every buffer, including GEMM split-K workspace (omni_gemm_plan sizes it);
+ *   - plain pointers and sizes only; row strides ("ld") are in ELEMENTS.
+ */
+#ifndef OMNI_H_
+#define OMNI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OMNI_OK 0
+#define OMNI_EINVAL -1       /* bad argument: maps to ValueError           */
+#define OMNI_ECUDA -2        /* CUDA runtime / driver failure: RuntimeError */
+#define OMNI_EUNSUPPORTED -3 /* shape/layout outside what a kernel handles  */
+
+const char* omni_last_error(void);
+int omni_version(void);
+int omni_device_sm_count(int device);
+
+/* ---------------------------------------------------------------- K1 --
+ * Batched lowering (type-1 im2col over b_p images starting at `start`).
+ * Replaces tensors.lower (tensors.py:164-181).  Row = img*m^2 + x*m + y,
+ * column = (c*k + kx)*k + ky (tensors.py:167-168); zero padding; pure copy,
+ * hence bit-exact in both element types.  Dhat is (b_p*m^2) x ld, ld >= c*k*k;
+ * columns [c*k*k, ld) are written with zeros.                              */
+int omni_lower_nchw_f32(const float* D, int b, int c, int n, int k, int stride, int pad,
+                        int start, int b_p, float* Dhat, long long ld, void* stream);
+int omni_lower_nchw_f64(const double* D, int b, int c, int n, int k, int stride, int pad,
+                        int start, int b_p, double* Dhat, long long ld, void* stream);
+/* Training-path lowering from NHWC activations (pixel stride cs >= c) with the
+ * tap-major column order (kx*k + ky)*c + ch.  Same values as the reference's
+ * lowered matrix up to that fixed column permutation.                      */
+int omni_lower_nhwc_f32(const float* X, int b, int n, int c, int cs, int k, int stride,
+                        int pad, float* Dhat, long long ld, void* stream);
+
+/* Lifting: Rhat (b*m^2) x ld -> NCHW (b, d_out, m, m).  Replaces tensors.lift
+ * (tensors.py:213-219); index remap only, bit-exact.                        */
+int omni_lift_nchw_f32(const float* Rhat, long long ld, int b, int m, int d_out, float* R,
+                       void* stream);
+int omni_lift_nchw_f64(const double* Rhat, long long ld, int b, int m, int d_out, double* R,
+                       void* stream);
+
+/* col2im (adjoint of omni_lower_nhwc_f32), deterministic gather form: dX (NHWC,
+ * pixel stride cs) is OVERWRITTEN with the sum over every lowered entry that
+ * copied from it.  Not in the reference (its only conv is layer 1, so
+ * problems.py:263-269 never needs dX); pinned by the adjoint identity.     */
+int omni_col2im_nhwc_f32(const float* dDhat, long long ld, int b, int n, int c, int cs, int k,
+                         int stride, int pad, float* dX, void* stream);
+
+/* ---------------------------------------------------------------- K2 --
+ * C[i,j] (op)= sum_r A(i,r) * B(j,r),  i < M, j < N, r < K, where
+ *   A(i,r) = a_mn_major ? A[r*lda + i] : A[i*lda + r]
+ *   B(j,r) = b_mn_major ? B[r*ldb + j] : B[j*ldb + r]
+ * Replaces tensors.gemm (tensors.py:193-210) and every product in
+ * problems.py:218,250-251,263-267.  tcgen05.mma kind::tf32 with TMA-fed
+ * 128B-swizzled shared-memory stages and TMEM accumulators.
+ * Requirements: lda, ldb multiples of 4 and A, B 16-byte aligned (TMA).     */
+#define OMNI_PREC_TF32 0      /* one tf32 pass (fast path)                        */
+#define OMNI_PREC_3XTF32 1    /* hi/lo split in shared memory, 3 tf32 passes       */
+#define OMNI_PREC_FP32_SIMT 2 /* CUDA-core fp32 (test reference only; not hot path) */
+
+#define OMNI_EPI_STORE 0       /* C = acc                                  */
+#define OMNI_EPI_BIAS 1        /* C = acc + bias[j]                        */
+#define OMNI_EPI_BIAS_RELU 2   /* C = max(acc + bias[j], 0)                */
+#define OMNI_EPI_ACCUM 3       /* C = C + acc                              */
+#define OMNI_EPI_MASK_AUX 4    /* C = acc * (aux[i*ld_aux + j] > 0)  (ReLU bwd) */
+#define OMNI_EPI_RELU 5        /* C = max(acc, 0)                          */
+
+/* Plan query: returns the split-K workspace (bytes) omni_gemm_f32 will need for
+ * these arguments; *splits / *bn report the chosen schedule (may be NULL).   */
+long long omni_gemm_plan(int precision, int M, int N, int K, int a_mn_major, int b_mn_major,
+                         int* splits, int* bn);
+int omni_gemm_f32(int precision, int M, int N, int K, const float* A, long long lda,
+                  int a_mn_major, const float* B, long long ldb, int b_mn_major, float* C,
+                  long long ldc, int epilogue, const float* bias, const float* aux,
+                  long long ld_aux, float* workspace, long long ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- K3 --
+ * Pooling over NHWC (pixel strides cs_in / cs_out).  mode 0 = max (first max in
+ * (dy,dx) window order, argmax = input pixel index iy*w + ix, as
+ * problems.py:213-216), mode 1 = average (Caffe semantics: divisor is the
+ * window clipped to the padded extent).  ceil_mode selects Caffe's output size
+ * rule.  Backward is a deterministic gather; if relu_mask_x != 0 the input
+ * gradient is also multiplied by (X > 0) (fused ReLU mask, problems.py:261). */
+int omni_pool_out_size(int n, int k, int stride, int pad, int ceil_mode);
+int omni_pool_fwd_nhwc_f32(int mode, const float* X, int b, int h, int w, int c, int cs_in,
+                           int k, int stride, int pad, int ceil_mode, float* Y, int cs_out,
+                           int32_t* argmax, void* stream);
+int omni_pool_bwd_nhwc_f32(int mode, const float* dY, int b, int h, int w, int c, int cs_in,
+                           int k, int stride, int pad, int ceil_mode, int cs_out,
+                           const int32_t* argmax, const float* X, int relu_mask_x, float* dX,
+                           void* stream);
+
+/* ---------------------------------------------------------------- K4 --
+ * Softmax cross-entropy over rows of logits (b x C, row stride ld):
+ * loss[0] = mean_i(lse_i - z_{i,y_i}) (problems.py:230-233); dlogits =
+ * (softmax - onehot) * scale (problems.py:246-248 with scale = 1/b).  One
+ * launch; deterministic.  dlogits may be NULL (loss only).                   */
+int omni_softmax_xent_f32(const float* logits, long long ld, const int32_t* labels, int b,
+                          int C, float* loss, float* dlogits, long long ldd, float scale,
+                          void* stream);
+
+/* ---------------------------------------------------------------- misc --
+ * ReLU forward/backward on a dense buffer (problems.py:211, :261; strict >). */
+int omni_relu_fwd_f32(const float* X, float* Y, long long n, void* stream);
+int omni_relu_bwd_f32(const float* dY, const float* Y, float* dX, long long n, void* stream);
+/* Bias gradient: db[j] = sum_i dY[i*ld + j], i < M (deterministic 2-pass).
+ * ws must hold omni_bias_grad_ws_elems(M, N) floats.                         */
+long long omni_bias_grad_ws_elems(int M, int N);
+int omni_bias_grad_f32(const float* dY, long long ld, int M, int N, float* db, float* ws,
+                       void* stream);
+/* K8 fused momentum SGD (sgd.py:92-101): V = mu*V - eta*(g + lam*w_read);
+ * W = W + V.  w_read may alias W (synchronous step).                         */
+int omni_sgd_momentum_f32(float* W, float* V, const float* g, const float* w_read, float eta,
+                          float mu, float lam, long long n, void* stream);
+/* K9 batch gather (problems.py:197-199): dst[i,:] = src[idx[i],:].            */
+int omni_gather_rows_f32(const float* src, long long row_elems, const int64_t* idx, int nidx,
+                         float* dst, void* stream);
+int omni_gather_i32(const int32_t* src, const int64_t* idx, int nidx, int32_t* dst,
+                    void* stream);
+/* Weight layout staging: OIHW (o,c,k,k) <-> tap-major (o, (kx*k+ky)*c + ch)
+ * rows of stride ld (pad columns zeroed).  inverse=0 reads W and writes Wt;
+ * inverse=1 reads Wt and writes W.                                           */
+int omni_conv_weight_to_tap_f32(float* W, int o, int c, int k, float* Wt, long long ld,
+                                int inverse, void* stream);
+/* Batched 2-D transpose: dst[bi][j*ldd + i] = src[bi][i*lds + j], i < rows,
+ * j < cols; batch strides in elements.  Used for NHWC <-> flattened CHW and
+ * for FC weight staging.                                                     */
+int omni_transpose_f32(const float* src, long long lds, long long src_bstride, int rows,
+                       int cols, float* dst, long long ldd, long long dst_bstride, int batch,
+                       void* stream);
+/* Fill / scale helpers. */
+int omni_fill_f32(float* X, float value, long long n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OMNI_H_ */

@@ -1,0 +1,123 @@
+"""ctypes binding of libomni.so (the C-ABI declared in include/omni.h).
+
+This is the only place Python touches the native library.  The product path
+fails loudly when the library is missing -- there is no CPU fallback.
+Status codes map onto the reference's error behaviour: argument errors raise
+``ValueError`` (as omnisim does, e.g. tensors.py:44-54), CUDA failures raise
+``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libomni.so")
+
+OMNI_OK = 0
+OMNI_EINVAL = -1
+OMNI_ECUDA = -2
+OMNI_EUNSUPPORTED = -3
+
+PREC_TF32 = 0
+PREC_3XTF32 = 1
+PREC_FP32_SIMT = 2
+PRECISIONS = {"tf32": PREC_TF32, "3xtf32": PREC_3XTF32, "fp32_simt": PREC_FP32_SIMT}
+
+EPI_STORE = 0
+EPI_BIAS = 1
+EPI_BIAS_RELU = 2
+EPI_ACCUM = 3
+EPI_MASK_AUX = 4
+EPI_RELU = 5
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_L = ctypes.c_longlong
+_F = ctypes.c_float
+
+# name -> (restype, argtypes); mirrors include/omni.h one to one.
+SIGNATURES: dict[str, tuple] = {
+    "omni_last_error": (ctypes.c_char_p, []),
+    "omni_version": (_I, []),
+    "omni_device_sm_count": (_I, [_I]),
+    "omni_lower_nchw_f32": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P]),
+    "omni_lower_nchw_f64": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P]),
+    "omni_lower_nhwc_f32": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P]),
+    "omni_lift_nchw_f32": (_I, [_P, _L, _I, _I, _I, _P, _P]),
+    "omni_lift_nchw_f64": (_I, [_P, _L, _I, _I, _I, _P, _P]),
+    "omni_col2im_nhwc_f32": (_I, [_P, _L, _I, _I, _I, _I, _I, _I, _I, _P, _P]),
+    "omni_gemm_plan": (_L, [_I, _I, _I, _I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
+    "omni_gemm_f32": (
+        _I,
+        [_I, _I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _P, _P, _L, _P, _L, _P],
+    ),
+    "omni_pool_out_size": (_I, [_I, _I, _I, _I, _I]),
+    "omni_pool_fwd_nhwc_f32": (_I, [_I, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
+    "omni_pool_bwd_nhwc_f32": (
+        _I,
+        [_I, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P],
+    ),
+    "omni_softmax_xent_f32": (_I, [_P, _L, _P, _I, _I, _P, _P, _L, _F, _P]),
+    "omni_relu_fwd_f32": (_I, [_P, _P, _L, _P]),
+    "omni_relu_bwd_f32": (_I, [_P, _P, _P, _L, _P]),
+    "omni_bias_grad_ws_elems": (_L, [_I, _I]),
+    "omni_bias_grad_f32": (_I, [_P, _L, _I, _I, _P, _P, _P]),
+    "omni_sgd_momentum_f32": (_I, [_P, _P, _P, _P, _F, _F, _F, _L, _P]),
+    "omni_gather_rows_f32": (_I, [_P, _L, _P, _I, _P, _P]),
+    "omni_gather_i32": (_I, [_P, _P, _I, _P, _P]),
+    "omni_conv_weight_to_tap_f32": (_I, [_P, _I, _I, _I, _P, _L, _I, _P]),
+    "omni_transpose_f32": (_I, [_P, _L, _L, _I, _I, _P, _L, _L, _I, _P]),
+    "omni_fill_f32": (_I, [_P, _F, _L, _P]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load() -> ctypes.CDLL:
+    """Load libomni.so once; raise if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build(); "
+                "this framework has no CPU fallback"
+            )
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)
+
+
+def last_error() -> str:
+    msg = load().omni_last_error()
+    return msg.decode() if msg else ""
+
+
+def call(name: str, *args) -> int:
+    """Invoke an int-returning entry point and map a failure status to an exception."""
+    rc = getattr(load(), name)(*args)
+    if rc != OMNI_OK:
+        msg = last_error()
+        if rc == OMNI_EINVAL:
+            raise ValueError(msg)
+        raise RuntimeError(f"{name}: {msg} (status {rc})")
+    return rc
+
+
+def query(name: str, *args):
+    """Invoke a value-returning entry point (no status mapping)."""
+    return getattr(load(), name)(*args)

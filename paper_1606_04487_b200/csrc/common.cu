@@ -1,0 +1,65 @@
+// Status plumbing shared by every entry point of libomni.so.
+#include <stdarg.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace omni {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: launch failed: %s", what, cudaGetErrorString(e));
+    return OMNI_ECUDA;
+  }
+  return OMNI_OK;
+}
+
+static int g_sm_count[64];
+static std::once_flag g_sm_once[64];
+
+int sm_count_cached(int dev) {
+  if (dev < 0 || dev >= 64) return 148;
+  std::call_once(g_sm_once[dev], [dev]() {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    g_sm_count[dev] = v;
+  });
+  return g_sm_count[dev];
+}
+
+int grid_for(long long work_items, int threads) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  long long sms = sm_count_cached(dev);
+  long long want = ceil_div(work_items, threads);
+  long long cap = sms * 8;  // 8 resident 256-thread blocks per SM saturate HBM
+  if (want > cap) want = cap;
+  if (want < 1) want = 1;
+  return (int)want;
+}
+
+}  // namespace omni
+
+extern "C" {
+
+const char* omni_last_error(void) { return omni::g_last_error.c_str(); }
+
+int omni_version(void) { return 1; }
+
+int omni_device_sm_count(int device) { return omni::sm_count_cached(device); }
+
+}  // extern "C"

@@ -1,0 +1,407 @@
+// Bandwidth-bound kernels of the CNN cascade: pooling (K3), softmax
+// cross-entropy (K4), ReLU, bias gradient (K7), fused momentum SGD (K8) and
+// the batch gather (K9).  Every reduction is a fixed-order gather or a
+// two-pass tree so results are bit-reproducible run to run (no atomics).
+#include <math.h>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__host__ __device__ inline int pool_out(int n, int k, int s, int p, int ceil_mode) {
+  const int span = n + 2 * p - k;
+  int out = (ceil_mode ? (span + s - 1) / s : span / s) + 1;
+  // Caffe's rule: the last window must start inside the (left-padded) input.
+  if (p > 0 && (out - 1) * s >= n + p) --out;
+  return out;
+}
+
+// One thread per (img, oy, ox, ch).  Max: first maximum in (dy, dx) order,
+// argmax = iy*w + ix (problems.py:213-216).  Avg: Caffe divisor.
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) pool_fwd_kernel(
+    const float* __restrict__ X, int b, int h, int w, int c, int cs_in, int k, int s, int p,
+    int oh, int ow, float* __restrict__ Y, int cs_out, int32_t* __restrict__ argmax) {
+  const long long total = (long long)b * oh * ow * c;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long opix = idx / c;
+    const int ch = (int)(idx - opix * c);
+    const int img = (int)(opix / (oh * ow));
+    const int r = (int)(opix - (long long)img * oh * ow);
+    const int oy = r / ow, ox = r - (r / ow) * ow;
+    int hs = oy * s - p, ws = ox * s - p;
+    int he = min(hs + k, h + p), we = min(ws + k, w + p);
+    const int pool_size = (he - hs) * (we - ws);
+    hs = max(hs, 0);
+    ws = max(ws, 0);
+    he = min(he, h);
+    we = min(we, w);
+    const float* Xi = X + (long long)img * h * w * cs_in + ch;
+    if (MODE == 0) {
+      float best = Xi[((long long)hs * w + ws) * cs_in];
+      int arg = hs * w + ws;
+      for (int iy = hs; iy < he; ++iy)
+        for (int ix = ws; ix < we; ++ix) {
+          const float v = Xi[((long long)iy * w + ix) * cs_in];
+          if (v > best) {
+            best = v;
+            arg = iy * w + ix;
+          }
+        }
+      Y[opix * cs_out + ch] = best;
+      if (argmax) argmax[idx] = arg;
+    } else {
+      float acc = 0.f;
+      for (int iy = hs; iy < he; ++iy)
+        for (int ix = ws; ix < we; ++ix) acc += Xi[((long long)iy * w + ix) * cs_in];
+      Y[opix * cs_out + ch] = acc / (float)pool_size;
+    }
+  }
+}
+
+// Gather-form backward: each input pixel sums the output gradients of the
+// windows that contain it, in ascending (oy, ox) order.
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) pool_bwd_kernel(
+    const float* __restrict__ dY, int b, int h, int w, int c, int cs_in, int k, int s, int p,
+    int oh, int ow, int cs_out, const int32_t* __restrict__ argmax, const float* __restrict__ X,
+    int relu_mask_x, float* __restrict__ dX) {
+  const long long total = (long long)b * h * w * c;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long pix = idx / c;
+    const int ch = (int)(idx - pix * c);
+    const int img = (int)(pix / (h * w));
+    const int r = (int)(pix - (long long)img * h * w);
+    const int iy = r / w, ix = r - (r / w) * w;
+    const int oy0 = (iy + p < k) ? 0 : (iy + p - k) / s + 1;
+    const int oy1 = min((iy + p) / s + 1, oh);
+    const int ox0 = (ix + p < k) ? 0 : (ix + p - k) / s + 1;
+    const int ox1 = min((ix + p) / s + 1, ow);
+    const long long obase = (long long)img * oh * ow;
+    float acc = 0.f;
+    for (int oy = oy0; oy < oy1; ++oy)
+      for (int ox = ox0; ox < ox1; ++ox) {
+        const long long o = obase + (long long)oy * ow + ox;
+        if (MODE == 0) {
+          if (argmax[o * c + ch] == iy * w + ix) acc += dY[o * cs_out + ch];
+        } else {
+          int hs = oy * s - p, ws = ox * s - p;
+          const int he = min(hs + k, h + p), we = min(ws + k, w + p);
+          const int pool_size = (he - hs) * (we - ws);
+          acc += dY[o * cs_out + ch] / (float)pool_size;
+        }
+      }
+    if (relu_mask_x && !(X[pix * cs_in + ch] > 0.f)) acc = 0.f;
+    dX[pix * cs_in + ch] = acc;
+  }
+}
+
+// Softmax cross-entropy: one CTA of 32 warps; warp w owns rows w, w+32, ...
+// Row losses are summed per warp in row order, then across warps in warp
+// order: a fixed reduction tree, so the loss is bit-reproducible.
+__global__ void __launch_bounds__(1024) softmax_xent_kernel(
+    const float* __restrict__ Z, long long ld, const int32_t* __restrict__ y, int b, int C,
+    float* __restrict__ loss, float* __restrict__ dZ, long long ldd, float scale) {
+  __shared__ float warp_loss[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float my_loss = 0.f;
+  for (int row = warp; row < b; row += 32) {
+    const float* z = Z + (long long)row * ld;
+    float mx = -INFINITY;
+    for (int j = lane; j < C; j += 32) mx = fmaxf(mx, z[j]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+    for (int j = lane; j < C; j += 32) sum += expf(z[j] - mx);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const int label = y[row];
+    if (lane == 0) my_loss += (logf(sum) + mx) - z[label];
+    if (dZ) {
+      const float inv = 1.f / sum;
+      float* d = dZ + (long long)row * ldd;
+      for (int j = lane; j < C; j += 32) {
+        float pj = expf(z[j] - mx) * inv;
+        if (j == label) pj -= 1.f;
+        d[j] = pj * scale;
+      }
+    }
+  }
+  if (lane == 0) warp_loss[warp] = my_loss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float tot = 0.f;
+    for (int i = 0; i < 32; ++i) tot += warp_loss[i];
+    loss[0] = tot / (float)b;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) relu_fwd_kernel(const float* __restrict__ X,
+                                                             float* __restrict__ Y, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    Y[i] = fmaxf(X[i], 0.f);
+}
+
+__global__ void __launch_bounds__(kThreads) relu_bwd_kernel(const float* __restrict__ dY,
+                                                             const float* __restrict__ Y,
+                                                             float* __restrict__ dX, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dX[i] = Y[i] > 0.f ? dY[i] : 0.f;
+}
+
+// Bias gradient pass 1: block (g, cb) sums rows [g*rpb, (g+1)*rpb) of columns
+// [cb*32, cb*32+32); 8 row-lanes per column, combined in lane order.
+__global__ void __launch_bounds__(256) bias_grad_pass1(const float* __restrict__ dY,
+                                                       long long ld, int M, int N, int rpb,
+                                                       float* __restrict__ ws) {
+  __shared__ float part[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int col = blockIdx.y * 32 + tx;
+  const long long r0 = (long long)blockIdx.x * rpb;
+  const long long r1 = min((long long)M, r0 + rpb);
+  float acc = 0.f;
+  if (col < N)
+    for (long long r = r0 + ty; r < r1; r += 8) acc += dY[r * ld + col];
+  part[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0 && col < N) {
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += part[i][tx];
+    ws[(long long)blockIdx.x * N + col] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) bias_grad_pass2(const float* __restrict__ ws, int G, int N,
+                                                       float* __restrict__ db) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= N) return;
+  float s = 0.f;
+  for (int g = 0; g < G; ++g) s += ws[(long long)g * N + col];
+  db[col] = s;
+}
+
+inline void bias_grad_geometry(int M, int* G, int* rpb) {
+  int r = (M + 295) / 296;  // about two row chunks per SM
+  if (r < 64) r = 64;
+  *rpb = r;
+  *G = (M + r - 1) / r;
+  if (*G < 1) *G = 1;
+}
+
+// V = mu*V - eta*(g + lam*w_read); W = W + V   (sgd.py:100-101), float4 body.
+__global__ void __launch_bounds__(kThreads) sgd_kernel(float* __restrict__ W, float* __restrict__ V,
+                                                       const float* __restrict__ g,
+                                                       const float* w_read, float eta, float mu,
+                                                       float lam, long long n) {
+  const long long n4 = n / 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 gv = reinterpret_cast<const float4*>(g)[i];
+    const float4 wr = reinterpret_cast<const float4*>(w_read)[i];
+    float4 v = reinterpret_cast<float4*>(V)[i];
+    float4 w = reinterpret_cast<float4*>(W)[i];
+    v.x = mu * v.x - eta * (gv.x + lam * wr.x);
+    v.y = mu * v.y - eta * (gv.y + lam * wr.y);
+    v.z = mu * v.z - eta * (gv.z + lam * wr.z);
+    v.w = mu * v.w - eta * (gv.w + lam * wr.w);
+    w.x += v.x; w.y += v.y; w.z += v.z; w.w += v.w;
+    reinterpret_cast<float4*>(V)[i] = v;
+    reinterpret_cast<float4*>(W)[i] = w;
+  }
+  for (long long i = n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    const float v = mu * V[i] - eta * (g[i] + lam * w_read[i]);
+    V[i] = v;
+    W[i] = W[i] + v;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) sgd_kernel_scalar(float* W, float* V,
+                                                              const float* __restrict__ g,
+                                                              const float* w_read, float eta,
+                                                              float mu, float lam, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float v = mu * V[i] - eta * (g[i] + lam * w_read[i]);
+    V[i] = v;
+    W[i] = W[i] + v;
+  }
+}
+
+template <bool VEC4>
+__global__ void __launch_bounds__(kThreads) gather_rows_kernel(const float* __restrict__ src,
+                                                               long long row_elems,
+                                                               const int64_t* __restrict__ idx,
+                                                               int nidx, float* __restrict__ dst) {
+  const long long per = VEC4 ? row_elems / 4 : row_elems;
+  const long long total = per * nidx;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / per, j = t - (t / per) * per;
+    const long long srow = idx[i];
+    if (VEC4)
+      reinterpret_cast<float4*>(dst)[i * per + j] =
+          reinterpret_cast<const float4*>(src)[srow * per + j];
+    else
+      dst[i * per + j] = src[srow * per + j];
+  }
+}
+
+__global__ void gather_i32_kernel(const int32_t* __restrict__ src, const int64_t* __restrict__ idx,
+                                  int nidx, int32_t* __restrict__ dst) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nidx; i += gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
+__global__ void fill_kernel(float* X, float v, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    X[i] = v;
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int omni_pool_out_size(int n, int k, int stride, int pad, int ceil_mode) {
+  if (n < 1 || k < 1 || stride < 1 || pad < 0 || k > n + 2 * pad) return -1;
+  return pool_out(n, k, stride, pad, ceil_mode);
+}
+
+int omni_pool_fwd_nhwc_f32(int mode, const float* X, int b, int h, int w, int c, int cs_in, int k,
+                           int stride, int pad, int ceil_mode, float* Y, int cs_out,
+                           int32_t* argmax, void* stream) {
+  OMNI_REQUIRE(mode == 0 || mode == 1, "pool: mode must be 0 (max) or 1 (avg)");
+  OMNI_REQUIRE(b >= 0 && h >= 1 && w >= 1 && c >= 1 && k >= 1 && stride >= 1 && pad >= 0 &&
+                   pad < k && k <= h + 2 * pad && k <= w + 2 * pad && cs_in >= c && cs_out >= c,
+               "pool: bad geometry");
+  OMNI_REQUIRE(mode == 1 || argmax != nullptr, "pool: max mode needs an argmax buffer");
+  const int oh = pool_out(h, k, stride, pad, ceil_mode), ow = pool_out(w, k, stride, pad, ceil_mode);
+  const long long work = (long long)b * oh * ow * c;
+  if (work == 0) return OMNI_OK;
+  cudaStream_t st = omni::as_stream(stream);
+  if (mode == 0)
+    pool_fwd_kernel<0><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(
+        X, b, h, w, c, cs_in, k, stride, pad, oh, ow, Y, cs_out, argmax);
+  else
+    pool_fwd_kernel<1><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(
+        X, b, h, w, c, cs_in, k, stride, pad, oh, ow, Y, cs_out, argmax);
+  return omni::check_launch("pool_fwd");
+}
+
+int omni_pool_bwd_nhwc_f32(int mode, const float* dY, int b, int h, int w, int c, int cs_in, int k,
+                           int stride, int pad, int ceil_mode, int cs_out, const int32_t* argmax,
+                           const float* X, int relu_mask_x, float* dX, void* stream) {
+  OMNI_REQUIRE(mode == 0 || mode == 1, "pool: mode must be 0 (max) or 1 (avg)");
+  OMNI_REQUIRE(b >= 0 && h >= 1 && w >= 1 && c >= 1 && k >= 1 && stride >= 1 && pad >= 0 &&
+                   pad < k && cs_in >= c && cs_out >= c,
+               "pool: bad geometry");
+  OMNI_REQUIRE(mode == 1 || argmax != nullptr, "pool: max mode needs the forward argmax");
+  OMNI_REQUIRE(!relu_mask_x || X != nullptr, "pool: relu mask needs X");
+  const int oh = pool_out(h, k, stride, pad, ceil_mode), ow = pool_out(w, k, stride, pad, ceil_mode);
+  const long long work = (long long)b * h * w * c;
+  if (work == 0) return OMNI_OK;
+  cudaStream_t st = omni::as_stream(stream);
+  if (mode == 0)
+    pool_bwd_kernel<0><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(
+        dY, b, h, w, c, cs_in, k, stride, pad, oh, ow, cs_out, argmax, X, relu_mask_x, dX);
+  else
+    pool_bwd_kernel<1><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(
+        dY, b, h, w, c, cs_in, k, stride, pad, oh, ow, cs_out, argmax, X, relu_mask_x, dX);
+  return omni::check_launch("pool_bwd");
+}
+
+int omni_softmax_xent_f32(const float* logits, long long ld, const int32_t* labels, int b, int C,
+                          float* loss, float* dlogits, long long ldd, float scale, void* stream) {
+  OMNI_REQUIRE(b >= 1 && C >= 1 && ld >= C && (dlogits == nullptr || ldd >= C),
+               "softmax_xent: bad shape");
+  softmax_xent_kernel<<<1, 1024, 0, omni::as_stream(stream)>>>(logits, ld, labels, b, C, loss,
+                                                               dlogits, ldd, scale);
+  return omni::check_launch("softmax_xent");
+}
+
+int omni_relu_fwd_f32(const float* X, float* Y, long long n, void* stream) {
+  if (n <= 0) return OMNI_OK;
+  relu_fwd_kernel<<<omni::grid_for(n, kThreads), kThreads, 0, omni::as_stream(stream)>>>(X, Y, n);
+  return omni::check_launch("relu_fwd");
+}
+
+int omni_relu_bwd_f32(const float* dY, const float* Y, float* dX, long long n, void* stream) {
+  if (n <= 0) return OMNI_OK;
+  relu_bwd_kernel<<<omni::grid_for(n, kThreads), kThreads, 0, omni::as_stream(stream)>>>(dY, Y, dX,
+                                                                                       n);
+  return omni::check_launch("relu_bwd");
+}
+
+long long omni_bias_grad_ws_elems(int M, int N) {
+  int G, rpb;
+  bias_grad_geometry(M, &G, &rpb);
+  return (long long)G * N;
+}
+
+int omni_bias_grad_f32(const float* dY, long long ld, int M, int N, float* db, float* ws,
+                       void* stream) {
+  OMNI_REQUIRE(M >= 1 && N >= 1 && ld >= N, "bias_grad: bad shape");
+  int G, rpb;
+  bias_grad_geometry(M, &G, &rpb);
+  cudaStream_t st = omni::as_stream(stream);
+  bias_grad_pass1<<<dim3(G, (N + 31) / 32), 256, 0, st>>>(dY, ld, M, N, rpb, ws);
+  int rc = omni::check_launch("bias_grad_pass1");
+  if (rc) return rc;
+  bias_grad_pass2<<<(N + 255) / 256, 256, 0, st>>>(ws, G, N, db);
+  return omni::check_launch("bias_grad_pass2");
+}
+
+int omni_sgd_momentum_f32(float* W, float* V, const float* g, const float* w_read, float eta,
+                          float mu, float lam, long long n, void* stream) {
+  OMNI_REQUIRE(n >= 0, "sgd: negative length");
+  if (n == 0) return OMNI_OK;
+  cudaStream_t st = omni::as_stream(stream);
+  if (aligned16(W) && aligned16(V) && aligned16(g) && aligned16(w_read))
+    sgd_kernel<<<omni::grid_for((n + 3) / 4, kThreads), kThreads, 0, st>>>(W, V, g, w_read, eta,
+                                                                          mu, lam, n);
+  else
+    sgd_kernel_scalar<<<omni::grid_for(n, kThreads), kThreads, 0, st>>>(W, V, g, w_read, eta, mu,
+                                                                       lam, n);
+  return omni::check_launch("sgd_momentum");
+}
+
+int omni_gather_rows_f32(const float* src, long long row_elems, const int64_t* idx, int nidx,
+                         float* dst, void* stream) {
+  OMNI_REQUIRE(row_elems >= 1 && nidx >= 0, "gather: bad shape");
+  if (nidx == 0) return OMNI_OK;
+  cudaStream_t st = omni::as_stream(stream);
+  const bool v4 = (row_elems % 4 == 0) && aligned16(src) && aligned16(dst);
+  const long long work = (v4 ? row_elems / 4 : row_elems) * nidx;
+  if (v4)
+    gather_rows_kernel<true><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(src, row_elems,
+                                                                                 idx, nidx, dst);
+  else
+    gather_rows_kernel<false><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(src, row_elems,
+                                                                                  idx, nidx, dst);
+  return omni::check_launch("gather_rows");
+}
+
+int omni_gather_i32(const int32_t* src, const int64_t* idx, int nidx, int32_t* dst, void* stream) {
+  if (nidx <= 0) return OMNI_OK;
+  gather_i32_kernel<<<omni::grid_for(nidx, kThreads), kThreads, 0, omni::as_stream(stream)>>>(
+      src, idx, nidx, dst);
+  return omni::check_launch("gather_i32");
+}
+
+int omni_fill_f32(float* X, float value, long long n, void* stream) {
+  if (n <= 0) return OMNI_OK;
+  fill_kernel<<<omni::grid_for(n, kThreads), kThreads, 0, omni::as_stream(stream)>>>(X, value, n);
+  return omni::check_launch("fill");
+}
+
+}  // extern "C"

@@ -1,0 +1,674 @@
+// K2: the conv/FC contraction -- "one big GEMM per layer per batch"
+// (tensors.py:193-210) -- as a persistent, warp-specialised
+// tcgen05 kernel for sm_100a.
+//
+//   C[i,j] (op)= sum_r A(i,r) B(j,r)
+//
+// Pipeline per CTA (one CTA per SM, 128 x BN output tiles, BK = 32 fp32):
+//   warp 0      TMA producer: 128B-swizzled A/B stages into a STAGES-deep
+//               shared-memory ring (mbarrier full/empty pairs)
+//   warp 1      MMA issuer: one thread issues tcgen05.mma.kind::tf32
+//               (M=128, N=BN, K=8) into a double-buffered TMEM accumulator
+//   warp 2      TMEM allocator
+//   warps 4-7   epilogue: tcgen05.ld 32 lanes x 16 columns -> registers ->
+//               fused bias / ReLU / ReLU-mask / accumulate -> global
+//   warps 8-11  (3xTF32 only) split every stage into hi (tf32-exact, in place)
+//               and lo = x - hi copies so the MMA warp can issue
+//               hi*hi + lo*hi + hi*lo: ~fp32 accuracy from tf32 tensor cores
+//               with no extra HBM traffic.
+// Operands may be K-major or MN-major (the weight-gradient products reduce
+// over the long M = b*m^2 axis of both lowered operands, problems.py:263-267,
+// so both operands are MN-major there); tcgen05 supports MN-major for tf32.
+// Few-tile shapes (FC layers, weight gradients) use split-K into a caller
+// workspace followed by a fixed-order reduction (deterministic, no atomics).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BK = 32;  // fp32 elements per stage along K = one 128-byte swizzle row
+
+struct Params {
+  int M, N, K;
+  int m_tiles, n_tiles, k_tiles, splits, kt_per_split;
+  int raster_m_inner;
+  int epilogue;
+  int vec_ok;  // C row stride % 4 == 0 and C 16-byte aligned
+  float* C;
+  long long ldc;
+  long long split_stride;  // elements between split-K partial outputs
+  const float* bias;
+  const float* aux;
+  long long ld_aux;
+};
+
+template <int BN, bool SPLIT3>
+struct Layout {
+  static constexpr int A_BYTES = BM * BK * 4;
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGE_ALL = SPLIT3 ? 2 * STAGE : STAGE;
+  static constexpr int BUDGET = 220 * 1024;
+  static constexpr int STAGES = (BUDGET / STAGE_ALL) > 8 ? 8 : (BUDGET / STAGE_ALL);
+  static constexpr int BAR_OFF = STAGES * STAGE_ALL;
+  static constexpr int BYTES = BAR_OFF + 256 + 1024;  // barriers + 1 KiB alignment slack
+  static constexpr int TMEM_COLS = 2 * BN <= 32    ? 32
+                                   : 2 * BN <= 64  ? 64
+                                   : 2 * BN <= 128 ? 128
+                                   : 2 * BN <= 256 ? 256
+                                                   : 512;
+  static constexpr int ACC_STRIDE = TMEM_COLS / 2;
+  static constexpr int THREADS = SPLIT3 ? 384 : 256;
+  static_assert(STAGES >= 2, "need at least two stages");
+  static_assert(B_BYTES % 1024 == 0, "B tile must keep 1 KiB swizzle alignment");
+};
+
+// ------------------------------------------------------------------ PTX --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint32_t dst, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor (tcgen05 "smem descriptor"): start address,
+// leading/stride byte offsets (>>4), version 1 (sm_100), SWIZZLE_128B (2).
+//  K-major : rows of 128 B (32 tf32 along K), 8-row atoms 1024 B apart (SBO).
+//  MN-major: 128 B along MN per K row; MN atoms of 32 elements are a whole
+//            BK-row chunk apart (LBO = 32 rows * 128 B), 8-row K groups 1024 B.
+template <bool MN>
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+  const uint64_t lbo = MN ? (uint64_t)((BK * 128) >> 4) : 1ull;
+  const uint64_t sbo = 1024 >> 4;
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | (lbo << 16) | (sbo << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+
+// Instruction descriptor: D=f32, A=B=tf32, majors, N>>3, M>>4.
+template <int BN, bool A_MN, bool B_MN>
+__host__ __device__ constexpr uint32_t instr_desc() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
+         ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void decode_work(const Params& p, int w, int& mt, int& nt, int& sp) {
+  const int per = p.m_tiles * p.n_tiles;
+  sp = w / per;
+  const int r = w - sp * per;
+  if (p.raster_m_inner) {
+    nt = r / p.m_tiles;
+    mt = r - nt * p.m_tiles;
+  } else {
+    mt = r / p.n_tiles;
+    nt = r - mt * p.n_tiles;
+  }
+}
+
+__device__ __forceinline__ float epi_apply(int mode, float acc, const Params& p, int row, int col,
+                                           const float* Crow) {
+  switch (mode) {
+    case OMNI_EPI_BIAS: return acc + __ldg(p.bias + col);
+    case OMNI_EPI_BIAS_RELU: return fmaxf(acc + __ldg(p.bias + col), 0.f);
+    case OMNI_EPI_ACCUM: return Crow[col] + acc;
+    case OMNI_EPI_MASK_AUX: return __ldg(p.aux + (long long)row * p.ld_aux + col) > 0.f ? acc : 0.f;
+    case OMNI_EPI_RELU: return fmaxf(acc, 0.f);
+    default: return acc;
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, bool SPLIT3>
+__global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
+    gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB, const Params p) {
+  using L = Layout<BN, SPLIT3>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = sbase + L::BAR_OFF;
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (8 + s); };
+  auto conv_bar = [&](int s) { return bar0 + 8u * (16 + s); };
+  auto tfull_bar = [&](int a) { return bar0 + 8u * (24 + a); };
+  auto tempty_bar = [&](int a) { return bar0 + 8u * (26 + a); };
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::BAR_OFF + 8 * 28);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < L::STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+      if (SPLIT3) mbar_init(conv_bar(s), 128);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "n"(L::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int total = p.m_tiles * p.n_tiles * p.splits;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------- TMA producer --
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+        int mt, nt, sp;
+        decode_work(p, w, mt, nt, sp);
+        const int kt0 = sp * p.kt_per_split;
+        const int kt1 = min(p.k_tiles, kt0 + p.kt_per_split);
+        for (int kt = kt0; kt < kt1; ++kt) {
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          mbar_expect_tx(full_bar(stage), (uint32_t)L::STAGE);
+          const uint32_t a_dst = sbase + stage * L::STAGE_ALL;
+          const uint32_t b_dst = a_dst + L::A_BYTES;
+          const int kc = kt * BK;
+          if (!A_MN) {
+            tma_load_2d(&tmA, a_dst, full_bar(stage), kc, mt * BM);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 32; ++j)
+              tma_load_2d(&tmA, a_dst + j * (BK * 128), full_bar(stage), mt * BM + 32 * j, kc);
+          }
+          if (!B_MN) {
+            tma_load_2d(&tmB, b_dst, full_bar(stage), kc, nt * BN);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 32; ++j)
+              tma_load_2d(&tmB, b_dst + j * (BK * 128), full_bar(stage), nt * BN + 32 * j, kc);
+          }
+          if (++stage == L::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------ MMA issuer --
+      constexpr uint32_t idesc = instr_desc<BN, A_MN, B_MN>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+        int mt, nt, sp;
+        decode_work(p, w, mt, nt, sp);
+        const int kt0 = sp * p.kt_per_split;
+        const int kt1 = min(p.k_tiles, kt0 + p.kt_per_split);
+        mbar_wait(tempty_bar(acc), acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * L::ACC_STRIDE);
+        for (int kt = kt0; kt < kt1; ++kt) {
+          mbar_wait(SPLIT3 ? conv_bar(stage) : full_bar(stage), phase);
+          tc_fence_after();
+          const uint32_t a_addr = sbase + stage * L::STAGE_ALL;
+          const uint32_t b_addr = a_addr + L::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t a_off = A_MN ? kk * 1024u : kk * 32u;
+            const uint32_t b_off = B_MN ? kk * 1024u : kk * 32u;
+            const uint64_t ad = smem_desc<A_MN>(a_addr + a_off);
+            const uint64_t bd = smem_desc<B_MN>(b_addr + b_off);
+            tc_mma_tf32(d_tmem, ad, bd, idesc, (kt > kt0 || kk > 0) ? 1u : 0u);
+            if (SPLIT3) {
+              const uint64_t ad_lo = smem_desc<A_MN>(a_addr + L::STAGE + a_off);
+              const uint64_t bd_lo = smem_desc<B_MN>(b_addr + L::STAGE + b_off);
+              tc_mma_tf32(d_tmem, ad_lo, bd, idesc, 1u);
+              tc_mma_tf32(d_tmem, ad, bd_lo, idesc, 1u);
+            }
+          }
+          tc_commit(empty_bar(stage));  // frees the stage once these MMAs have read it
+          if (++stage == L::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(tfull_bar(acc));  // accumulator complete -> epilogue
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // -------------------------------------------------------- epilogue --
+    const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const int mode = p.splits > 1 ? OMNI_EPI_STORE : p.epilogue;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int mt, nt, sp;
+      decode_work(p, w, mt, nt, sp);
+      mbar_wait(tfull_bar(acc), acc_phase);
+      tc_fence_after();
+      const int row = mt * BM + ew * 32 + lane;
+      const uint32_t t_row =
+          tmem_base + (uint32_t)(acc * L::ACC_STRIDE) + ((uint32_t)(ew * 32) << 16);
+      float* Crow = p.C + (long long)sp * p.split_stride + (long long)row * p.ldc;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        const int col0 = nt * BN + c0;
+        if (col0 >= p.N) break;  // warp-uniform
+        uint32_t r[16];
+        tmem_ld16(t_row + (uint32_t)c0, r);
+        tmem_wait_ld();
+        if (row < p.M) {
+          if (p.vec_ok && col0 + 16 <= p.N && mode != OMNI_EPI_ACCUM && mode != OMNI_EPI_MASK_AUX) {
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              v[j] = epi_apply(mode, __uint_as_float(r[j]), p, row, col0 + j, Crow);
+            float4* dst = reinterpret_cast<float4*>(Crow + col0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int col = col0 + j;
+              if (col < p.N) Crow[col] = epi_apply(mode, __uint_as_float(r[j]), p, row, col, Crow);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty_bar(acc));
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else if (SPLIT3 && warp >= 8) {
+    // ------------------------------------------- 3xTF32 hi/lo converters --
+    const int t = threadIdx.x - 256;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int mt, nt, sp;
+      decode_work(p, w, mt, nt, sp);
+      const int kt0 = sp * p.kt_per_split;
+      const int kt1 = min(p.k_tiles, kt0 + p.kt_per_split);
+      for (int kt = kt0; kt < kt1; ++kt) {
+        mbar_wait(full_bar(stage), phase);
+        uint4* hi = reinterpret_cast<uint4*>(smem + stage * L::STAGE_ALL);
+        uint4* lo = reinterpret_cast<uint4*>(smem + stage * L::STAGE_ALL + L::STAGE);
+        for (int i = t; i < L::STAGE / 16; i += 128) {
+          const uint4 v = hi[i];
+          uint4 h, l;
+          h.x = v.x & 0xFFFFE000u; l.x = __float_as_uint(__uint_as_float(v.x) - __uint_as_float(h.x));
+          h.y = v.y & 0xFFFFE000u; l.y = __float_as_uint(__uint_as_float(v.y) - __uint_as_float(h.y));
+          h.z = v.z & 0xFFFFE000u; l.z = __float_as_uint(__uint_as_float(v.z) - __uint_as_float(h.z));
+          h.w = v.w & 0xFFFFE000u; l.w = __float_as_uint(__uint_as_float(v.w) - __uint_as_float(h.w));
+          hi[i] = h;
+          lo[i] = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(conv_bar(stage));
+        if (++stage == L::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(L::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// Split-K reduction: C[i,j] = epi(sum_s ws[s][i][j]) in ascending s.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int S,
+                                                            int M, int N, Params p) {
+  const long long total = (long long)M * N;
+  const long long MN = total;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / N), col = (int)(idx - (idx / N) * N);
+    float acc = 0.f;
+    for (int s = 0; s < S; ++s) acc += ws[(long long)s * MN + idx];
+    float* Crow = p.C + (long long)row * p.ldc;
+    Crow[col] = epi_apply(p.epilogue, acc, p, row, col, Crow);
+  }
+}
+
+// CUDA-core fp32 reference GEMM (OMNI_PREC_FP32_SIMT): 16x16 tiles through
+// shared memory.  Test reference only; never on the training path.
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(256) simt_gemm_kernel(const float* __restrict__ A, long long lda,
+                                                        const float* __restrict__ B, long long ldb,
+                                                        Params p) {
+  __shared__ float As[16][17], Bs[16][17];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int i = blockIdx.y * 16 + ty, j = blockIdx.x * 16 + tx;
+  float acc = 0.f;
+  for (int r0 = 0; r0 < p.K; r0 += 16) {
+    {
+      const int ii = blockIdx.y * 16 + ty, rr = r0 + tx;
+      As[ty][tx] = (ii < p.M && rr < p.K) ? (A_MN ? A[(long long)rr * lda + ii]
+                                                  : A[(long long)ii * lda + rr])
+                                          : 0.f;
+      const int jj = blockIdx.x * 16 + ty;
+      Bs[ty][tx] = (jj < p.N && rr < p.K) ? (B_MN ? B[(long long)rr * ldb + jj]
+                                                  : B[(long long)jj * ldb + rr])
+                                          : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) acc = fmaf(As[ty][r], Bs[tx][r], acc);
+    __syncthreads();
+  }
+  if (i < p.M && j < p.N) {
+    float* Crow = p.C + (long long)i * p.ldc;
+    Crow[j] = epi_apply(p.epilogue, acc, p, i, j, Crow);
+  }
+}
+
+// ------------------------------------------------------------ host side --
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+int make_tmap(CUtensorMap* map, const float* ptr, long long inner, long long outer, long long ld,
+              int box_inner, int box_outer) {
+  auto fn = encode_fn();
+  if (!fn) {
+    omni::set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+    return OMNI_ECUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    omni::set_error("cuTensorMapEncodeTiled failed (%d): inner=%lld outer=%lld ld=%lld box=%dx%d",
+                    (int)r, inner, outer, ld, box_inner, box_outer);
+    return OMNI_ECUDA;
+  }
+  return OMNI_OK;
+}
+
+struct Plan {
+  int bn, splits, kps, m_tiles, n_tiles, k_tiles, grid, raster_m_inner;
+};
+
+constexpr int kBNs[] = {32, 64, 96, 128, 192, 256};
+
+Plan make_plan(int M, int N, int K, int sms) {
+  Plan pl{};
+  if (N <= 256) {
+    for (int b : kBNs)
+      if (b >= N) {
+        pl.bn = b;
+        break;
+      }
+  } else {
+    long long best = -1;
+    for (int b : {256, 192, 128}) {
+      const long long padded = omni::ceil_div(N, b) * b;
+      if (best < 0 || padded < best) {
+        best = padded;
+        pl.bn = b;
+      }
+    }
+  }
+  pl.m_tiles = (int)omni::ceil_div(M, BM);
+  pl.n_tiles = (int)omni::ceil_div(N, pl.bn);
+  pl.k_tiles = (int)omni::ceil_div(K, BK);
+  const long long tiles = (long long)pl.m_tiles * pl.n_tiles;
+  int splits = 1;
+  if (tiles < sms && pl.k_tiles >= 8) {
+    splits = (int)(sms / tiles);
+    const int max_splits = pl.k_tiles / 4;  // keep >= 4 k-tiles per split
+    if (splits > max_splits) splits = max_splits;
+    if (splits < 1) splits = 1;
+  }
+  pl.kps = (int)omni::ceil_div(pl.k_tiles, splits);
+  pl.splits = (int)omni::ceil_div(pl.k_tiles, pl.kps);
+  const long long work = tiles * pl.splits;
+  pl.grid = (int)(work < sms ? work : sms);
+  pl.raster_m_inner = pl.m_tiles < pl.n_tiles;
+  return pl;
+}
+
+template <int BN, bool A_MN, bool B_MN, bool SPLIT3>
+int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, long long ldb,
+              const Params& p, cudaStream_t st) {
+  using L = Layout<BN, SPLIT3>;
+  CUtensorMap ta, tb;
+  int rc = A_MN ? make_tmap(&ta, A, p.M, p.K, lda, 32, BK) : make_tmap(&ta, A, p.K, p.M, lda, 32, BM);
+  if (rc) return rc;
+  rc = B_MN ? make_tmap(&tb, B, p.N, p.K, ldb, 32, BK) : make_tmap(&tb, B, p.K, p.N, ldb, 32, BN);
+  if (rc) return rc;
+  auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT3>;
+  OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
+  kern<<<pl.grid, L::THREADS, L::BYTES, st>>>(ta, tb, p);
+  return omni::check_launch("gemm_tf32");
+}
+
+template <bool A_MN, bool B_MN, bool SPLIT3>
+int dispatch_bn(const Plan& pl, const float* A, long long lda, const float* B, long long ldb,
+                const Params& p, cudaStream_t st) {
+  switch (pl.bn) {
+    case 32: return launch_tc<32, A_MN, B_MN, SPLIT3>(pl, A, lda, B, ldb, p, st);
+    case 64: return launch_tc<64, A_MN, B_MN, SPLIT3>(pl, A, lda, B, ldb, p, st);
+    case 96: return launch_tc<96, A_MN, B_MN, SPLIT3>(pl, A, lda, B, ldb, p, st);
+    case 128: return launch_tc<128, A_MN, B_MN, SPLIT3>(pl, A, lda, B, ldb, p, st);
+    case 192: return launch_tc<192, A_MN, B_MN, SPLIT3>(pl, A, lda, B, ldb, p, st);
+    case 256: return launch_tc<256, A_MN, B_MN, SPLIT3>(pl, A, lda, B, ldb, p, st);
+  }
+  omni::set_error("gemm: no kernel for BN=%d", pl.bn);
+  return OMNI_EUNSUPPORTED;
+}
+
+template <bool SPLIT3>
+int dispatch_major(const Plan& pl, int a_mn, int b_mn, const float* A, long long lda,
+                   const float* B, long long ldb, const Params& p, cudaStream_t st) {
+  if (!a_mn && !b_mn) return dispatch_bn<false, false, SPLIT3>(pl, A, lda, B, ldb, p, st);
+  if (!a_mn && b_mn) return dispatch_bn<false, true, SPLIT3>(pl, A, lda, B, ldb, p, st);
+  if (a_mn && !b_mn) return dispatch_bn<true, false, SPLIT3>(pl, A, lda, B, ldb, p, st);
+  return dispatch_bn<true, true, SPLIT3>(pl, A, lda, B, ldb, p, st);
+}
+
+}  // namespace gemm
+
+extern "C" {
+
+long long omni_gemm_plan(int precision, int M, int N, int K, int a_mn_major, int b_mn_major,
+                         int* splits, int* bn) {
+  (void)a_mn_major;
+  (void)b_mn_major;
+  if (M < 1 || N < 1 || K < 1) return -1;
+  if (precision == OMNI_PREC_FP32_SIMT) {
+    if (splits) *splits = 1;
+    if (bn) *bn = 16;
+    return 0;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const gemm::Plan pl = gemm::make_plan(M, N, K, omni::sm_count_cached(dev));
+  if (splits) *splits = pl.splits;
+  if (bn) *bn = pl.bn;
+  return pl.splits > 1 ? (long long)pl.splits * M * N * 4 : 0;
+}
+
+int omni_gemm_f32(int precision, int M, int N, int K, const float* A, long long lda,
+                  int a_mn_major, const float* B, long long ldb, int b_mn_major, float* C,
+                  long long ldc, int epilogue, const float* bias, const float* aux,
+                  long long ld_aux, float* workspace, long long ws_bytes, void* stream) {
+  OMNI_REQUIRE(M >= 1 && N >= 1 && K >= 1, "gemm: empty problem (M=%d N=%d K=%d)", M, N, K);
+  OMNI_REQUIRE(precision >= 0 && precision <= 2, "gemm: unknown precision %d", precision);
+  OMNI_REQUIRE(epilogue >= 0 && epilogue <= 5, "gemm: unknown epilogue %d", epilogue);
+  OMNI_REQUIRE(lda >= (a_mn_major ? M : K) && ldb >= (b_mn_major ? N : K) && ldc >= N,
+               "gemm: leading dimension too small (lda=%lld ldb=%lld ldc=%lld)", lda, ldb, ldc);
+  OMNI_REQUIRE(!(epilogue == OMNI_EPI_BIAS || epilogue == OMNI_EPI_BIAS_RELU) || bias,
+               "gemm: bias epilogue needs a bias vector");
+  OMNI_REQUIRE(epilogue != OMNI_EPI_MASK_AUX || (aux && ld_aux >= N),
+               "gemm: mask epilogue needs aux");
+  cudaStream_t st = omni::as_stream(stream);
+  gemm::Params p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.epilogue = epilogue;
+  p.bias = bias;
+  p.aux = aux;
+  p.ld_aux = ld_aux;
+  if (precision == OMNI_PREC_FP32_SIMT) {
+    p.C = C;
+    p.ldc = ldc;
+    dim3 grid((unsigned)omni::ceil_div(N, 16), (unsigned)omni::ceil_div(M, 16));
+    if (!a_mn_major && !b_mn_major)
+      gemm::simt_gemm_kernel<false, false><<<grid, 256, 0, st>>>(A, lda, B, ldb, p);
+    else if (!a_mn_major && b_mn_major)
+      gemm::simt_gemm_kernel<false, true><<<grid, 256, 0, st>>>(A, lda, B, ldb, p);
+    else if (a_mn_major && !b_mn_major)
+      gemm::simt_gemm_kernel<true, false><<<grid, 256, 0, st>>>(A, lda, B, ldb, p);
+    else
+      gemm::simt_gemm_kernel<true, true><<<grid, 256, 0, st>>>(A, lda, B, ldb, p);
+    return omni::check_launch("gemm_simt");
+  }
+  OMNI_REQUIRE(lda % 4 == 0 && ldb % 4 == 0,
+               "gemm: lda/ldb must be multiples of 4 for TMA (lda=%lld ldb=%lld)", lda, ldb);
+  OMNI_REQUIRE(((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0,
+               "gemm: A and B must be 16-byte aligned for TMA");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const gemm::Plan pl = gemm::make_plan(M, N, K, omni::sm_count_cached(dev));
+  p.m_tiles = pl.m_tiles;
+  p.n_tiles = pl.n_tiles;
+  p.k_tiles = pl.k_tiles;
+  p.splits = pl.splits;
+  p.kt_per_split = pl.kps;
+  p.raster_m_inner = pl.raster_m_inner;
+  if (pl.splits > 1) {
+    const long long need = (long long)pl.splits * M * N * 4;
+    OMNI_REQUIRE(workspace && ws_bytes >= need,
+                 "gemm: split-K workspace of %lld bytes required (got %lld)", need, ws_bytes);
+    OMNI_REQUIRE(((uintptr_t)workspace & 15) == 0, "gemm: workspace must be 16-byte aligned");
+    p.C = workspace;
+    p.ldc = N;
+    p.split_stride = (long long)M * N;
+    p.vec_ok = (N % 4 == 0);
+  } else {
+    p.C = C;
+    p.ldc = ldc;
+    p.split_stride = 0;
+    p.vec_ok = (ldc % 4 == 0) && (((uintptr_t)C & 15) == 0);
+  }
+  const int b_mn = b_mn_major ? 1 : 0;
+  int rc = precision == OMNI_PREC_3XTF32
+               ? gemm::dispatch_major<true>(pl, a_mn_major, b_mn, A, lda, B, ldb, p, st)
+               : gemm::dispatch_major<false>(pl, a_mn_major, b_mn, A, lda, B, ldb, p, st);
+  if (rc) return rc;
+  if (pl.splits > 1) {
+    gemm::Params q = p;
+    q.C = C;
+    q.ldc = ldc;
+    gemm::splitk_reduce_kernel<<<omni::grid_for((long long)M * N, 256), 256, 0, st>>>(
+        workspace, pl.splits, M, N, q);
+    rc = omni::check_launch("splitk_reduce");
+  }
+  return rc;
+}
+
+}  // extern "C"

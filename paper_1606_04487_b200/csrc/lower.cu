@@ -1,0 +1,353 @@
+// K1 batched lowering (im2col over the whole mini-batch), lifting, the col2im
+// adjoint, weight-layout staging and the batched transpose.
+//
+// All of these are pure data movement: they are HBM-bound and written so that
+// consecutive threads produce consecutive output addresses (coalesced stores,
+// 16-byte vectors when the row stride allows); the gathered reads hit L1/L2
+// because every input element is re-read up to k*k/s^2 times in a short window.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// Reference column order (tensors.py:167-168): col = (ch*k + kx)*k + ky,
+// row = img*m^2 + x*m + y, value = D[start+img, ch, x*s+kx-p, y*s+ky-p] or 0.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(kThreads) lower_nchw_kernel(
+    const T* __restrict__ D, int c, int n, int k, int s, int p, int m, int start,
+    long long rows, int K, long long ld, T* __restrict__ Dhat) {
+  const long long cols_v = ld / VEC;
+  const long long total = rows * cols_v;
+  const int mm = m * m, kk = k * k;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long row = idx / cols_v;
+    const int col0 = (int)(idx - row * cols_v) * VEC;
+    const int img = (int)(row / mm);
+    const int rem = (int)(row - (long long)img * mm);
+    const int x = rem / m, y = rem - (rem / m) * m;
+    const T* Dimg = D + (long long)(start + img) * c * n * n;
+    T v[VEC];
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      const int col = col0 + j;
+      T val = T(0);
+      if (col < K) {
+        const int ch = col / kk;
+        const int t = col - ch * kk;
+        const int kx = t / k, ky = t - (t / k) * k;
+        const int ix = x * s + kx - p, iy = y * s + ky - p;
+        if ((unsigned)ix < (unsigned)n && (unsigned)iy < (unsigned)n)
+          val = __ldg(Dimg + ((long long)ch * n + ix) * n + iy);
+      }
+      v[j] = val;
+    }
+    T* out = Dhat + row * ld + col0;
+    if constexpr (VEC == 4 && sizeof(T) == 4) {
+      *reinterpret_cast<float4*>(out) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) out[j] = v[j];
+    }
+  }
+}
+
+// Tap-major lowering from NHWC (pixel stride cs): col = (kx*k + ky)*c + ch.
+// VEC4: c, cs, ld all multiples of 4, so one float4 load feeds one float4 store.
+template <bool VEC4>
+__global__ void __launch_bounds__(kThreads) lower_nhwc_kernel(
+    const float* __restrict__ X, int n, int c, int cs, int k, int s, int p, int m,
+    long long rows, int K, long long ld, float* __restrict__ Dhat) {
+  const long long cols_v = ld / 4;
+  const long long total = rows * cols_v;
+  const int mm = m * m;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long row = idx / cols_v;
+    const int col0 = (int)(idx - row * cols_v) * 4;
+    const int img = (int)(row / mm);
+    const int rem = (int)(row - (long long)img * mm);
+    const int x = rem / m, y = rem - (rem / m) * m;
+    const float* Ximg = X + (long long)img * n * n * cs;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (VEC4) {
+      if (col0 < K) {
+        const int tap = col0 / c;
+        const int ch = col0 - tap * c;
+        const int kx = tap / k, ky = tap - (tap / k) * k;
+        const int ix = x * s + kx - p, iy = y * s + ky - p;
+        if ((unsigned)ix < (unsigned)n && (unsigned)iy < (unsigned)n)
+          v = __ldg(reinterpret_cast<const float4*>(Ximg + ((long long)ix * n + iy) * cs + ch));
+      }
+    } else {
+      float t4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = col0 + j;
+        float val = 0.f;
+        if (col < K) {
+          const int tap = col / c;
+          const int ch = col - tap * c;
+          const int kx = tap / k, ky = tap - (tap / k) * k;
+          const int ix = x * s + kx - p, iy = y * s + ky - p;
+          if ((unsigned)ix < (unsigned)n && (unsigned)iy < (unsigned)n)
+            val = __ldg(Ximg + ((long long)ix * n + iy) * cs + ch);
+        }
+        t4[j] = val;
+      }
+      v = make_float4(t4[0], t4[1], t4[2], t4[3]);
+    }
+    *reinterpret_cast<float4*>(Dhat + row * ld + col0) = v;
+  }
+}
+
+// Adjoint of lower_nhwc: dX[img, ix, iy, ch] = sum over (kx, ky) with
+// x = (ix+p-kx)/s, y = (iy+p-ky)/s integral and in [0, m) of
+// dDhat[(img*m^2 + x*m + y)*ld + (kx*k + ky)*c + ch].  Fixed (kx, ky) order:
+// deterministic, no atomics.
+template <bool VEC4>
+__global__ void __launch_bounds__(kThreads) col2im_nhwc_kernel(
+    const float* __restrict__ dD, long long ld, int b, int n, int c, int cs, int k, int s, int p,
+    int m, float* __restrict__ dX) {
+  const int cv = VEC4 ? c / 4 : c;
+  const long long total = (long long)b * n * n * cv;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long pix = idx / cv;
+    const int chv = (int)(idx - pix * cv);
+    const int ch = VEC4 ? chv * 4 : chv;
+    const int img = (int)(pix / (n * n));
+    const int r = (int)(pix - (long long)img * n * n);
+    const int ix = r / n, iy = r - (r / n) * n;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int kx = 0; kx < k; ++kx) {
+      const int tx = ix + p - kx;
+      if (tx < 0) break;
+      if (tx % s) continue;
+      const int x = tx / s;
+      if (x >= m) continue;
+      for (int ky = 0; ky < k; ++ky) {
+        const int ty = iy + p - ky;
+        if (ty < 0) break;
+        if (ty % s) continue;
+        const int y = ty / s;
+        if (y >= m) continue;
+        const float* src =
+            dD + ((long long)img * m * m + (long long)x * m + y) * ld + (kx * k + ky) * c + ch;
+        if constexpr (VEC4) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(src));
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        } else {
+          acc.x += __ldg(src);
+        }
+      }
+    }
+    float* dst = dX + pix * cs + ch;
+    if constexpr (VEC4) *reinterpret_cast<float4*>(dst) = acc;
+    else *dst = acc.x;
+  }
+}
+
+// OIHW (o, c, k, k) <-> tap-major rows Wt[o*ld + (kx*k+ky)*c + ch].
+__global__ void __launch_bounds__(kThreads) weight_to_tap_kernel(
+    const float* __restrict__ W, int o, int c, int k, float* __restrict__ Wt, long long ld) {
+  const long long total = (long long)o * ld;
+  const int K = c * k * k;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int oo = (int)(idx / ld);
+    const int col = (int)(idx - (long long)oo * ld);
+    float v = 0.f;
+    if (col < K) {
+      const int tap = col / c, ch = col - (col / c) * c;
+      const int kx = tap / k, ky = tap - (tap / k) * k;
+      v = W[(((long long)oo * c + ch) * k + kx) * k + ky];
+    }
+    Wt[idx] = v;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) weight_from_tap_kernel(
+    const float* __restrict__ Wt, int o, int c, int k, float* __restrict__ W, long long ld) {
+  const long long total = (long long)o * c * k * k;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long r = idx;
+    const int ky = (int)(r % k); r /= k;
+    const int kx = (int)(r % k); r /= k;
+    const int ch = (int)(r % c); r /= c;
+    const int oo = (int)r;
+    W[idx] = Wt[(long long)oo * ld + (kx * k + ky) * c + ch];
+  }
+}
+
+// Batched tiled transpose through shared memory (32x33 tile: no bank conflicts).
+template <typename T>
+__global__ void __launch_bounds__(256) transpose_kernel(
+    const T* __restrict__ src, long long lds, long long sb, int rows, int cols,
+    T* __restrict__ dst, long long ldd, long long db, int batch) {
+  __shared__ T tile[32][33];
+  const int tiles_c = (cols + 31) / 32;
+  const int tr = blockIdx.x / tiles_c, tc = blockIdx.x - (blockIdx.x / tiles_c) * tiles_c;
+  for (int bi = blockIdx.y; bi < batch; bi += gridDim.y) {
+    const T* S = src + (long long)bi * sb;
+    T* Dd = dst + (long long)bi * db;
+    const int r0 = tr * 32, c0 = tc * 32;
+    for (int j = threadIdx.y; j < 32; j += 8) {
+      const int r = r0 + j, cc = c0 + threadIdx.x;
+      if (r < rows && cc < cols) tile[j][threadIdx.x] = S[(long long)r * lds + cc];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += 8) {
+      const int cc = c0 + j, r = r0 + threadIdx.x;
+      if (r < rows && cc < cols) Dd[(long long)cc * ldd + r] = tile[threadIdx.x][j];
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+int launch_transpose(const T* src, long long lds, long long sb, int rows, int cols, T* dst,
+                     long long ldd, long long db, int batch, cudaStream_t st) {
+  if (rows == 0 || cols == 0 || batch == 0) return OMNI_OK;
+  const long long tiles = omni::ceil_div(rows, 32) * omni::ceil_div(cols, 32);
+  OMNI_REQUIRE(tiles < (1LL << 31), "transpose: too many tiles");
+  dim3 grid((unsigned)tiles, (unsigned)(batch < 65535 ? batch : 65535));
+  transpose_kernel<T><<<grid, dim3(32, 8), 0, st>>>(src, lds, sb, rows, cols, dst, ldd, db,
+                                                    batch);
+  return omni::check_launch("transpose");
+}
+
+int check_conv_geom(int b, int c, int n, int k, int stride, int pad, int* m) {
+  OMNI_REQUIRE(b >= 0 && c >= 1 && n >= 1 && k >= 1 && stride >= 1 && pad >= 0,
+               "n, k, d_in, d_out, stride must be positive");
+  OMNI_REQUIRE(k <= n + 2 * pad, "kernel %d exceeds padded input %d", k, n + 2 * pad);
+  OMNI_REQUIRE((n + 2 * pad - k) % stride == 0,
+               "output size not integral: (n + 2*pad - k) = %d is not divisible by stride %d",
+               n + 2 * pad - k, stride);
+  *m = (n + 2 * pad - k) / stride + 1;
+  return OMNI_OK;
+}
+
+template <typename T>
+int lower_nchw(const T* D, int b, int c, int n, int k, int stride, int pad, int start, int b_p,
+               T* Dhat, long long ld, void* stream) {
+  int m = 0;
+  int rc = check_conv_geom(b, c, n, k, stride, pad, &m);
+  if (rc) return rc;
+  OMNI_REQUIRE(b_p >= 1 && b_p <= b, "b_p=%d out of range [1, %d]", b_p, b);
+  OMNI_REQUIRE(start >= 0 && start <= b - b_p, "start=%d leaves fewer than b_p=%d images", start,
+               b_p);
+  const int K = c * k * k;
+  OMNI_REQUIRE(ld >= K, "ld=%lld < lowered width %d", ld, K);
+  const long long rows = (long long)b_p * m * m;
+  cudaStream_t st = omni::as_stream(stream);
+  const bool vec = sizeof(T) == 4 && (ld % 4 == 0) && ((uintptr_t)Dhat % 16 == 0);
+  if (vec) {
+    lower_nchw_kernel<T, 4><<<omni::grid_for(rows * ld / 4, kThreads), kThreads, 0, st>>>(
+        D, c, n, k, stride, pad, m, start, rows, K, ld, Dhat);
+  } else {
+    lower_nchw_kernel<T, 1><<<omni::grid_for(rows * ld, kThreads), kThreads, 0, st>>>(
+        D, c, n, k, stride, pad, m, start, rows, K, ld, Dhat);
+  }
+  return omni::check_launch("lower_nchw");
+}
+
+}  // namespace
+
+extern "C" {
+
+int omni_lower_nchw_f32(const float* D, int b, int c, int n, int k, int stride, int pad,
+                        int start, int b_p, float* Dhat, long long ld, void* stream) {
+  return lower_nchw<float>(D, b, c, n, k, stride, pad, start, b_p, Dhat, ld, stream);
+}
+
+int omni_lower_nchw_f64(const double* D, int b, int c, int n, int k, int stride, int pad,
+                        int start, int b_p, double* Dhat, long long ld, void* stream) {
+  return lower_nchw<double>(D, b, c, n, k, stride, pad, start, b_p, Dhat, ld, stream);
+}
+
+int omni_lower_nhwc_f32(const float* X, int b, int n, int c, int cs, int k, int stride, int pad,
+                        float* Dhat, long long ld, void* stream) {
+  int m = 0;
+  int rc = check_conv_geom(b, c, n, k, stride, pad, &m);
+  if (rc) return rc;
+  const int K = c * k * k;
+  OMNI_REQUIRE(cs >= c, "pixel stride cs=%d < channels %d", cs, c);
+  OMNI_REQUIRE(ld >= K && ld % 4 == 0, "ld=%lld must be >= %d and a multiple of 4", ld, K);
+  OMNI_REQUIRE((uintptr_t)Dhat % 16 == 0, "Dhat must be 16-byte aligned");
+  if (b == 0) return OMNI_OK;
+  const long long rows = (long long)b * m * m;
+  cudaStream_t st = omni::as_stream(stream);
+  const bool v4 = (c % 4 == 0) && (cs % 4 == 0) && ((uintptr_t)X % 16 == 0);
+  const int grid = omni::grid_for(rows * ld / 4, kThreads);
+  if (v4)
+    lower_nhwc_kernel<true><<<grid, kThreads, 0, st>>>(X, n, c, cs, k, stride, pad, m, rows, K,
+                                                       ld, Dhat);
+  else
+    lower_nhwc_kernel<false><<<grid, kThreads, 0, st>>>(X, n, c, cs, k, stride, pad, m, rows, K,
+                                                        ld, Dhat);
+  return omni::check_launch("lower_nhwc");
+}
+
+int omni_lift_nchw_f32(const float* Rhat, long long ld, int b, int m, int d_out, float* R,
+                       void* stream) {
+  OMNI_REQUIRE(b >= 0 && m >= 1 && d_out >= 1 && ld >= d_out, "lift: bad shape");
+  // Per image, Rhat_img is (m^2 x d_out) with row stride ld; R_img is its transpose.
+  return launch_transpose<float>(Rhat, ld, (long long)m * m * ld, m * m, d_out, R,
+                                 (long long)m * m, (long long)d_out * m * m, b,
+                                 omni::as_stream(stream));
+}
+
+int omni_lift_nchw_f64(const double* Rhat, long long ld, int b, int m, int d_out, double* R,
+                       void* stream) {
+  OMNI_REQUIRE(b >= 0 && m >= 1 && d_out >= 1 && ld >= d_out, "lift: bad shape");
+  return launch_transpose<double>(Rhat, ld, (long long)m * m * ld, m * m, d_out, R,
+                                  (long long)m * m, (long long)d_out * m * m, b,
+                                  omni::as_stream(stream));
+}
+
+int omni_col2im_nhwc_f32(const float* dDhat, long long ld, int b, int n, int c, int cs, int k,
+                         int stride, int pad, float* dX, void* stream) {
+  int m = 0;
+  int rc = check_conv_geom(b, c, n, k, stride, pad, &m);
+  if (rc) return rc;
+  OMNI_REQUIRE(cs >= c && ld >= (long long)c * k * k, "col2im: bad strides");
+  if (b == 0) return OMNI_OK;
+  cudaStream_t st = omni::as_stream(stream);
+  const bool v4 = (c % 4 == 0) && (cs % 4 == 0) && (ld % 4 == 0) &&
+                  ((uintptr_t)dX % 16 == 0) && ((uintptr_t)dDhat % 16 == 0);
+  const long long work = (long long)b * n * n * (v4 ? c / 4 : c);
+  if (v4)
+    col2im_nhwc_kernel<true><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(
+        dDhat, ld, b, n, c, cs, k, stride, pad, m, dX);
+  else
+    col2im_nhwc_kernel<false><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(
+        dDhat, ld, b, n, c, cs, k, stride, pad, m, dX);
+  return omni::check_launch("col2im_nhwc");
+}
+
+int omni_conv_weight_to_tap_f32(float* W, int o, int c, int k, float* Wt, long long ld,
+                                int inverse, void* stream) {
+  OMNI_REQUIRE(o >= 1 && c >= 1 && k >= 1 && ld >= (long long)c * k * k, "weight staging: bad shape");
+  cudaStream_t st = omni::as_stream(stream);
+  if (!inverse) {
+    weight_to_tap_kernel<<<omni::grid_for((long long)o * ld, kThreads), kThreads, 0, st>>>(
+        W, o, c, k, Wt, ld);
+  } else {
+    weight_from_tap_kernel<<<omni::grid_for((long long)o * c * k * k, kThreads), kThreads, 0,
+                             st>>>(Wt, o, c, k, W, ld);
+  }
+  return omni::check_launch("conv_weight_to_tap");
+}
+
+int omni_transpose_f32(const float* src, long long lds, long long src_bstride, int rows, int cols,
+                       float* dst, long long ldd, long long dst_bstride, int batch, void* stream) {
+  OMNI_REQUIRE(rows >= 0 && cols >= 0 && batch >= 0 && lds >= cols && ldd >= rows,
+               "transpose: bad shape");
+  return launch_transpose<float>(src, lds, src_bstride, rows, cols, dst, ldd, dst_bstride, batch,
+                                 omni::as_stream(stream));
+}
+
+}  // extern "C"

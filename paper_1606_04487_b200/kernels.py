@@ -1,0 +1,222 @@
+"""Device-level wrappers: torch CUDA tensors in, libomni.so kernels out.
+
+PyTorch is only the allocator and the stream provider here; every op below
+is one (or two) launches of a hand-written sm_100a kernel through the C-ABI.
+Strides ("ld") are in elements, as in include/omni.h.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _abi
+from ._abi import call, query
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _require_cuda(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("libomni kernels take CUDA tensors")
+
+
+def round_up(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+# ----------------------------------------------------------------- K1 ----
+def lower_nchw(D: torch.Tensor, k: int, stride: int, pad: int, start: int, b_p: int,
+               ld: int | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Reference-order lowering of images [start, start+b_p) of NCHW ``D`` (tensors.py:164-181)."""
+    _require_cuda(D)
+    b, c, n, n2 = D.shape
+    if n != n2:
+        raise ValueError("lower expects square images")
+    m = (n + 2 * pad - k) // stride + 1
+    K = c * k * k
+    ld = K if ld is None else ld
+    if out is None:
+        out = torch.empty((b_p * m * m, ld), dtype=D.dtype, device=D.device)
+    D = D.contiguous()
+    name = "omni_lower_nchw_f64" if D.dtype == torch.float64 else "omni_lower_nchw_f32"
+    call(name, _ptr(D), b, c, n, k, stride, pad, start, b_p, _ptr(out), ld, _stream())
+    return out
+
+
+def lower_nhwc(X: torch.Tensor, c: int, k: int, stride: int, pad: int, ld: int,
+               out: torch.Tensor | None = None) -> torch.Tensor:
+    """Tap-major lowering of NHWC activations (pixel stride X.shape[3])."""
+    _require_cuda(X)
+    b, n, _, cs = X.shape
+    m = (n + 2 * pad - k) // stride + 1
+    if out is None:
+        out = torch.empty((b * m * m, ld), dtype=torch.float32, device=X.device)
+    call("omni_lower_nhwc_f32", _ptr(X), b, n, c, cs, k, stride, pad, _ptr(out), ld, _stream())
+    return out
+
+
+def lift_nchw(Rhat: torch.Tensor, b: int, m: int, d_out: int) -> torch.Tensor:
+    """(b*m^2, d_out) GEMM output -> NCHW tensor (tensors.py:213-219)."""
+    _require_cuda(Rhat)
+    out = torch.empty((b, d_out, m, m), dtype=Rhat.dtype, device=Rhat.device)
+    name = "omni_lift_nchw_f64" if Rhat.dtype == torch.float64 else "omni_lift_nchw_f32"
+    call(name, _ptr(Rhat), Rhat.stride(0), b, m, d_out, _ptr(out), _stream())
+    return out
+
+
+def col2im_nhwc(dDhat: torch.Tensor, ld: int, b: int, n: int, c: int, cs: int, k: int,
+                stride: int, pad: int, dX: torch.Tensor) -> torch.Tensor:
+    call("omni_col2im_nhwc_f32", _ptr(dDhat), ld, b, n, c, cs, k, stride, pad, _ptr(dX), _stream())
+    return dX
+
+
+# ----------------------------------------------------------------- K2 ----
+_ws_cache: dict[int, torch.Tensor] = {}
+
+
+def gemm_workspace_bytes(precision: int, M: int, N: int, K: int, a_mn: bool, b_mn: bool) -> int:
+    return int(query("omni_gemm_plan", precision, M, N, K, int(a_mn), int(b_mn), None, None))
+
+
+def gemm_plan(precision: int, M: int, N: int, K: int) -> tuple[int, int]:
+    import ctypes
+
+    s = ctypes.c_int(0)
+    bn = ctypes.c_int(0)
+    query("omni_gemm_plan", precision, M, N, K, 0, 0, ctypes.byref(s), ctypes.byref(bn))
+    return s.value, bn.value
+
+
+def _workspace(nbytes: int, device: torch.device) -> torch.Tensor | None:
+    if nbytes <= 0:
+        return None
+    key = device.index if device.index is not None else torch.cuda.current_device()
+    ws = _ws_cache.get(key)
+    if ws is None or ws.numel() * 4 < nbytes:
+        ws = torch.empty((nbytes + 3) // 4, dtype=torch.float32, device=device)
+        _ws_cache[key] = ws
+    return ws
+
+
+def gemm(M: int, N: int, K: int, A: torch.Tensor, lda: int, a_mn: bool, B: torch.Tensor,
+         ldb: int, b_mn: bool, C: torch.Tensor, ldc: int, *, precision: int = _abi.PREC_TF32,
+         epilogue: int = _abi.EPI_STORE, bias: torch.Tensor | None = None,
+         aux: torch.Tensor | None = None, ld_aux: int = 0,
+         workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """C[i,j] (op)= sum_r A(i,r) B(j,r) on tcgen05 (see include/omni.h for the operand maps)."""
+    _require_cuda(A, B, C)
+    need = gemm_workspace_bytes(precision, M, N, K, a_mn, b_mn)
+    if need > 0 and (workspace is None or workspace.numel() * 4 < need):
+        workspace = _workspace(need, C.device)
+    call("omni_gemm_f32", precision, M, N, K, _ptr(A), lda, int(a_mn), _ptr(B), ldb, int(b_mn),
+         _ptr(C), ldc, epilogue, _ptr(bias), _ptr(aux), ld_aux, _ptr(workspace),
+         0 if workspace is None else workspace.numel() * 4, _stream())
+    return C
+
+
+def matmul(A: torch.Tensor, B: torch.Tensor, precision: int = _abi.PREC_3XTF32) -> torch.Tensor:
+    """Plain (M x K) @ (K x N) product of dense fp32 CUDA matrices on tcgen05."""
+    M, K = A.shape
+    K2, N = B.shape
+    if K != K2:
+        raise ValueError(f"inner dimensions disagree: {tuple(A.shape)} x {tuple(B.shape)}")
+    lda = round_up(K, 4)
+    if A.stride(0) != lda or A.stride(1) != 1 or A.data_ptr() % 16:
+        Ap = torch.zeros((M, lda), dtype=torch.float32, device=A.device)
+        Ap[:, :K] = A
+    else:
+        Ap = A
+    ldb = round_up(N, 4)
+    if B.stride(0) != ldb or B.stride(1) != 1 or B.data_ptr() % 16:
+        Bp = torch.zeros((K, ldb), dtype=torch.float32, device=B.device)
+        Bp[:, :N] = B
+    else:
+        Bp = B
+    C = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    # A is K-major; B (K x N row-major) is MN-major for the B(j, r) operand.
+    return gemm(M, N, K, Ap, lda, False, Bp, ldb, True, C, N, precision=precision)
+
+
+# ----------------------------------------------------------------- K3 ----
+def pool_out_size(n: int, k: int, stride: int, pad: int, ceil_mode: bool) -> int:
+    v = query("omni_pool_out_size", n, k, stride, pad, int(ceil_mode))
+    if v < 1:
+        raise ValueError(f"invalid pooling geometry n={n} k={k} s={stride} p={pad}")
+    return int(v)
+
+
+def pool_fwd(mode: int, X: torch.Tensor, c: int, k: int, stride: int, pad: int, ceil_mode: bool,
+             Y: torch.Tensor, argmax: torch.Tensor | None) -> None:
+    b, h, w, cs_in = X.shape
+    call("omni_pool_fwd_nhwc_f32", mode, _ptr(X), b, h, w, c, cs_in, k, stride, pad,
+         int(ceil_mode), _ptr(Y), Y.shape[3], _ptr(argmax), _stream())
+
+
+def pool_bwd(mode: int, dY: torch.Tensor, X_shape, c: int, k: int, stride: int, pad: int,
+             ceil_mode: bool, argmax: torch.Tensor | None, X: torch.Tensor | None,
+             relu_mask: bool, dX: torch.Tensor) -> None:
+    b, h, w, cs_in = X_shape
+    call("omni_pool_bwd_nhwc_f32", mode, _ptr(dY), b, h, w, c, cs_in, k, stride, pad,
+         int(ceil_mode), dY.shape[3], _ptr(argmax), _ptr(X), int(relu_mask), _ptr(dX), _stream())
+
+
+# ----------------------------------------------------------------- K4 ----
+def softmax_xent(logits: torch.Tensor, ld: int, labels: torch.Tensor, b: int, C: int,
+                 loss: torch.Tensor, dlogits: torch.Tensor | None, ldd: int, scale: float) -> None:
+    call("omni_softmax_xent_f32", _ptr(logits), ld, _ptr(labels), b, C, _ptr(loss),
+         _ptr(dlogits), ldd, scale, _stream())
+
+
+# ---------------------------------------------------------------- misc ---
+def relu_fwd(X: torch.Tensor, Y: torch.Tensor) -> None:
+    call("omni_relu_fwd_f32", _ptr(X), _ptr(Y), X.numel(), _stream())
+
+
+def relu_bwd(dY: torch.Tensor, Y: torch.Tensor, dX: torch.Tensor) -> None:
+    call("omni_relu_bwd_f32", _ptr(dY), _ptr(Y), _ptr(dX), dY.numel(), _stream())
+
+
+def bias_grad_ws_elems(M: int, N: int) -> int:
+    return int(query("omni_bias_grad_ws_elems", M, N))
+
+
+def bias_grad(dY: torch.Tensor, ld: int, M: int, N: int, db: torch.Tensor,
+              ws: torch.Tensor) -> None:
+    call("omni_bias_grad_f32", _ptr(dY), ld, M, N, _ptr(db), _ptr(ws), _stream())
+
+
+def sgd_momentum(W: torch.Tensor, V: torch.Tensor, g: torch.Tensor, w_read: torch.Tensor,
+                 eta: float, mu: float, lam: float) -> None:
+    call("omni_sgd_momentum_f32", _ptr(W), _ptr(V), _ptr(g), _ptr(w_read), eta, mu, lam,
+         W.numel(), _stream())
+
+
+def gather_rows(src: torch.Tensor, idx: torch.Tensor, dst: torch.Tensor) -> None:
+    row = src[0].numel()
+    call("omni_gather_rows_f32", _ptr(src), row, _ptr(idx), idx.numel(), _ptr(dst), _stream())
+
+
+def gather_i32(src: torch.Tensor, idx: torch.Tensor, dst: torch.Tensor) -> None:
+    call("omni_gather_i32", _ptr(src), _ptr(idx), idx.numel(), _ptr(dst), _stream())
+
+
+def conv_weight_to_tap(W: torch.Tensor, o: int, c: int, k: int, Wt: torch.Tensor, ld: int,
+                       inverse: bool = False) -> None:
+    call("omni_conv_weight_to_tap_f32", _ptr(W), o, c, k, _ptr(Wt), ld, int(inverse), _stream())
+
+
+def transpose(src: torch.Tensor, lds: int, src_bstride: int, rows: int, cols: int,
+              dst: torch.Tensor, ldd: int, dst_bstride: int, batch: int = 1) -> None:
+    call("omni_transpose_f32", _ptr(src), lds, src_bstride, rows, cols, _ptr(dst), ldd,
+         dst_bstride, batch, _stream())
+
+
+def fill(X: torch.Tensor, value: float) -> None:
+    call("omni_fill_f32", _ptr(X), float(value), X.numel(), _stream())

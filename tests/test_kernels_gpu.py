@@ -1,0 +1,268 @@
+"""GPU unit tests of the individual sm_100a kernels through the C-ABI.
+
+Floating-point kernels are compared against a plain PyTorch fp64/fp32
+reference of the same op; data-movement kernels must be bit-exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_1606_04487_b200 import _abi, kernels as K  # noqa: E402
+
+DEV = "cuda"
+
+
+def rel_err(x, ref):
+    x = x.double()
+    ref = ref.double()
+    return float((x - ref).norm() / max(ref.norm().item(), 1e-300))
+
+
+def make_operand(rows_i, rows_r, mn_major, gen):
+    """Return (storage tensor, ld, logical (i x r) fp64 matrix)."""
+    logical = torch.randn(rows_i, rows_r, generator=gen, dtype=torch.float64)
+    if mn_major:
+        ld = K.round_up(rows_i, 4)
+        st = torch.zeros(rows_r, ld, dtype=torch.float32)
+        st[:, :rows_i] = logical.t().float()
+    else:
+        ld = K.round_up(rows_r, 4)
+        st = torch.zeros(rows_i, ld, dtype=torch.float32)
+        st[:, :rows_r] = logical.float()
+    return st.to(DEV), ld, logical.float().double()
+
+
+SHAPES = [
+    (128, 128, 32),
+    (300, 96, 363),
+    (257, 200, 100),
+    (1000, 256, 2400),
+    (64, 384, 1152),
+    (96, 363, 20000),  # few tiles: split-K
+    (4, 10, 9),
+]
+
+
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("prec", ["tf32", "3xtf32"])
+def test_gemm_vs_torch(a_mn, b_mn, shape, prec):
+    M, N, Kd = shape
+    gen = torch.Generator().manual_seed(M * 7 + N * 13 + Kd)
+    A, lda, Al = make_operand(M, Kd, a_mn, gen)
+    B, ldb, Bl = make_operand(N, Kd, b_mn, gen)
+    C = torch.full((M, N), float("nan"), device=DEV)
+    K.gemm(M, N, Kd, A, lda, a_mn, B, ldb, b_mn, C, N, precision=_abi.PRECISIONS[prec])
+    torch.cuda.synchronize()
+    ref = Al @ Bl.t()
+    err = rel_err(C.cpu(), ref)
+    tol = 3e-3 if prec == "tf32" else 2e-6
+    assert err < tol, (shape, a_mn, b_mn, prec, err)
+
+
+@pytest.mark.parametrize("epi", ["bias", "bias_relu", "relu", "mask", "accum"])
+def test_gemm_epilogues(epi):
+    M, N, Kd = 333, 130, 250
+    gen = torch.Generator().manual_seed(5)
+    A, lda, Al = make_operand(M, Kd, False, gen)
+    B, ldb, Bl = make_operand(N, Kd, False, gen)
+    bias = torch.randn(N, generator=gen).to(DEV)
+    aux = torch.randn(M, N, generator=gen).to(DEV)
+    C0 = torch.randn(M, N, generator=gen).to(DEV)
+    C = C0.clone()
+    code = {"bias": _abi.EPI_BIAS, "bias_relu": _abi.EPI_BIAS_RELU, "relu": _abi.EPI_RELU,
+            "mask": _abi.EPI_MASK_AUX, "accum": _abi.EPI_ACCUM}[epi]
+    K.gemm(M, N, Kd, A, lda, False, B, ldb, False, C, N, precision=_abi.PREC_3XTF32,
+           epilogue=code, bias=bias, aux=aux, ld_aux=N)
+    torch.cuda.synchronize()
+    acc = Al @ Bl.t()
+    b64 = bias.cpu().double()
+    ref = {"bias": acc + b64, "bias_relu": (acc + b64).clamp_min(0), "relu": acc.clamp_min(0),
+           "mask": acc * (aux.cpu().double() > 0), "accum": C0.cpu().double() + acc}[epi]
+    assert rel_err(C.cpu(), ref) < 2e-6
+
+
+def test_gemm_simt_reference():
+    M, N, Kd = 70, 50, 40
+    gen = torch.Generator().manual_seed(1)
+    A, lda, Al = make_operand(M, Kd, True, gen)
+    B, ldb, Bl = make_operand(N, Kd, False, gen)
+    C = torch.empty(M, N, device=DEV)
+    K.gemm(M, N, Kd, A, lda, True, B, ldb, False, C, N, precision=_abi.PREC_FP32_SIMT)
+    torch.cuda.synchronize()
+    assert rel_err(C.cpu(), Al @ Bl.t()) < 1e-6
+
+
+def test_gemm_bad_args_raise():
+    A = torch.zeros(8, 8, device=DEV)
+    with pytest.raises(ValueError):
+        K.gemm(8, 8, 8, A, 6, False, A, 8, False, A, 8)  # lda not a multiple of 4
+    with pytest.raises(ValueError):
+        K.gemm(0, 8, 8, A, 8, False, A, 8, False, A, 8)
+
+
+def ref_lower_np(D, k, s, p):
+    """Independent numpy lowering in the reference's (c, kx, ky) column order."""
+    b, c, n, _ = D.shape
+    m = (n + 2 * p - k) // s + 1
+    Dp = np.pad(D, ((0, 0), (0, 0), (p, p), (p, p)))
+    out = np.empty((b, m, m, c, k, k), D.dtype)
+    for kx in range(k):
+        for ky in range(k):
+            out[:, :, :, :, kx, ky] = Dp[:, :, kx:kx + s * (m - 1) + 1:s,
+                                         ky:ky + s * (m - 1) + 1:s].transpose(0, 2, 3, 1)
+    return out.reshape(b * m * m, c * k * k)
+
+
+@pytest.mark.parametrize("geom", [(2, 3, 9, 3, 1, 1), (3, 1, 8, 3, 1, 1), (2, 3, 27, 11, 4, 0),
+                                  (1, 5, 13, 5, 2, 2), (4, 2, 6, 1, 1, 0)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_lower_nchw_bit_exact(geom, dtype):
+    b, c, n, k, s, p = geom
+    rng = np.random.default_rng(0)
+    D = rng.standard_normal((b, c, n, n)).astype(np.float32).astype(np.float64)
+    Dt = torch.from_numpy(D).to(dtype).to(DEV)
+    got = K.lower_nchw(Dt, k, s, p, 0, b).cpu().numpy()
+    want = ref_lower_np(D, k, s, p).astype(got.dtype)
+    assert np.array_equal(got, want)
+    # padded ld: pad columns are zero
+    ld = K.round_up(c * k * k, 4) + 4
+    got2 = K.lower_nchw(Dt, k, s, p, 0, b, ld=ld).cpu().numpy()
+    assert np.array_equal(got2[:, : c * k * k], want) and not got2[:, c * k * k:].any()
+
+
+@pytest.mark.parametrize("geom", [(2, 3, 9, 3, 1, 1), (2, 8, 10, 3, 1, 1), (2, 3, 27, 11, 4, 0),
+                                  (1, 16, 13, 5, 2, 2)])
+def test_lower_nhwc_tap_major_and_col2im_adjoint(geom):
+    b, c, n, k, s, p = geom
+    rng = np.random.default_rng(1)
+    D = rng.standard_normal((b, c, n, n)).astype(np.float32)
+    cs = K.round_up(c, 4)
+    X = torch.zeros(b, n, n, cs)
+    X[..., :c] = torch.from_numpy(D).permute(0, 2, 3, 1)
+    Kc = c * k * k
+    ld = K.round_up(Kc, 4)
+    got = K.lower_nhwc(X.to(DEV), c, k, s, p, ld).cpu().numpy()
+    ref = ref_lower_np(D, k, s, p)  # (c, kx, ky) order
+    m = (n + 2 * p - k) // s + 1
+    ref_tap = ref.reshape(b * m * m, c, k * k).transpose(0, 2, 1).reshape(b * m * m, Kc)
+    assert np.array_equal(got[:, :Kc], ref_tap)
+    assert not got[:, Kc:].any()
+    # adjoint: <lower(X), G> == <X, col2im(G)>
+    G = torch.randn(b * m * m, ld, dtype=torch.float32)
+    G[:, Kc:] = 0
+    dX = torch.zeros(b, n, n, cs, device=DEV)
+    K.col2im_nhwc(G.to(DEV), ld, b, n, c, cs, k, s, p, dX)
+    lhs = float((torch.from_numpy(got).double() * G.double()).sum())
+    rhs = float((X.double() * dX.cpu().double()).sum())
+    assert abs(lhs - rhs) <= 1e-4 * max(1.0, abs(lhs))
+
+
+def test_lift_bit_exact():
+    b, m, d = 3, 5, 7
+    R = torch.randn(b * m * m, d, dtype=torch.float64)
+    got = K.lift_nchw(R.to(DEV), b, m, d).cpu()
+    want = R.reshape(b, m, m, d).permute(0, 3, 1, 2)
+    assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("geom", [(2, 8, 8, 3, 2, 2, 0, True), (2, 55, 55, 5, 3, 2, 0, True),
+                                  (3, 32, 32, 4, 3, 2, 0, True), (1, 7, 7, 4, 3, 2, 1, True)])
+def test_pool_fwd_bwd(mode, geom):
+    b, h, w, c, k, s, p, ceil_mode = geom
+    gen = torch.Generator().manual_seed(3)
+    X = torch.randn(b, h, w, c, generator=gen)
+    oh = K.pool_out_size(h, k, s, p, ceil_mode)
+    ow = K.pool_out_size(w, k, s, p, ceil_mode)
+    Y = torch.empty(b, oh, ow, c, device=DEV)
+    am = torch.empty(b * oh * ow * c, dtype=torch.int32, device=DEV)
+    K.pool_fwd(mode, X.to(DEV), c, k, s, p, ceil_mode, Y, am if mode == 0 else None)
+    # reference via explicit loops
+    Yr = torch.empty(b, oh, ow, c, dtype=torch.float64)
+    for oy in range(oh):
+        for ox in range(ow):
+            hs, ws = oy * s - p, ox * s - p
+            he, we = min(hs + k, h + p), min(ws + k, w + p)
+            size = (he - hs) * (we - ws)
+            hs, ws, he, we = max(hs, 0), max(ws, 0), min(he, h), min(we, w)
+            win = X[:, hs:he, ws:we, :].double()
+            Yr[:, oy, ox] = win.amax(dim=(1, 2)) if mode == 0 else win.sum(dim=(1, 2)) / size
+    assert torch.allclose(Y.cpu().double(), Yr, rtol=1e-6, atol=1e-6)
+    # backward vs autograd of the same reference
+    Xa = X.double().requires_grad_(True)
+    outs = []
+    for oy in range(oh):
+        row = []
+        for ox in range(ow):
+            hs, ws = oy * s - p, ox * s - p
+            he, we = min(hs + k, h + p), min(ws + k, w + p)
+            size = (he - hs) * (we - ws)
+            hs, ws, he, we = max(hs, 0), max(ws, 0), min(he, h), min(we, w)
+            win = Xa[:, hs:he, ws:we, :]
+            row.append(win.amax(dim=(1, 2)) if mode == 0 else win.sum(dim=(1, 2)) / size)
+        outs.append(torch.stack(row, 1))
+    Yg = torch.stack(outs, 1)
+    dY = torch.randn(b, oh, ow, c, generator=gen)
+    Yg.backward(dY.double())
+    dX = torch.empty(b, h, w, c, device=DEV)
+    K.pool_bwd(mode, dY.to(DEV), X.shape, c, k, s, p, ceil_mode, am if mode == 0 else None,
+               None, False, dX)
+    assert torch.allclose(dX.cpu().double(), Xa.grad, rtol=1e-5, atol=1e-5)
+
+
+def test_softmax_xent():
+    b, C = 37, 1000
+    gen = torch.Generator().manual_seed(2)
+    Z = torch.randn(b, C, generator=gen) * 3
+    y = torch.randint(0, C, (b,), generator=gen, dtype=torch.int32)
+    loss = torch.empty(1, device=DEV)
+    dZ = torch.empty(b, C, device=DEV)
+    K.softmax_xent(Z.to(DEV), C, y.to(DEV), b, C, loss, dZ, C, 1.0 / b)
+    Zd = Z.double().requires_grad_(True)
+    ref = torch.nn.functional.cross_entropy(Zd, y.long())
+    ref.backward()
+    assert abs(loss.item() - ref.item()) < 1e-5 * abs(ref.item())
+    assert rel_err(dZ.cpu(), Zd.grad) < 1e-5
+
+
+def test_bias_grad_sgd_gather_transpose():
+    gen = torch.Generator().manual_seed(4)
+    M, N = 10007, 96
+    dY = torch.randn(M, N, generator=gen)
+    db = torch.empty(N, device=DEV)
+    ws = torch.empty(K.bias_grad_ws_elems(M, N), device=DEV)
+    K.bias_grad(dY.to(DEV), N, M, N, db, ws)
+    assert rel_err(db.cpu(), dY.double().sum(0)) < 1e-6
+    n = 1001
+    W, V, g, wr = (torch.randn(n, generator=gen) for _ in range(4))
+    Wd, Vd = W.to(DEV), V.to(DEV)
+    K.sgd_momentum(Wd, Vd, g.to(DEV), wr.to(DEV), 0.1, 0.9, 0.01)
+    Vr = 0.9 * V.double() - 0.1 * (g.double() + 0.01 * wr.double())
+    assert rel_err(Vd.cpu(), Vr) < 1e-6 and rel_err(Wd.cpu(), W.double() + Vr) < 1e-6
+    src = torch.randn(50, 3, 5, 5, generator=gen)
+    idx = torch.tensor([3, 3, 49, 0, 7], dtype=torch.int64)
+    dst = torch.empty(5, 3, 5, 5, device=DEV)
+    K.gather_rows(src.to(DEV), idx.to(DEV), dst)
+    assert torch.equal(dst.cpu(), src[idx])
+    T = torch.randn(4, 33, 65, generator=gen)
+    out = torch.empty(4, 65, 33, device=DEV)
+    K.transpose(T.to(DEV), 65, 33 * 65, 33, 65, out, 33, 65 * 33, 4)
+    assert torch.equal(out.cpu(), T.transpose(1, 2))
+
+
+def test_conv_weight_tap_roundtrip():
+    o, c, k = 7, 3, 5
+    W = torch.randn(o, c, k, k)
+    ld = K.round_up(c * k * k, 4)
+    Wt = torch.empty(o, ld, device=DEV)
+    K.conv_weight_to_tap(W.to(DEV), o, c, k, Wt, ld)
+    ref = W.permute(0, 2, 3, 1).reshape(o, k * k * c)
+    assert torch.equal(Wt.cpu()[:, : c * k * k], ref)
+    back = torch.empty(o, c, k, k, device=DEV)
+    K.conv_weight_to_tap(back, o, c, k, Wt, ld, inverse=True)
+    assert torch.equal(back.cpu(), W)
