@@ -139,16 +139,20 @@ __device__ __forceinline__ void tmem_wait_ld() {
 }
 
 // Shared-memory matrix descriptor (tcgen05 "smem descriptor"): start address,
-// leading/stride byte offsets (>>4), version 1 (sm_100), SWIZZLE_128B (2).
-//  K-major : rows of 128 B (32 tf32 along K), 8-row atoms 1024 B apart (SBO).
-//  MN-major: 128 B along MN per K row; MN atoms of 32 elements are a whole
-//            BK-row chunk apart (LBO = 32 rows * 128 B), 8-row K groups 1024 B.
+// leading/stride byte offsets (>>4), version 1 (sm_100), layout type.
+//  K-major : SWIZZLE_128B (type 2, 16-byte atoms): rows of 128 B (32 tf32
+//            along K), 8-row atoms 1024 B apart (SBO).
+//  MN-major: tf32 only supports SWIZZLE_128B_BASE32B (type 1, 32-byte atoms,
+//            TMA mode 128B_ATOM_32B): 128 B along MN per K row; MN atoms of 32
+//            elements are a whole BK-row chunk apart (LBO = 32 rows * 128 B),
+//            4-row K groups 512 B apart (SBO).
 template <bool MN>
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
   const uint64_t lbo = MN ? (uint64_t)((BK * 128) >> 4) : 1ull;
-  const uint64_t sbo = 1024 >> 4;
+  const uint64_t sbo = MN ? (512 >> 4) : (1024 >> 4);
+  const uint64_t layout = MN ? 1ull : 2ull;
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | (lbo << 16) | (sbo << 32) | (1ull << 46) |
-         (2ull << 61);
+         (layout << 61);
 }
 
 // Instruction descriptor: D=f32, A=B=tf32, majors, N>>3, M>>4.
@@ -466,7 +470,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 int make_tmap(CUtensorMap* map, const float* ptr, long long inner, long long outer, long long ld,
-              int box_inner, int box_outer) {
+              int box_inner, int box_outer, bool mn_major) {
   auto fn = encode_fn();
   if (!fn) {
     omni::set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
@@ -477,7 +481,8 @@ int make_tmap(CUtensorMap* map, const float* ptr, long long inner, long long out
   cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     omni::set_error("cuTensorMapEncodeTiled failed (%d): inner=%lld outer=%lld ld=%lld box=%dx%d",
@@ -535,9 +540,11 @@ int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, lon
               const Params& p, cudaStream_t st) {
   using L = Layout<BN, SPLIT3>;
   CUtensorMap ta, tb;
-  int rc = A_MN ? make_tmap(&ta, A, p.M, p.K, lda, 32, BK) : make_tmap(&ta, A, p.K, p.M, lda, 32, BM);
+  int rc = A_MN ? make_tmap(&ta, A, p.M, p.K, lda, 32, BK, true)
+                : make_tmap(&ta, A, p.K, p.M, lda, 32, BM, false);
   if (rc) return rc;
-  rc = B_MN ? make_tmap(&tb, B, p.N, p.K, ldb, 32, BK) : make_tmap(&tb, B, p.K, p.N, ldb, 32, BN);
+  rc = B_MN ? make_tmap(&tb, B, p.N, p.K, ldb, 32, BK, true)
+            : make_tmap(&tb, B, p.K, p.N, ldb, 32, BN, false);
   if (rc) return rc;
   auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT3>;
   OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));

@@ -60,7 +60,8 @@ def test_gemm_vs_torch(a_mn, b_mn, shape, prec):
     torch.cuda.synchronize()
     ref = Al @ Bl.t()
     err = rel_err(C.cpu(), ref)
-    tol = 3e-3 if prec == "tf32" else 2e-6
+    # fp32 accumulation error grows like sqrt(K)
+    tol = 3e-3 if prec == "tf32" else 2e-6 * max(1.0, (Kd / 1000.0) ** 0.5)
     assert err < tol, (shape, a_mn, b_mn, prec, err)
 
 
