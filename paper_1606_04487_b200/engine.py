@@ -1,0 +1,372 @@
+"""GpuNet: one NetSpec compiled into a fixed sequence of sm_100a launches.
+
+This is the device-resident training step behind ``CNNProblem.grad`` and the
+g-group runtime: the reference's problems.py:206-269 cascade (forward through
+lowering + one GEMM per layer, softmax-CE, hand-written backward) and
+sgd.py:92-101 update, for any NetSpec.
+
+Layout in HBM (all fp32):
+  * activations NHWC, pixel stride cs = round_up(c, 4) (16-byte rows for TMA
+    and float4 kernels); FC activations (b, round_up(f, 4));
+  * lowered matrices Dhat (b*m^2, round_up(c*k*k, 4)) in tap-major column
+    order (kx*k + ky)*c + ch, kept from forward for the weight gradient;
+  * conv weights staged each step from the flat OIHW vector into tap-major
+    rows (the GEMM's K-major B operand); FC weights staged transposed
+    (out, in) so the forward product is K-major x K-major;
+  * the flat parameter / gradient vectors use the reference's packing
+    (problems.py:201-204 generalised in nets.py).
+
+Fusion: conv/FC + bias + ReLU in the GEMM epilogue; the ReLU mask of the
+backward pass is applied by whichever kernel produces the gradient (pool
+backward, FC dgrad epilogue) and only falls back to a separate pass after
+col2im.  Per-step launches are static, so the whole step can be captured in a
+CUDA graph (``capture``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _abi
+from . import kernels as K
+from .nets import NetSpec, pool_out
+
+ru4 = lambda x: K.round_up(int(x), 4)  # noqa: E731
+
+
+@dataclass
+class Act:
+    spatial: bool
+    c: int = 0        # channels (spatial) or features (flat)
+    n: int = 0        # spatial size
+    cs: int = 0       # pixel stride (spatial) or row stride (flat)
+    fused_relu: bool = False
+    value: torch.Tensor | None = None
+    grad: torch.Tensor | None = None
+
+    def shape(self, b):
+        return (b, self.n, self.n, self.cs) if self.spatial else (b, self.cs)
+
+
+@dataclass
+class Op:
+    kind: str
+    layer: object
+    inp: Act
+    out: Act
+    woff: int = -1
+    wsz: int = 0
+    boff: int = -1
+    relu: bool = False
+    first_param_layer: bool = False
+    # conv
+    c_in: int = 0
+    k: int = 0
+    s: int = 1
+    p: int = 0
+    m: int = 0
+    Kc: int = 0
+    ldK: int = 0
+    dhat: torch.Tensor | None = None
+    wstage: torch.Tensor | None = None
+    dwstage: torch.Tensor | None = None
+    # pool
+    argmax: torch.Tensor | None = None
+    # fc
+    f_in: int = 0
+    flat: Act | None = None
+    extra: dict = field(default_factory=dict)
+
+
+class GpuNet:
+    """Device buffers + launch sequence for one NetSpec at a fixed max batch."""
+
+    def __init__(self, net: NetSpec, batch: int, device=None, precision: str = "tf32"):
+        if precision not in ("tf32", "3xtf32"):
+            raise ValueError("precision must be 'tf32' or '3xtf32'")
+        self.net = net
+        self.b = int(batch)
+        self.device = torch.device(device if device is not None else "cuda")
+        self.prec = _abi.PRECISIONS[precision]
+        self.precision = precision
+        _abi.load()  # fail loudly now if the native library is missing
+        z = lambda *shape, dtype=torch.float32: torch.zeros(shape, dtype=dtype, device=self.device)  # noqa: E731
+        self._zeros = z
+        geom = net.geometry()
+        c0 = net.in_channels
+        self.input = Act(True, c0, net.in_size, c0)
+        self.input.value = z(self.b, net.in_size, net.in_size, c0)
+        self.labels = z(self.b, dtype=torch.int32)
+        self.ops: list[Op] = []
+        cur = self.input
+        first_param = True
+        i = 0
+        while i < len(geom):
+            g = geom[i]
+            L = g.layer
+            nxt_relu = i + 1 < len(geom) and geom[i + 1].layer.kind == "relu"
+            if L.kind == "conv":
+                c, n, _ = g.in_shape
+                d, m, _ = g.out_shape
+                out = Act(True, d, m, ru4(d), fused_relu=nxt_relu)
+                op = Op("conv", L, cur, out, woff=g.param_offsets[0], wsz=g.param_sizes[0],
+                        boff=g.param_offsets[1], relu=nxt_relu, first_param_layer=first_param,
+                        c_in=c, k=L.k, s=L.stride, p=L.pad, m=m)
+                op.Kc = c * L.k * L.k
+                op.ldK = ru4(op.Kc)
+                op.dhat = z(self.b * m * m, op.ldK)
+                op.wstage = z(d, op.ldK)
+                op.dwstage = z(d, op.ldK)
+                first_param = False
+                i += 2 if nxt_relu else 1
+            elif L.kind == "fc":
+                f = int(torch.tensor(g.in_shape).prod())
+                out = Act(False, L.d_out, 0, ru4(L.d_out), fused_relu=nxt_relu)
+                op = Op("fc", L, cur, out, woff=g.param_offsets[0], wsz=g.param_sizes[0],
+                        boff=g.param_offsets[1], relu=nxt_relu, first_param_layer=first_param, f_in=f)
+                if cur.spatial:
+                    op.flat = Act(False, f, 0, ru4(f), fused_relu=cur.fused_relu)
+                    op.flat.value = z(self.b, ru4(f))
+                else:
+                    op.flat = cur
+                op.wstage = z(L.d_out, ru4(f))
+                first_param = False
+                i += 2 if nxt_relu else 1
+            elif L.kind == "pool":
+                c, n, _ = g.in_shape
+                _, o, _ = g.out_shape
+                out = Act(True, c, o, cur.cs)
+                op = Op("pool", L, cur, out, k=L.k, s=L.stride or L.k, p=L.pad, m=o)
+                if L.mode == "max":
+                    op.argmax = z(self.b * o * o * c, dtype=torch.int32)
+                i += 1
+            elif L.kind == "relu":
+                out = Act(cur.spatial, cur.c, cur.n, cur.cs)
+                op = Op("relu", L, cur, out)
+                i += 1
+            else:  # pragma: no cover
+                raise ValueError(L)
+            out.value = z(*out.shape(self.b))
+            self.ops.append(op)
+            cur = out
+        self.logits = cur
+        # gradient buffers (the input needs none)
+        for op in self.ops:
+            op.out.grad = z(*op.out.shape(self.b))
+            if op.kind == "fc" and op.flat is not op.inp and not op.first_param_layer:
+                op.flat.grad = z(self.b, op.flat.cs)
+        self.loss_buf = z(1)
+        self.dim = net.dim
+        self.grad = z(self.dim)
+        self.wread = None
+        # workspaces sized for the largest GEMM / bias reduction
+        ws, bws, dd = 0, 0, 0
+        for op in self.ops:
+            for M, N, Kd in self._gemm_shapes(op, self.b):
+                ws = max(ws, K.gemm_workspace_bytes(self.prec, M, N, Kd, False, False))
+            if op.kind in ("conv", "fc") and op.boff >= 0:
+                M = self.b * op.m * op.m if op.kind == "conv" else self.b
+                bws = max(bws, K.bias_grad_ws_elems(M, op.layer.d_out))
+            if op.kind == "conv" and not op.first_param_layer:
+                dd = max(dd, self.b * op.m * op.m * op.ldK)
+        self.gemm_ws = z(max(ws // 4, 4))
+        self.bias_ws = z(max(bws, 4))
+        self.ddhat = z(max(dd, 4))
+        self.graph = None
+
+    # ------------------------------------------------------------ shapes --
+    @staticmethod
+    def _gemm_shapes(op: Op, b: int):
+        if op.kind == "conv":
+            Mr = b * op.m * op.m
+            d = op.layer.d_out
+            out = [(Mr, d, op.Kc), (d, op.Kc, Mr)]
+            if not op.first_param_layer:
+                out.append((Mr, op.Kc, d))
+            return out
+        if op.kind == "fc":
+            d = op.layer.d_out
+            out = [(b, d, op.f_in), (op.f_in, d, b)]
+            if not op.first_param_layer:
+                out.append((b, op.f_in, d))
+            return out
+        return []
+
+    def _gemm(self, M, N, Kd, A, lda, a_mn, B, ldb, b_mn, C, ldc, epi=_abi.EPI_STORE, bias=None,
+              aux=None, ld_aux=0):
+        K.gemm(M, N, Kd, A, lda, a_mn, B, ldb, b_mn, C, ldc, precision=self.prec, epilogue=epi,
+               bias=bias, aux=aux, ld_aux=ld_aux, workspace=self.gemm_ws)
+
+    # ----------------------------------------------------------- staging --
+    def stage_weights(self, W: torch.Tensor) -> None:
+        """Flat fp32 parameters -> GEMM-ready layouts (tap-major conv rows,
+        transposed FC weights)."""
+        for op in self.ops:
+            if op.kind == "conv":
+                d = op.layer.d_out
+                K.conv_weight_to_tap(W[op.woff:op.woff + op.wsz], d, op.c_in, op.k, op.wstage, op.ldK)
+            elif op.kind == "fc":
+                d = op.layer.d_out
+                K.transpose(W[op.woff:op.woff + op.wsz], d, 0, op.f_in, d, op.wstage, op.flat.cs, 0, 1)
+
+    # ----------------------------------------------------------- forward --
+    def forward(self, W: torch.Tensor, b: int | None = None, need_grad: bool = True) -> torch.Tensor:
+        """Run the forward pass on self.input / self.labels (first b rows);
+        leaves the mean loss in self.loss_buf and, if need_grad, dlogits in
+        the logits' grad buffer.  W is the flat fp32 parameter vector."""
+        b = self.b if b is None else int(b)
+        self.stage_weights(W)
+        for op in self.ops:
+            L = op.layer
+            if op.kind == "conv":
+                d = L.d_out
+                Mr = b * op.m * op.m
+                K.lower_nhwc(op.inp.value[:b], op.c_in, op.k, op.s, op.p, op.ldK, out=op.dhat)
+                if op.boff >= 0:
+                    epi = _abi.EPI_BIAS_RELU if op.relu else _abi.EPI_BIAS
+                    bias = W[op.boff:op.boff + d]
+                else:
+                    epi = _abi.EPI_RELU if op.relu else _abi.EPI_STORE
+                    bias = None
+                self._gemm(Mr, d, op.Kc, op.dhat, op.ldK, False, op.wstage, op.ldK, False,
+                           op.out.value, op.out.cs, epi, bias)
+            elif op.kind == "pool":
+                mode = 0 if L.mode == "max" else 1
+                K.pool_fwd(mode, op.inp.value[:b], op.inp.c, op.k, op.s, op.p, L.ceil,
+                           op.out.value[:b], op.argmax)
+            elif op.kind == "relu":
+                n = b * (op.out.value[0].numel())
+                K.relu_fwd(op.inp.value.view(-1)[:n], op.out.value.view(-1)[:n])
+            elif op.kind == "fc":
+                d = L.d_out
+                if op.flat is not op.inp:
+                    hw = op.inp.n * op.inp.n
+                    K.transpose(op.inp.value, op.inp.cs, hw * op.inp.cs, hw, op.inp.c,
+                                op.flat.value, hw, op.flat.cs, b)
+                if op.boff >= 0:
+                    epi = _abi.EPI_BIAS_RELU if op.relu else _abi.EPI_BIAS
+                    bias = W[op.boff:op.boff + d]
+                else:
+                    epi = _abi.EPI_RELU if op.relu else _abi.EPI_STORE
+                    bias = None
+                self._gemm(b, d, op.f_in, op.flat.value, op.flat.cs, False, op.wstage, op.flat.cs,
+                           False, op.out.value, op.out.cs, epi, bias)
+        C = self.net.classes
+        K.softmax_xent(self.logits.value, self.logits.cs, self.labels, b, C, self.loss_buf,
+                       self.logits.grad if need_grad else None, self.logits.cs, 1.0 / b)
+        return self.loss_buf
+
+    # ---------------------------------------------------------- backward --
+    def backward(self, b: int | None = None) -> torch.Tensor:
+        """Gradient of the mean loss w.r.t. the flat parameters -> self.grad."""
+        b = self.b if b is None else int(b)
+        G = self.grad
+        for op in reversed(self.ops):
+            L = op.layer
+            if op.kind == "fc":
+                d = L.d_out
+                dZ = op.out.grad
+                # weight gradient straight into the flat (in, out) slice
+                self._gemm(op.f_in, d, b, op.flat.value, op.flat.cs, True, dZ, op.out.cs, True,
+                           G[op.woff:op.woff + op.wsz], d)
+                if op.boff >= 0:
+                    K.bias_grad(dZ, op.out.cs, b, d, G[op.boff:op.boff + d], self.bias_ws)
+                if op.first_param_layer:
+                    continue
+                if op.flat is op.inp:
+                    if op.inp.fused_relu:
+                        self._gemm(b, op.f_in, d, dZ, op.out.cs, False, op.wstage, op.flat.cs, True,
+                                   op.inp.grad, op.inp.cs, _abi.EPI_MASK_AUX, aux=op.inp.value,
+                                   ld_aux=op.inp.cs)
+                    else:
+                        self._gemm(b, op.f_in, d, dZ, op.out.cs, False, op.wstage, op.flat.cs, True,
+                                   op.inp.grad, op.inp.cs)
+                else:
+                    self._gemm(b, op.f_in, d, dZ, op.out.cs, False, op.wstage, op.flat.cs, True,
+                               op.flat.grad, op.flat.cs)
+                    hw = op.inp.n * op.inp.n
+                    K.transpose(op.flat.grad, hw, op.flat.cs, op.inp.c, hw, op.inp.grad,
+                                op.inp.cs, hw * op.inp.cs, b)
+                    if op.inp.fused_relu:
+                        n = b * op.inp.grad[0].numel()
+                        K.relu_bwd(op.inp.grad.view(-1)[:n], op.inp.value.view(-1)[:n],
+                                   op.inp.grad.view(-1)[:n])
+            elif op.kind == "conv":
+                d = L.d_out
+                Mr = b * op.m * op.m
+                dZ = op.out.grad
+                self._gemm(d, op.Kc, Mr, dZ, op.out.cs, True, op.dhat, op.ldK, True, op.dwstage,
+                           op.ldK)
+                K.conv_weight_to_tap(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k, op.dwstage,
+                                     op.ldK, inverse=True)
+                if op.boff >= 0:
+                    K.bias_grad(dZ, op.out.cs, Mr, d, G[op.boff:op.boff + d], self.bias_ws)
+                if op.first_param_layer:
+                    continue
+                self._gemm(Mr, op.Kc, d, dZ, op.out.cs, False, op.wstage, op.ldK, True, self.ddhat,
+                           op.ldK)
+                K.col2im_nhwc(self.ddhat, op.ldK, b, op.inp.n, op.c_in, op.inp.cs, op.k, op.s, op.p,
+                              op.inp.grad)
+                if op.inp.fused_relu:
+                    n = b * op.inp.grad[0].numel()
+                    K.relu_bwd(op.inp.grad.view(-1)[:n], op.inp.value.view(-1)[:n],
+                               op.inp.grad.view(-1)[:n])
+            elif op.kind == "pool":
+                if op.inp.grad is None:
+                    continue
+                mode = 0 if L.mode == "max" else 1
+                K.pool_bwd(mode, op.out.grad[:b], (b, op.inp.n, op.inp.n, op.inp.cs), op.inp.c,
+                           op.k, op.s, op.p, L.ceil, op.argmax, op.inp.value,
+                           op.inp.fused_relu, op.inp.grad)
+            elif op.kind == "relu":
+                if op.inp.grad is None:
+                    continue
+                n = b * op.out.grad[0].numel()
+                K.relu_bwd(op.out.grad.view(-1)[:n], op.out.value.view(-1)[:n],
+                           op.inp.grad.view(-1)[:n])
+        return G
+
+    # ------------------------------------------------------------- input --
+    def load_batch(self, X_nhwc: torch.Tensor, y: torch.Tensor) -> None:
+        b = X_nhwc.shape[0]
+        self.input.value[:b].copy_(X_nhwc)
+        self.labels[:b].copy_(y)
+
+    def gather_batch(self, data: torch.Tensor, labels: torch.Tensor, idx: torch.Tensor) -> None:
+        """Device gather of a sampled batch (problems.py:197-199) from a
+        device-resident NHWC dataset."""
+        K.gather_rows(data, idx, self.input.value)
+        K.gather_i32(labels, idx, self.labels)
+
+    def loss_and_grad(self, W: torch.Tensor, b: int | None = None):
+        self.forward(W, b, need_grad=True)
+        self.backward(b)
+        return self.loss_buf, self.grad
+
+    def kernel_launches_per_step(self) -> int:
+        """Launches of libomni kernels in one gather + fwd + bwd + SGD step."""
+        n = 2 + 1 + 1  # gathers, softmax, sgd
+        for op in self.ops:
+            if op.kind == "conv":
+                n += 1 + 1 + 1   # stage, lower, gemm
+                n += 1 + 1       # wgrad gemm, inverse stage
+                n += 2 if op.boff >= 0 else 0
+                if not op.first_param_layer:
+                    n += 2 + (1 if op.inp.fused_relu else 0)
+            elif op.kind == "fc":
+                n += 1 + 1 + (1 if op.flat is not op.inp else 0)
+                n += 1 + (2 if op.boff >= 0 else 0)
+                if not op.first_param_layer:
+                    n += 1 + (1 if op.flat is not op.inp else 0)
+            elif op.kind == "pool":
+                n += 1 + (1 if op.inp.grad is not None else 0)
+            elif op.kind == "relu":
+                n += 2
+        # split-K GEMMs add a reduction launch each
+        for op in self.ops:
+            for M, N, Kd in self._gemm_shapes(op, self.b):
+                s, _ = K.gemm_plan(self.prec, M, N, Kd)
+                n += 1 if s > 1 else 0
+        return n

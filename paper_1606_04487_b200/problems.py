@@ -1,0 +1,252 @@
+"""Drop-in CNN training problems (omnisim.problems, problems.py:152-279), on the GPU.
+
+``CNNProblem`` implements the reference's ``TrainingProblem`` plug-in
+(sgd.py:115-152) for any NetSpec: batches are sampled with replacement by the
+caller's RNG exactly as the reference does (problems.py:197-199), gradients
+use the mean-over-batch convention (:248), and every forward/backward runs on
+the B200 through ``engine.GpuNet``.  At this boundary W and gradients are
+float64 NumPy (as in the reference); ``device_session`` keeps the model in
+HBM for the training loops.
+
+``TinyCNNProblem`` is the reference's only CNN, with the same constructor,
+validation, synthetic data and teacher labels (problems.py:168-199), so its
+losses and gradients can be compared with the reference on identical inputs.
+"""
+
+from __future__ import annotations
+
+from typing import Any
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from . import nets
+from .engine import GpuNet
+from .sgd import Hyperparams, SGDState, TrainingProblem
+from .tensors import ConvSpec
+
+HOST_DATA_LIMIT = 32 * 1024 * 1024  # elements; larger synthetic sets are generated on the device
+
+
+def _rng(seed: int, *key: int) -> np.random.Generator:
+    return np.random.default_rng(np.random.SeedSequence(seed, spawn_key=tuple(key)))
+
+
+class Batch:
+    """A sampled mini-batch: indices into the problem's dataset.  Unpacks to
+    host (images, labels) arrays like the reference's batches."""
+
+    __slots__ = ("idx", "_problem")
+
+    def __init__(self, problem: "CNNProblem", idx: np.ndarray):
+        self.idx = np.asarray(idx, dtype=np.int64)
+        self._problem = problem
+
+    def __len__(self) -> int:
+        return 2
+
+    def __iter__(self):
+        p = self._problem
+        if p.images is None:
+            raise ValueError("this problem's dataset lives on the device only")
+        yield p.images[self.idx]
+        yield p.labels[self.idx]
+
+    @property
+    def size(self) -> int:
+        return int(self.idx.size)
+
+
+class DeviceSession:
+    """W, V resident in HBM; one step = gather + forward + backward + K8."""
+
+    def __init__(self, problem: "CNNProblem", state: SGDState, hp: Hyperparams):
+        self.problem = problem
+        self.hp = hp
+        dev = problem.device
+        self.W = torch.from_numpy(np.ascontiguousarray(state.W, dtype=np.float32)).to(dev)
+        self.V = torch.from_numpy(np.ascontiguousarray(state.V, dtype=np.float32)).to(dev)
+        self.t = state.t
+        self.engine = problem.engine(hp.b)
+
+    def step(self, batch: Any, w_read: torch.Tensor | None = None) -> None:
+        """V = mu V - eta (grad(w_read) + lam w_read); W += V, with w_read = W when
+        synchronous (sgd.py:104-112)."""
+        wr = self.W if w_read is None else w_read
+        b = self.problem.load_batch(self.engine, batch)
+        self.engine.loss_and_grad(wr, b)
+        hp = self.hp
+        K.sgd_momentum(self.W, self.V, self.engine.grad, wr, hp.eta, hp.mu, hp.lam)
+        self.t += 1
+
+    def full_loss(self) -> float:
+        return self.problem.full_loss_device(self.W)
+
+    def state(self) -> SGDState:
+        return SGDState(W=self.W.double().cpu().numpy(), V=self.V.double().cpu().numpy(), t=self.t)
+
+
+class CNNProblem(TrainingProblem):
+    """Softmax-CE training of a NetSpec on synthetic Gaussian images."""
+
+    def __init__(self, net: nets.NetSpec | str, n_examples: int = 128, seed: int = 0,
+                 labels: str | None = None, precision: str = "3xtf32", device=None):
+        self.net = nets.get(net) if isinstance(net, str) else net
+        if n_examples < 1:
+            raise ValueError("n_examples must be >= 1")
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1606_04487_b200 needs a CUDA device (no CPU fallback)")
+        self.seed = seed
+        self.precision = precision
+        self.device = torch.device(device if device is not None else "cuda")
+        c, s, C = self.net.in_channels, self.net.in_size, self.net.classes
+        per = c * s * s
+        self._n = n_examples
+        if labels is None:
+            labels = "teacher" if per * C <= 4 * 1024 * 1024 else "uniform"
+        if n_examples * per <= HOST_DATA_LIMIT:
+            rng = _rng(seed, 0)
+            images = rng.standard_normal((n_examples, c, s, s))
+            if labels == "teacher":
+                teacher = rng.standard_normal((C, per))
+                lab = np.argmax(teacher @ images.reshape(n_examples, -1).T, axis=0)
+            else:
+                lab = rng.integers(0, C, size=n_examples)
+            self.images, self.labels = images, lab
+            self.data = torch.from_numpy(images.astype(np.float32)).to(self.device)
+            self.data = self.data.permute(0, 2, 3, 1).contiguous()
+            self.data_labels = torch.from_numpy(lab.astype(np.int32)).to(self.device)
+        else:
+            gen = torch.Generator(device=self.device)
+            gen.manual_seed(seed)
+            self.images = self.labels = None
+            self.data = torch.randn((n_examples, s, s, c), generator=gen, device=self.device)
+            self.data_labels = torch.randint(0, C, (n_examples,), generator=gen,
+                                             device=self.device, dtype=torch.int32)
+        self._engines: dict[int, GpuNet] = {}
+
+    # ------------------------------------------------------------- API ---
+    @property
+    def dim(self) -> int:
+        return self.net.dim
+
+    @property
+    def n_examples(self) -> int:
+        return self._n
+
+    def initial_weights(self) -> np.ndarray:
+        """0.01 * N(0, 1) over the whole flat vector (problems.py:194-195)."""
+        return 0.01 * _rng(self.seed, 1).standard_normal(self.dim)
+
+    def sample_batch(self, rng: np.random.Generator, b: int) -> Batch:
+        return Batch(self, rng.integers(0, self._n, size=b))
+
+    def engine(self, b: int) -> GpuNet:
+        e = self._engines.get(b)
+        if e is None:
+            e = GpuNet(self.net, b, self.device, self.precision)
+            self._engines[b] = e
+        return e
+
+    def load_batch(self, engine: GpuNet, batch: Any) -> int:
+        """Put a batch on the device (gather by index, or upload host arrays)."""
+        if isinstance(batch, Batch):
+            idx = torch.from_numpy(batch.idx).to(self.device, non_blocking=True)
+            engine.gather_batch(self.data, self.data_labels, idx)
+            return batch.size
+        X, y = batch
+        X = np.asarray(X)
+        Xd = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float32)).to(self.device)
+        engine.load_batch(Xd.permute(0, 2, 3, 1), torch.from_numpy(np.asarray(y, dtype=np.int32)).to(self.device))
+        return X.shape[0]
+
+    def _w(self, W) -> torch.Tensor:
+        if isinstance(W, torch.Tensor):
+            return W
+        W = np.asarray(W, dtype=np.float64)
+        if W.shape != (self.dim,):
+            raise ValueError(f"weight vector has shape {W.shape}, problem needs ({self.dim},)")
+        return torch.from_numpy(W.astype(np.float32)).to(self.device)
+
+    def _batch_size(self, batch) -> int:
+        return batch.size if isinstance(batch, Batch) else len(batch[1])
+
+    def loss(self, W, batch) -> float:
+        e = self.engine(self._batch_size(batch))
+        b = self.load_batch(e, batch)
+        return float(e.forward(self._w(W), b, need_grad=False).item())
+
+    def grad(self, W, batch) -> np.ndarray:
+        e = self.engine(self._batch_size(batch))
+        b = self.load_batch(e, batch)
+        _, G = e.loss_and_grad(self._w(W), b)
+        return G.double().cpu().numpy()
+
+    def full_loss_device(self, Wd: torch.Tensor, chunk: int = 256) -> float:
+        n = self._n
+        e = self.engine(min(n, chunk))
+        tot = torch.zeros(1, dtype=torch.float64, device=self.device)
+        for s0 in range(0, n, e.b):
+            b = min(e.b, n - s0)
+            idx = torch.arange(s0, s0 + b, device=self.device, dtype=torch.int64)
+            e.gather_batch(self.data, self.data_labels, idx)
+            tot += e.forward(Wd, b, need_grad=False).double() * b
+        return float(tot.item() / n)
+
+    def full_loss(self, W) -> float:
+        return self.full_loss_device(self._w(W))
+
+    def full_grad(self, W, chunk: int = 256) -> np.ndarray:
+        n = self._n
+        e = self.engine(min(n, chunk))
+        Wd = self._w(W)
+        acc = torch.zeros(self.dim, dtype=torch.float64, device=self.device)
+        for s0 in range(0, n, e.b):
+            b = min(e.b, n - s0)
+            idx = torch.arange(s0, s0 + b, device=self.device, dtype=torch.int64)
+            e.gather_batch(self.data, self.data_labels, idx)
+            _, G = e.loss_and_grad(Wd, b)
+            acc += G.double() * (b / n)
+        return acc.cpu().numpy()
+
+    def device_session(self, state: SGDState, hp: Hyperparams) -> DeviceSession:
+        return DeviceSession(self, state, hp)
+
+
+def make_cnn(net: str, n_examples: int = 128, seed: int = 0, **kw) -> CNNProblem:
+    return CNNProblem(net, n_examples, seed, **kw)
+
+
+class TinyCNNProblem(CNNProblem):
+    """conv(3x3, 4 ch) -> ReLU -> 2x2 max-pool -> linear -> softmax-CE (problems.py:152-275)."""
+
+    D_OUT = 4
+    K = 3
+
+    def __init__(self, image_size: int, classes: int, seed: int = 0, n_examples: int = 128,
+                 precision: str = "3xtf32", device=None):
+        if image_size < 4 or image_size > 16 or image_size % 2 != 0:
+            raise ValueError("image_size must be even and in [4, 16]")
+        if not 2 <= classes <= 10:
+            raise ValueError("classes must be in [2, 10]")
+        self.image_size = image_size
+        self.classes = classes
+        s = image_size
+        self.spec = ConvSpec(n=s, k=self.K, d_in=1, d_out=self.D_OUT, stride=1, pad=1)
+        self.feat = self.D_OUT * (s // 2) * (s // 2)
+        self.k_size = self.D_OUT * self.K * self.K
+        super().__init__(nets.tiny_cnn(s, classes), n_examples, seed, labels="teacher",
+                         precision=precision, device=device)
+
+    def predict_proba(self, W, X) -> np.ndarray:
+        X = np.asarray(X)
+        e = self.engine(X.shape[0])
+        self.load_batch(e, (X, np.zeros(X.shape[0], dtype=np.int32)))
+        e.forward(self._w(W), X.shape[0], need_grad=False)
+        logits = e.logits.value[: X.shape[0], : self.classes].double()
+        return torch.softmax(logits, dim=1).cpu().numpy()
+
+
+def make_tiny_cnn(image_size: int, classes: int, seed: int = 0, n_examples: int = 128) -> TinyCNNProblem:
+    return TinyCNNProblem(image_size, classes, seed, n_examples)

@@ -1,0 +1,244 @@
+"""Drop-in for omnisim.simulator's hot-path part: the g-group asynchronous schedule.
+
+``simulate`` keeps the reference's event semantics exactly (simulator.py:123-213):
+g groups snapshot the master model, draw a batch from their own stream,
+"compute" for t_conv(k), queue FIFO at one serial FC server, and on
+completion apply one momentum update with the gradient evaluated at their
+snapshot (the regulariser uses the snapshot too).  With a GPU problem the
+master W, V and every snapshot stay in HBM and each update is one fused
+forward/backward + K8 launch sequence; the event order is host logic and
+deterministic per seed.  ``groups.py`` runs the same schedule across real
+GPUs.
+"""
+
+from __future__ import annotations
+
+import heapq
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .cluster import ExecutionPlan, PhaseProfile, t_conv
+from .sgd import (DIVERGENCE_FACTOR, Hyperparams, LossTrace, SGDState, TrainingProblem,
+                  batch_stream, service_stream, sgd_step)
+
+DEFAULT_BURN_IN = 100
+
+
+@dataclass(frozen=True)
+class SimConfig:
+    plan: ExecutionPlan
+    profile: PhaseProfile
+    hp: Hyperparams
+    problem: TrainingProblem
+    service_mode: str = "deterministic"
+    max_updates: Optional[int] = None
+    max_sim_seconds: Optional[float] = None
+    seed: int = 0
+    init: Optional[SGDState] = None
+    loss_sample_interval: int = 1
+    record_models: bool = False
+
+    def __post_init__(self) -> None:
+        if self.service_mode not in ("deterministic", "exponential"):
+            raise ValueError(f"unknown service_mode {self.service_mode!r}")
+        if self.max_updates is None and self.max_sim_seconds is None:
+            raise ValueError("need max_updates and/or max_sim_seconds")
+        if self.max_updates is not None and self.max_updates < 1:
+            raise ValueError("max_updates must be >= 1")
+        if self.loss_sample_interval < 1:
+            raise ValueError("loss_sample_interval must be >= 1")
+
+
+@dataclass(frozen=True, slots=True)
+class SimEvent:
+    group_id: int
+    read_step: int
+    write_step: int
+    staleness: int
+    start_time: float
+    fc_enqueue_time: float
+    finish_time: float
+
+
+@dataclass
+class SimTrace:
+    events: list
+    loss_steps: np.ndarray
+    loss_times: np.ndarray
+    loss_values: np.ndarray
+    final_state: SGDState
+    diverged: bool = False
+    models: Optional[np.ndarray] = None
+
+    @property
+    def write_times(self) -> np.ndarray:
+        return np.array([e.finish_time for e in self.events])
+
+    def to_loss_trace(self) -> LossTrace:
+        return LossTrace(steps=self.loss_steps, sim_times=self.loss_times, losses=self.loss_values,
+                         final_state=self.final_state, diverged=self.diverged)
+
+    def write_csv(self, path) -> None:
+        sampled = dict(zip(self.loss_steps.tolist(), self.loss_values.tolist()))
+        with open(path, "w") as f:
+            f.write("write_step,group_id,read_step,staleness,start_s,finish_s,loss\n")
+            last = sampled.get(0, float("nan"))
+            for e in self.events:
+                last = sampled.get(e.write_step, last)
+                f.write(f"{e.write_step},{e.group_id},{e.read_step},{e.staleness},"
+                        f"{e.start_time:.6f},{e.finish_time:.6f},{last!r}\n")
+
+
+class _HostModel:
+    """Master model for problems without a device session (host arrays)."""
+
+    def __init__(self, problem, state, hp):
+        self.problem, self.state, self.hp = problem, state, hp
+
+    @property
+    def t(self):
+        return self.state.t
+
+    def snapshot(self):
+        return self.state.W.copy()
+
+    def apply(self, snapshot, batch):
+        g = self.problem.grad(snapshot, batch)
+        self.state = sgd_step(self.state, self.hp, g, snapshot)
+
+    def finite(self):
+        return bool(np.all(np.isfinite(self.state.W)))
+
+    def full_loss(self):
+        return self.problem.full_loss(self.state.W)
+
+    def model_copy(self):
+        return self.state.W.copy()
+
+    def final(self):
+        return self.state
+
+
+class _DeviceModel:
+    """Master W, V and snapshots resident in HBM (CNNProblem)."""
+
+    def __init__(self, problem, state, hp):
+        import torch
+
+        self.torch = torch
+        self.s = problem.device_session(state, hp)
+
+    @property
+    def t(self):
+        return self.s.t
+
+    def snapshot(self):
+        return self.s.W.clone()
+
+    def apply(self, snapshot, batch):
+        self.s.step(batch, w_read=snapshot)
+
+    def finite(self):
+        return bool(self.torch.isfinite(self.s.W).all().item())
+
+    def full_loss(self):
+        return self.s.full_loss()
+
+    def model_copy(self):
+        return self.s.W.double().cpu().numpy()
+
+    def final(self):
+        return self.s.state()
+
+
+def simulate(cfg: SimConfig) -> SimTrace:
+    """Run the event loop until the update or sim-time budget, or divergence."""
+    g = cfg.plan.g
+    conv_mean = t_conv(cfg.plan.k, cfg.profile)
+    fc_mean = cfg.profile.t_fc
+    exponential = cfg.service_mode == "exponential"
+    batch_rngs = [batch_stream(cfg.seed, i) for i in range(g)]
+    svc_rngs = [service_stream(cfg.seed, i) for i in range(g)] if exponential else None
+
+    state = cfg.init if cfg.init is not None else cfg.problem.initial_state()
+    model = (_DeviceModel if hasattr(cfg.problem, "device_session") else _HostModel)(cfg.problem, state, cfg.hp)
+    initial_loss = model.full_loss()
+    bound = DIVERGENCE_FACTOR * max(abs(initial_loss), 1.0)
+    events: list[SimEvent] = []
+    loss_steps, loss_times, loss_values = [model.t], [0.0], [initial_loss]
+    models = [model.model_copy()] if cfg.record_models else None
+    diverged = not np.isfinite(initial_loss)
+    t0 = model.t
+
+    def draw(i):
+        if exponential:
+            r = svc_rngs[i]
+            return r.exponential(conv_mean), r.exponential(fc_mean)
+        return conv_mean, fc_mean
+
+    heap: list = []
+    seq = 0
+    for i in range(g):
+        cd, fs = draw(i)
+        batch = cfg.problem.sample_batch(batch_rngs[i], cfg.hp.b)
+        heapq.heappush(heap, (cd, seq, i, model.snapshot(), model.t, 0.0, batch, fs))
+        seq += 1
+
+    fc_free = 0.0
+    while not diverged:
+        if cfg.max_updates is not None and model.t - t0 >= cfg.max_updates:
+            break
+        conv_done, _, i, snap, read_step, read_time, batch, fs = heap[0]
+        finish = max(fc_free, conv_done) + fs
+        if cfg.max_sim_seconds is not None and finish > cfg.max_sim_seconds:
+            break
+        heapq.heappop(heap)
+        fc_free = finish
+        model.apply(snap, batch)
+        t = model.t
+        events.append(SimEvent(i, read_step, t, t - 1 - read_step, read_time, conv_done, finish))
+        if models is not None:
+            models.append(model.model_copy())
+        if not model.finite():
+            diverged = True
+        if (t - t0) % cfg.loss_sample_interval == 0 or diverged:
+            loss = model.full_loss()
+            loss_steps.append(t)
+            loss_times.append(finish)
+            loss_values.append(loss)
+            if not np.isfinite(loss) or loss > bound:
+                diverged = True
+        if diverged:
+            break
+        cd, nfs = draw(i)
+        nb = cfg.problem.sample_batch(batch_rngs[i], cfg.hp.b)
+        heapq.heappush(heap, (finish + cd, seq, i, model.snapshot(), t, finish, nb, nfs))
+        seq += 1
+
+    return SimTrace(events=events, loss_steps=np.array(loss_steps), loss_times=np.array(loss_times),
+                    loss_values=np.array(loss_values), final_state=model.final(), diverged=diverged,
+                    models=np.array(models) if models is not None else None)
+
+
+def measured_he(trace: SimTrace, burn_in: int = DEFAULT_BURN_IN) -> float:
+    """Mean inter-write interval after discarding the first burn_in events."""
+    if len(trace.events) <= burn_in + 1:
+        raise ValueError(
+            f"trace has {len(trace.events)} events; need more than burn_in + 1 = {burn_in + 1}")
+    return float(np.diff(trace.write_times[burn_in:]).mean())
+
+
+@dataclass(frozen=True)
+class StalenessStats:
+    mean: float
+    histogram: dict
+
+
+def staleness_stats(trace: SimTrace, burn_in: int = 0) -> StalenessStats:
+    s = np.array([e.staleness for e in trace.events[burn_in:]])
+    if s.size == 0:
+        raise ValueError("trace has no events past burn_in")
+    v, c = np.unique(s, return_counts=True)
+    return StalenessStats(mean=float(s.mean()), histogram={int(a): int(b) for a, b in zip(v, c)})

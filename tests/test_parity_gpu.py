@@ -1,0 +1,166 @@
+"""Parity of the B200 path with the reference (golden fixtures) and the CPU oracle.
+
+Tolerances (normwise relative error unless stated), 3xTF32 mode:
+  lowering / lifting / argmax-routing           bit-exact
+  conv_lowered, gemm                           <= 2e-6
+  per-network loss                             <= 1e-5 relative
+  per-network gradient (each parameter tensor) <= 2e-5
+  g = 1 multi-step weights (8 steps)           <= 1e-4
+  g > 1 deterministic schedule                 event log exact, weights <= 1e-4
+TF32 mode (the throughput path): gradient <= 2e-2, reported only.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_1606_04487_b200 as P  # noqa: E402
+from paper_1606_04487_b200 import nets  # noqa: E402
+from paper_1606_04487_b200.problems import CNNProblem, TinyCNNProblem  # noqa: E402
+from oracle import refcnn as R  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def gold(name):
+    return np.load(os.path.join(GOLD, name))
+
+
+def nrel(x, ref):
+    return float(np.linalg.norm(np.asarray(x) - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+# ------------------------------------------------------- operator API ----
+def test_lower_lift_bit_exact_vs_reference():
+    z = gold("lower.npz")
+    i = 0
+    while f"case{i}_geom" in z:
+        b, c, n, k, s, p, start, b_p = (int(v) for v in z[f"case{i}_geom"])
+        spec = P.ConvSpec(n=n, k=k, d_in=c, d_out=1, stride=s, pad=p)
+        got = P.lower(P.Tensor4(z[f"case{i}_D"]), spec, b_p=b_p, start=start)
+        assert np.array_equal(got.matrix, z[f"case{i}_Dhat"]), i
+        i += 1
+    spec = P.ConvSpec(n=5, k=3, d_in=2, d_out=3, pad=1)
+    R_ = np.random.default_rng(0).standard_normal((2 * 25, 3))
+    assert np.array_equal(P.lift(R_, spec, 2).values, R.lift(R_, 2, 5, 3))
+
+
+def test_conv_gemm_vs_reference():
+    z = gold("conv.npz")
+    i = 0
+    while f"conv{i}_geom" in z:
+        n, k, din, dout, s, p, b = (int(v) for v in z[f"conv{i}_geom"])
+        spec = P.ConvSpec(n=n, k=k, d_in=din, d_out=dout, stride=s, pad=p)
+        for b_p in (1, b):
+            got = P.conv_lowered(P.Tensor4(z[f"conv{i}_D"]), P.Tensor4(z[f"conv{i}_K"]), spec, b_p=b_p, workers=2)
+            assert nrel(got.values, z[f"conv{i}_R"]) < 2e-6
+        i += 1
+    kat = P.conv_lowered(P.Tensor4(z["kat_D"]), P.Tensor4(z["kat_K"]), P.ConvSpec(n=3, k=2, d_in=1, d_out=1))
+    assert np.allclose(kat.values.reshape(2, 2), [[6, 8], [12, 14]], atol=1e-5)
+    assert nrel(P.gemm(z["gemm_A"], z["gemm_B"]), z["gemm_C"]) < 2e-6
+    assert np.allclose(P.gemm([[1.0, 2.0], [3.0, 4.0]], [[5.0], [6.0]]), [[17.0], [39.0]], atol=1e-4)
+
+
+def test_sgd_step_kat():
+    s = P.sgd_step(P.SGDState(W=np.array([1.0]), V=np.array([0.0])), P.Hyperparams(eta=0.1, mu=0.9),
+                   np.array([2.0]), np.array([1.0]))
+    assert abs(s.V[0] + 0.2) < 1e-7 and abs(s.W[0] - 0.8) < 1e-7 and s.t == 1
+
+
+# ----------------------------------------------------------- TinyCNN -----
+@pytest.mark.parametrize("tag", ["s8c4", "s16c10"])
+def test_tiny_cnn_vs_reference(tag):
+    z = gold("tinycnn.npz")
+    size, classes, n_ex, b, seed = (int(v) for v in z[f"{tag}_meta"])
+    prob = TinyCNNProblem(size, classes, seed=seed, n_examples=n_ex)
+    assert np.array_equal(prob.images, z[f"{tag}_images"]) and np.array_equal(prob.labels, z[f"{tag}_labels"])
+    W0 = prob.initial_weights()
+    assert np.array_equal(W0, z[f"{tag}_W0"])
+    batch = prob.sample_batch(P.batch_stream(seed), b)
+    X, y = batch
+    assert np.array_equal(X, z[f"{tag}_bx"])
+    g = prob.grad(W0, batch)
+    assert nrel(g, z[f"{tag}_grad"]) < 2e-5
+    assert abs(prob.loss(W0, batch) - float(z[f"{tag}_loss"])) < 1e-5 * abs(float(z[f"{tag}_loss"]))
+    assert abs(prob.full_loss(W0) - float(z[f"{tag}_full_loss"])) < 1e-5
+    g2 = prob.grad(W0, (X, y))  # host-array batch, the reference's batch type
+    assert nrel(g2, g) < 1e-6
+
+
+def test_run_sync_vs_reference():
+    z = gold("tinycnn.npz")
+    eta, mu, lam, b, steps, seed = z["sync_hp"]
+    prob = TinyCNNProblem(8, 4, seed=3, n_examples=64)
+    hp = P.Hyperparams(eta=float(eta), mu=float(mu), lam=float(lam), b=int(b))
+    tr = P.run_sync(prob, hp, prob.initial_state(), P.StopRule(max_steps=int(steps)), seed=int(seed))
+    assert nrel(tr.final_state.W, z["sync_W"]) < 1e-4
+    assert nrel(tr.final_state.V, z["sync_V"]) < 1e-3
+    assert np.allclose(tr.losses, z["sync_losses"], rtol=1e-5)
+
+
+def test_simulate_deterministic_vs_reference():
+    z = gold("tinycnn.npz")
+    prob = TinyCNNProblem(8, 4, seed=3, n_examples=64)
+    hp = P.Hyperparams(eta=0.05, mu=0.9, lam=1e-3, b=16)
+    cfg = P.SimConfig(plan=P.ExecutionPlan(N=8, g=4), profile=P.PhaseProfile(T_cc=8.0, T_nc=0.1, t_fc=0.5),
+                      hp=hp, problem=prob, max_updates=12, seed=5)
+    tr = P.simulate(cfg)
+    ev = np.array([[e.group_id, e.read_step, e.write_step, e.staleness] for e in tr.events])
+    assert np.array_equal(ev, z["sim_events"][:, :4])
+    assert nrel(tr.final_state.W, z["sim_W"]) < 1e-4
+    st = P.staleness_stats(tr, burn_in=4)
+    assert st.mean == 3.0
+
+
+# ------------------------------------------------ networks vs oracle ------
+NETS = [("lenet", 6, {}), ("cifar10_quick", 4, {}), ("caffenet", 2, {})]
+
+
+def per_param_errors(net, g, ref):
+    errs = []
+    for geo in net.geometry():
+        for off, sz in zip(geo.param_offsets, geo.param_sizes):
+            if sz and off >= 0:
+                errs.append((geo.layer.kind, geo.index, nrel(g[off:off + sz], ref[off:off + sz])))
+    return errs
+
+
+@pytest.mark.parametrize("name,b,kw", NETS)
+def test_network_grad_vs_oracle(name, b, kw):
+    net = nets.get(name)
+    prob = CNNProblem(net, n_examples=max(16, b), seed=1, precision="3xtf32")
+    rng = np.random.default_rng(7)
+    W = 0.05 * rng.standard_normal(net.dim)   # larger than 0.01 so deep layers carry signal
+    batch = prob.sample_batch(P.batch_stream(2), b)
+    if prob.images is not None:
+        X, y = batch
+    else:
+        idx = torch.from_numpy(batch.idx).cuda()
+        X = prob.data[idx].permute(0, 3, 1, 2).double().cpu().numpy()
+        y = prob.data_labels[idx].cpu().numpy()
+    ref = R.grad(net.to_dicts(), net.in_channels, net.in_size, W, X, y, workers=os.cpu_count() or 1)
+    ref_loss = R.loss(net.to_dicts(), net.in_channels, net.in_size, W, X, y)
+    g = prob.grad(W, batch)
+    loss = prob.loss(W, batch)
+    assert abs(loss - ref_loss) <= 1e-5 * max(1.0, abs(ref_loss)), (loss, ref_loss)
+    errs = per_param_errors(net, g, ref)
+    worst = max(e for _, _, e in errs)
+    assert worst < 2e-5, errs
+    # tf32 (throughput) mode, reported with a loose bound
+    p32 = CNNProblem(net, n_examples=max(16, b), seed=1, precision="tf32")
+    g32 = p32.grad(W, batch)
+    assert nrel(g32, ref) < 2e-2
+
+
+def test_full_grad_and_chunked_loss():
+    prob = CNNProblem("lenet", n_examples=300, seed=4)
+    W = prob.initial_weights()
+    net = prob.net
+    ref = R.grad(net.to_dicts(), 1, 28, W, prob.images, prob.labels, workers=os.cpu_count() or 1)
+    assert nrel(prob.full_grad(W), ref) < 2e-5
+    ref_loss = R.loss(net.to_dicts(), 1, 28, W, prob.images, prob.labels)
+    assert abs(prob.full_loss(W) - ref_loss) < 1e-5
