@@ -276,6 +276,45 @@ def forward(layers, in_ch, in_size, W, X, workers: int = 1):
     return h, cache
 
 
+def _partitions(b, workers):
+    bounds = np.linspace(0, b, num=min(workers, b) + 1, dtype=int)
+    return [(int(a), int(z)) for a, z in zip(bounds[:-1], bounds[1:]) if z > a]
+
+
+def _par_rows(A, B, b, workers):
+    """gemm(A, B) with A's rows split into contiguous image partitions, one
+    thread each (the reference's conv_lowered partitioning, tensors.py:242-255)."""
+    parts = _partitions(b, workers)
+    rows = A.shape[0] // b
+    out = np.empty((A.shape[0], B.shape[1]))
+
+    def run(ab):
+        lo, hi = ab
+        out[lo * rows:hi * rows] = gemm(A[lo * rows:hi * rows], B)
+
+    if len(parts) == 1:
+        run(parts[0])
+    else:
+        with ThreadPoolExecutor(max_workers=len(parts)) as ex:
+            list(ex.map(run, parts))
+    return out
+
+
+def _par_wgrad(Dhat, dR, b, workers):
+    """Dhat^T dR summed over image partitions (fixed partition order)."""
+    parts = _partitions(b, workers)
+    rows = Dhat.shape[0] // b
+    if len(parts) == 1:
+        return gemm(Dhat.T, dR)
+    with ThreadPoolExecutor(max_workers=len(parts)) as ex:
+        partial = list(ex.map(lambda ab: gemm(Dhat[ab[0] * rows:ab[1] * rows].T,
+                                              dR[ab[0] * rows:ab[1] * rows]), parts))
+    out = partial[0]
+    for q in partial[1:]:
+        out = out + q
+    return out
+
+
 def softmax(logits):
     shifted = logits - logits.max(axis=1, keepdims=True)
     e = np.exp(shifted)
@@ -325,11 +364,11 @@ def grad(layers, in_ch, in_size, W, X, y, workers: int = 1, return_acts: bool = 
             m = conv_out(n, k, s, p)
             dR = dh.transpose(0, 2, 3, 1).reshape(b_ * m * m, d_out)
             Dhat = lower(x, k, s, p)
-            gk = gemm(Dhat.T, dR).T.reshape(pv[0].shape)
+            gk = _par_wgrad(Dhat, dR, b_, workers).T.reshape(pv[0].shape)
             gl = [gk] + ([dR.sum(axis=0)] if len(pv) > 1 else [])
             grads[li] = gl
             if li > 0:
-                dh = col2im(gemm(dR, lower_kernel(pv[0]).T), b_, c, n, k, s, p)
+                dh = col2im(_par_rows(dR, lower_kernel(pv[0]).T, b_, workers), b_, c, n, k, s, p)
     flat = np.concatenate([g.ravel() for gl in grads if gl is not None for g in gl])
     if return_acts:
         return flat, logits

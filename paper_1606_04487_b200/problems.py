@@ -58,6 +58,23 @@ class Batch:
         return int(self.idx.size)
 
 
+class HostBatch:
+    """A batch already laid out for the device -- images NHWC float32, labels
+    int32 -- in (preferably pinned) host memory; copied asynchronously on the
+    compute stream when a step consumes it."""
+
+    __slots__ = ("X", "y")
+
+    def __init__(self, X: torch.Tensor, y: torch.Tensor):
+        if X.dim() != 4 or X.dtype != torch.float32 or y.dtype != torch.int32:
+            raise ValueError("HostBatch wants X (b, n, n, c) float32 and y (b,) int32")
+        self.X, self.y = X, y
+
+    @property
+    def size(self) -> int:
+        return int(self.X.shape[0])
+
+
 class DeviceSession:
     """W, V resident in HBM; one step = gather + forward + backward + K8."""
 
@@ -82,6 +99,10 @@ class DeviceSession:
 
     def full_loss(self) -> float:
         return self.problem.full_loss_device(self.W)
+
+    def last_loss(self) -> float:
+        """Mean loss of the last step's batch (one 4-byte device-to-host read)."""
+        return float(self.engine.loss_buf.item())
 
     def state(self) -> SGDState:
         return SGDState(W=self.W.double().cpu().numpy(), V=self.V.double().cpu().numpy(), t=self.t)
@@ -155,6 +176,11 @@ class CNNProblem(TrainingProblem):
             idx = torch.from_numpy(batch.idx).to(self.device, non_blocking=True)
             engine.gather_batch(self.data, self.data_labels, idx)
             return batch.size
+        if isinstance(batch, HostBatch):
+            b = batch.size
+            engine.input.value[:b].copy_(batch.X, non_blocking=True)
+            engine.labels[:b].copy_(batch.y, non_blocking=True)
+            return b
         X, y = batch
         X = np.asarray(X)
         Xd = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float32)).to(self.device)
@@ -170,7 +196,7 @@ class CNNProblem(TrainingProblem):
         return torch.from_numpy(W.astype(np.float32)).to(self.device)
 
     def _batch_size(self, batch) -> int:
-        return batch.size if isinstance(batch, Batch) else len(batch[1])
+        return batch.size if isinstance(batch, (Batch, HostBatch)) else len(batch[1])
 
     def loss(self, W, batch) -> float:
         e = self.engine(self._batch_size(batch))

@@ -7,7 +7,7 @@ Tolerances (normwise relative error unless stated), 3xTF32 mode:
   per-network gradient (each parameter tensor) <= 2e-5
   g = 1 multi-step weights (8 steps)           <= 1e-4
   g > 1 deterministic schedule                 event log exact, weights <= 1e-4
-TF32 mode (the throughput path): gradient <= 2e-2, reported only.
+TF32 mode (the throughput path): gradient <= 5e-2, reported only.
 """
 
 import os
@@ -120,6 +120,22 @@ def test_simulate_deterministic_vs_reference():
 NETS = [("lenet", 6, {}), ("cifar10_quick", 4, {}), ("caffenet", 2, {})]
 
 
+def scaled_weights(net, seed):
+    """N(0, 2/fan_in) weights (He scaling) so every layer of a deep net carries
+    O(1) activations and the comparison is not dominated by saturation."""
+    rng = np.random.default_rng(seed)
+    W = np.zeros(net.dim)
+    for geo in net.geometry():
+        woff, boff = geo.param_offsets
+        wsz, bsz = geo.param_sizes
+        if wsz:
+            fan_in = wsz // geo.layer.d_out
+            W[woff:woff + wsz] = rng.standard_normal(wsz) * np.sqrt(2.0 / fan_in)
+        if bsz:
+            W[boff:boff + bsz] = 0.1 * rng.standard_normal(bsz)
+    return W
+
+
 def per_param_errors(net, g, ref):
     errs = []
     for geo in net.geometry():
@@ -133,8 +149,7 @@ def per_param_errors(net, g, ref):
 def test_network_grad_vs_oracle(name, b, kw):
     net = nets.get(name)
     prob = CNNProblem(net, n_examples=max(16, b), seed=1, precision="3xtf32")
-    rng = np.random.default_rng(7)
-    W = 0.05 * rng.standard_normal(net.dim)   # larger than 0.01 so deep layers carry signal
+    W = scaled_weights(net, seed=7)
     batch = prob.sample_batch(P.batch_stream(2), b)
     if prob.images is not None:
         X, y = batch
@@ -153,7 +168,7 @@ def test_network_grad_vs_oracle(name, b, kw):
     # tf32 (throughput) mode, reported with a loose bound
     p32 = CNNProblem(net, n_examples=max(16, b), seed=1, precision="tf32")
     g32 = p32.grad(W, batch)
-    assert nrel(g32, ref) < 2e-2
+    assert nrel(g32, ref) < 5e-2
 
 
 def test_full_grad_and_chunked_loss():
