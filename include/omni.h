@@ -61,9 +61,11 @@ int omni_lift_nchw_f64(const double* Rhat, long long ld, int b, int m, int d_out
 /* col2im (adjoint of omni_lower_nhwc_f32), deterministic gather form: dX (NHWC,
  * pixel stride cs) is OVERWRITTEN with the sum over every lowered entry that
  * copied from it.  Not in the reference (its only conv is layer 1, so
- * problems.py:263-269 never needs dX); pinned by the adjoint identity.     */
+ * problems.py:263-269 never needs dX); pinned by the adjoint identity.
+ * relu_mask_x (NHWC like dX, may be NULL) fuses the ReLU backward mask of the
+ * layer that produced X: dX = col2im(dDhat) * (X > 0) (problems.py:261).    */
 int omni_col2im_nhwc_f32(const float* dDhat, long long ld, int b, int n, int c, int cs, int k,
-                         int stride, int pad, float* dX, void* stream);
+                         int stride, int pad, const float* relu_mask_x, float* dX, void* stream);
 
 /* ---------------------------------------------------------------- K2 --
  * C[i,j] (op)= sum_r A(i,r) * B(j,r),  i < M, j < N, r < K, where

@@ -47,7 +47,7 @@ SIGNATURES: dict[str, tuple] = {
     "omni_lower_nhwc_f32": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P]),
     "omni_lift_nchw_f32": (_I, [_P, _L, _I, _I, _I, _P, _P]),
     "omni_lift_nchw_f64": (_I, [_P, _L, _I, _I, _I, _P, _P]),
-    "omni_col2im_nhwc_f32": (_I, [_P, _L, _I, _I, _I, _I, _I, _I, _I, _P, _P]),
+    "omni_col2im_nhwc_f32": (_I, [_P, _L, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
     "omni_gemm_plan": (_L, [_I, _I, _I, _I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "omni_gemm_f32": (
         _I,

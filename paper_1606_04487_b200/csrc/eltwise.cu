@@ -10,6 +10,8 @@ namespace {
 
 constexpr int kThreads = 256;
 
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
 __host__ __device__ inline int pool_out(int n, int k, int s, int p, int ceil_mode) {
   const int span = n + 2 * p - k;
   int out = (ceil_mode ? (span + s - 1) / s : span / s) + 1;
@@ -18,85 +20,151 @@ __host__ __device__ inline int pool_out(int n, int k, int s, int p, int ceil_mod
   return out;
 }
 
-// One thread per (img, oy, ox, ch).  Max: first maximum in (dy, dx) order,
-// argmax = iy*w + ix (problems.py:213-216).  Avg: Caffe divisor.
-template <int MODE>
+// One thread per (img, oy, ox, channel group of V).  Max: first maximum in
+// (dy, dx) order, argmax = iy*w + ix (problems.py:213-216).  Avg: Caffe
+// divisor.  V = 4 uses float4/int4 accesses (c, cs_in, cs_out multiples of 4).
+template <int MODE, int V>
 __global__ void __launch_bounds__(kThreads) pool_fwd_kernel(
     const float* __restrict__ X, int b, int h, int w, int c, int cs_in, int k, int s, int p,
     int oh, int ow, float* __restrict__ Y, int cs_out, int32_t* __restrict__ argmax) {
-  const long long total = (long long)b * oh * ow * c;
-  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long opix = idx / c;
-    const int ch = (int)(idx - opix * c);
-    const int img = (int)(opix / (oh * ow));
-    const int r = (int)(opix - (long long)img * oh * ow);
+  const int cv = c / V;
+  const int total = b * oh * ow * cv;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int opix = idx / cv;
+    const int ch = (idx - opix * cv) * V;
+    const int img = opix / (oh * ow);
+    const int r = opix - img * oh * ow;
     const int oy = r / ow, ox = r - (r / ow) * ow;
     int hs = oy * s - p, ws = ox * s - p;
     int he = min(hs + k, h + p), we = min(ws + k, w + p);
-    const int pool_size = (he - hs) * (we - ws);
+    const float inv = 1.f / (float)((he - hs) * (we - ws));
     hs = max(hs, 0);
     ws = max(ws, 0);
     he = min(he, h);
     we = min(we, w);
     const float* Xi = X + (long long)img * h * w * cs_in + ch;
-    if (MODE == 0) {
-      float best = Xi[((long long)hs * w + ws) * cs_in];
-      int arg = hs * w + ws;
-      for (int iy = hs; iy < he; ++iy)
-        for (int ix = ws; ix < we; ++ix) {
-          const float v = Xi[((long long)iy * w + ix) * cs_in];
-          if (v > best) {
-            best = v;
-            arg = iy * w + ix;
+    float best[V], acc[V];
+    int arg[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      best[v] = -INFINITY;
+      acc[v] = 0.f;
+      arg[v] = hs * w + ws;
+    }
+    bool first = true;
+    for (int iy = hs; iy < he; ++iy)
+      for (int ix = ws; ix < we; ++ix) {
+        const float* src = Xi + (iy * w + ix) * cs_in;
+        float val[V];
+        if (V == 4) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(src));
+          val[0] = t.x; val[1] = t.y; val[2 % V] = t.z; val[3 % V] = t.w;
+        } else {
+          val[0] = __ldg(src);
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          if (MODE == 0) {
+            if (first || val[v] > best[v]) {
+              best[v] = val[v];
+              arg[v] = iy * w + ix;
+            }
+          } else {
+            acc[v] += val[v];
           }
         }
-      Y[opix * cs_out + ch] = best;
-      if (argmax) argmax[idx] = arg;
+        first = false;
+      }
+    float* dst = Y + (long long)opix * cs_out + ch;
+    if (MODE == 0) {
+      if (V == 4) {
+        *reinterpret_cast<float4*>(dst) = make_float4(best[0], best[1 % V], best[2 % V], best[3 % V]);
+        *reinterpret_cast<int4*>(argmax + (long long)opix * c + ch) =
+            make_int4(arg[0], arg[1 % V], arg[2 % V], arg[3 % V]);
+      } else {
+        dst[0] = best[0];
+        argmax[(long long)opix * c + ch] = arg[0];
+      }
     } else {
-      float acc = 0.f;
-      for (int iy = hs; iy < he; ++iy)
-        for (int ix = ws; ix < we; ++ix) acc += Xi[((long long)iy * w + ix) * cs_in];
-      Y[opix * cs_out + ch] = acc / (float)pool_size;
+      if (V == 4)
+        *reinterpret_cast<float4*>(dst) =
+            make_float4(acc[0] * inv, acc[1 % V] * inv, acc[2 % V] * inv, acc[3 % V] * inv);
+      else
+        dst[0] = acc[0] * inv;
     }
   }
 }
 
 // Gather-form backward: each input pixel sums the output gradients of the
-// windows that contain it, in ascending (oy, ox) order.
-template <int MODE>
+// windows that contain it, in ascending (oy, ox) order; fused ReLU mask.
+template <int MODE, int V>
 __global__ void __launch_bounds__(kThreads) pool_bwd_kernel(
     const float* __restrict__ dY, int b, int h, int w, int c, int cs_in, int k, int s, int p,
     int oh, int ow, int cs_out, const int32_t* __restrict__ argmax, const float* __restrict__ X,
     int relu_mask_x, float* __restrict__ dX) {
-  const long long total = (long long)b * h * w * c;
-  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long pix = idx / c;
-    const int ch = (int)(idx - pix * c);
-    const int img = (int)(pix / (h * w));
-    const int r = (int)(pix - (long long)img * h * w);
+  const int cv = c / V;
+  const int total = b * h * w * cv;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int pix = idx / cv;
+    const int ch = (idx - pix * cv) * V;
+    const int img = pix / (h * w);
+    const int r = pix - img * h * w;
     const int iy = r / w, ix = r - (r / w) * w;
     const int oy0 = (iy + p < k) ? 0 : (iy + p - k) / s + 1;
     const int oy1 = min((iy + p) / s + 1, oh);
     const int ox0 = (ix + p < k) ? 0 : (ix + p - k) / s + 1;
     const int ox1 = min((ix + p) / s + 1, ow);
-    const long long obase = (long long)img * oh * ow;
-    float acc = 0.f;
+    const int obase = img * oh * ow;
+    const int me = iy * w + ix;
+    float acc[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = 0.f;
     for (int oy = oy0; oy < oy1; ++oy)
       for (int ox = ox0; ox < ox1; ++ox) {
-        const long long o = obase + (long long)oy * ow + ox;
-        if (MODE == 0) {
-          if (argmax[o * c + ch] == iy * w + ix) acc += dY[o * cs_out + ch];
+        const int o = obase + oy * ow + ox;
+        float g[V];
+        if (V == 4) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(dY + (long long)o * cs_out + ch));
+          g[0] = t.x; g[1 % V] = t.y; g[2 % V] = t.z; g[3 % V] = t.w;
         } else {
-          int hs = oy * s - p, ws = ox * s - p;
+          g[0] = __ldg(dY + (long long)o * cs_out + ch);
+        }
+        if (MODE == 0) {
+          int a[V];
+          if (V == 4) {
+            const int4 t = __ldg(reinterpret_cast<const int4*>(argmax + (long long)o * c + ch));
+            a[0] = t.x; a[1 % V] = t.y; a[2 % V] = t.z; a[3 % V] = t.w;
+          } else {
+            a[0] = __ldg(argmax + (long long)o * c + ch);
+          }
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            if (a[v] == me) acc[v] += g[v];
+        } else {
+          const int hs = oy * s - p, ws = ox * s - p;
           const int he = min(hs + k, h + p), we = min(ws + k, w + p);
-          const int pool_size = (he - hs) * (we - ws);
-          acc += dY[o * cs_out + ch] / (float)pool_size;
+          const float inv = 1.f / (float)((he - hs) * (we - ws));
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[v] += g[v] * inv;
         }
       }
-    if (relu_mask_x && !(X[pix * cs_in + ch] > 0.f)) acc = 0.f;
-    dX[pix * cs_in + ch] = acc;
+    float* dst = dX + (long long)pix * cs_in + ch;
+    if (relu_mask_x) {
+      const float* xm = X + (long long)pix * cs_in + ch;
+      if (V == 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(xm));
+        acc[0] = t.x > 0.f ? acc[0] : 0.f;
+        acc[1 % V] = t.y > 0.f ? acc[1 % V] : 0.f;
+        acc[2 % V] = t.z > 0.f ? acc[2 % V] : 0.f;
+        acc[3 % V] = t.w > 0.f ? acc[3 % V] : 0.f;
+      } else {
+        acc[0] = __ldg(xm) > 0.f ? acc[0] : 0.f;
+      }
+    }
+    if (V == 4)
+      *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1 % V], acc[2 % V], acc[3 % V]);
+    else
+      dst[0] = acc[0];
   }
 }
 
@@ -266,8 +334,6 @@ __global__ void fill_kernel(float* X, float v, long long n) {
     X[i] = v;
 }
 
-bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
-
 }  // namespace
 
 extern "C" {
@@ -288,13 +354,20 @@ int omni_pool_fwd_nhwc_f32(int mode, const float* X, int b, int h, int w, int c,
   const int oh = pool_out(h, k, stride, pad, ceil_mode), ow = pool_out(w, k, stride, pad, ceil_mode);
   const long long work = (long long)b * oh * ow * c;
   if (work == 0) return OMNI_OK;
+  OMNI_REQUIRE((long long)b * h * w * cs_in < (1LL << 31) && work < (1LL << 31),
+               "pool: tensor too large for 32-bit indexing");
   cudaStream_t st = omni::as_stream(stream);
-  if (mode == 0)
-    pool_fwd_kernel<0><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(
-        X, b, h, w, c, cs_in, k, stride, pad, oh, ow, Y, cs_out, argmax);
-  else
-    pool_fwd_kernel<1><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(
-        X, b, h, w, c, cs_in, k, stride, pad, oh, ow, Y, cs_out, argmax);
+  const bool v4 = c % 4 == 0 && cs_in % 4 == 0 && cs_out % 4 == 0 && aligned16(X) && aligned16(Y) &&
+                  (mode == 1 || aligned16(argmax));
+  const int grid = omni::grid_for(v4 ? work / 4 : work, kThreads);
+#define OMNI_POOL_FWD(M, V) \
+  pool_fwd_kernel<M, V><<<grid, kThreads, 0, st>>>(X, b, h, w, c, cs_in, k, stride, pad, oh, ow, Y, cs_out, argmax)
+  if (mode == 0) {
+    if (v4) OMNI_POOL_FWD(0, 4); else OMNI_POOL_FWD(0, 1);
+  } else {
+    if (v4) OMNI_POOL_FWD(1, 4); else OMNI_POOL_FWD(1, 1);
+  }
+#undef OMNI_POOL_FWD
   return omni::check_launch("pool_fwd");
 }
 
@@ -310,13 +383,20 @@ int omni_pool_bwd_nhwc_f32(int mode, const float* dY, int b, int h, int w, int c
   const int oh = pool_out(h, k, stride, pad, ceil_mode), ow = pool_out(w, k, stride, pad, ceil_mode);
   const long long work = (long long)b * h * w * c;
   if (work == 0) return OMNI_OK;
+  OMNI_REQUIRE((long long)b * h * w * cs_in < (1LL << 31), "pool: tensor too large for 32-bit indexing");
   cudaStream_t st = omni::as_stream(stream);
-  if (mode == 0)
-    pool_bwd_kernel<0><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(
-        dY, b, h, w, c, cs_in, k, stride, pad, oh, ow, cs_out, argmax, X, relu_mask_x, dX);
-  else
-    pool_bwd_kernel<1><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(
-        dY, b, h, w, c, cs_in, k, stride, pad, oh, ow, cs_out, argmax, X, relu_mask_x, dX);
+  const bool v4 = c % 4 == 0 && cs_in % 4 == 0 && cs_out % 4 == 0 && aligned16(dY) && aligned16(dX) &&
+                  (mode == 1 || aligned16(argmax)) && (!relu_mask_x || aligned16(X));
+  const int grid = omni::grid_for(v4 ? work / 4 : work, kThreads);
+#define OMNI_POOL_BWD(M, V)                                                                     \
+  pool_bwd_kernel<M, V><<<grid, kThreads, 0, st>>>(dY, b, h, w, c, cs_in, k, stride, pad, oh, ow, \
+                                                   cs_out, argmax, X, relu_mask_x, dX)
+  if (mode == 0) {
+    if (v4) OMNI_POOL_BWD(0, 4); else OMNI_POOL_BWD(0, 1);
+  } else {
+    if (v4) OMNI_POOL_BWD(1, 4); else OMNI_POOL_BWD(1, 1);
+  }
+#undef OMNI_POOL_BWD
   return omni::check_launch("pool_bwd");
 }
 

@@ -24,6 +24,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <stdlib.h>
+#include <string.h>
+
 #include <mutex>
 
 #include "common.cuh"
@@ -38,7 +41,8 @@ struct Params {
   int m_tiles, n_tiles, k_tiles, splits, kt_per_split;
   int raster_m_inner;
   int epilogue;
-  int vec_ok;  // C row stride % 4 == 0 and C 16-byte aligned
+  int vec_ok;         // C row stride % 4 == 0 and C 16-byte aligned
+  int use_tma_store;  // epilogue stages 32x32 sub-tiles in smem and TMA-stores them
   float* C;
   long long ldc;
   long long split_stride;  // elements between split-K partial outputs
@@ -53,9 +57,11 @@ struct Layout {
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGE_ALL = SPLIT3 ? 2 * STAGE : STAGE;
-  static constexpr int BUDGET = 220 * 1024;
+  static constexpr int STG_BYTES = 4 * 2 * 32 * 32 * 4;  // 4 epilogue warps x 2 x (32x32 fp32)
+  static constexpr int BUDGET = 232448 - STG_BYTES - 256 - 1024;  // 227 KiB opt-in maximum
   static constexpr int STAGES = (BUDGET / STAGE_ALL) > 8 ? 8 : (BUDGET / STAGE_ALL);
-  static constexpr int BAR_OFF = STAGES * STAGE_ALL;
+  static constexpr int STG_OFF = STAGES * STAGE_ALL;
+  static constexpr int BAR_OFF = STG_OFF + STG_BYTES;
   static constexpr int BYTES = BAR_OFF + 256 + 1024;  // barriers + 1 KiB alignment slack
   static constexpr int TMEM_COLS = 2 * BN <= 32    ? 32
                                    : 2 * BN <= 64  ? 64
@@ -100,6 +106,29 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint32_t dst
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1,
+                                             int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(src), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
 }
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -190,7 +219,8 @@ __device__ __forceinline__ float epi_apply(int mode, float acc, const Params& p,
 template <int BN, bool A_MN, bool B_MN, bool SPLIT3>
 __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA,
-                     const __grid_constant__ CUtensorMap tmB, const Params p) {
+                     const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmC, const Params p) {
   using L = Layout<BN, SPLIT3>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -209,6 +239,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (p.use_tma_store) tma_prefetch_desc(&tmC);
     for (int s = 0; s < L::STAGES; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
@@ -323,6 +354,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     const int mode = p.splits > 1 ? OMNI_EPI_STORE : p.epilogue;
+    int st_chunk = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int mt, nt, sp;
       decode_work(p, w, mt, nt, sp);
@@ -331,6 +363,47 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
       const int row = mt * BM + ew * 32 + lane;
       const uint32_t t_row =
           tmem_base + (uint32_t)(acc * L::ACC_STRIDE) + ((uint32_t)(ew * 32) << 16);
+      if (p.use_tma_store) {
+        // 32 x 32 sub-tiles: registers -> 128B-swizzled smem -> TMA bulk store
+        // (coalesced, clipped at the M/N edges by the tensor map).
+        const uint32_t stg = sbase + L::STG_OFF + ew * 8192;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          const int col0 = nt * BN + c0;
+          if (col0 >= p.N) break;  // warp-uniform
+          uint32_t r[32];
+          tmem_ld16(t_row + (uint32_t)c0, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+          tmem_ld16(t_row + (uint32_t)c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
+          tmem_wait_ld();
+          if (c0 + 32 >= BN || col0 + 32 >= p.N) {
+            // last TMEM read of this accumulator: hand it back to the MMA warp early
+            tc_fence_before();
+            mbar_arrive(tempty_bar(acc));
+          }
+          const uint32_t buf = stg + (uint32_t)(st_chunk & 1) * 4096u;
+          if (lane == 0) bulk_wait_read<1>();  // the store that last used `buf` has read it
+          __syncwarp();
+          const float* Crow_unused = nullptr;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float v0 = epi_apply(mode, __uint_as_float(r[4 * j + 0]), p, row, col0 + 4 * j + 0, Crow_unused);
+            float v1 = epi_apply(mode, __uint_as_float(r[4 * j + 1]), p, row, col0 + 4 * j + 1, Crow_unused);
+            float v2 = epi_apply(mode, __uint_as_float(r[4 * j + 2]), p, row, col0 + 4 * j + 2, Crow_unused);
+            float v3 = epi_apply(mode, __uint_as_float(r[4 * j + 3]), p, row, col0 + 4 * j + 3, Crow_unused);
+            st_shared_v4(buf + (uint32_t)lane * 128u + ((uint32_t)(j ^ (lane & 7)) << 4), v0, v1, v2, v3);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tmC, buf, col0, mt * BM + ew * 32, sp);
+            bulk_commit();
+          }
+          ++st_chunk;
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        continue;
+      }
       float* Crow = p.C + (long long)sp * p.split_stride + (long long)row * p.ldc;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -363,6 +436,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (p.use_tma_store && lane == 0) bulk_wait_all();
   } else if (SPLIT3 && warp >= 8) {
     // ------------------------------------------- 3xTF32 hi/lo converters --
     const int t = threadIdx.x - 256;
@@ -469,6 +543,27 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+int make_tmap_c(CUtensorMap* map, const float* ptr, long long N, long long M, long long ld,
+                long long splits, long long split_stride) {
+  auto fn = encode_fn();
+  if (!fn) {
+    omni::set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+    return OMNI_ECUDA;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)splits};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)(split_stride > 0 ? split_stride : M * ld) * 4};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    omni::set_error("cuTensorMapEncodeTiled (C) failed (%d): N=%lld M=%lld ld=%lld", (int)r, N, M, ld);
+    return OMNI_ECUDA;
+  }
+  return OMNI_OK;
+}
+
 int make_tmap(CUtensorMap* map, const float* ptr, long long inner, long long outer, long long ld,
               int box_inner, int box_outer, bool mn_major) {
   auto fn = encode_fn();
@@ -546,9 +641,15 @@ int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, lon
   rc = B_MN ? make_tmap(&tb, B, p.N, p.K, ldb, 32, BK, true)
             : make_tmap(&tb, B, p.K, p.N, ldb, 32, BN, false);
   if (rc) return rc;
+  CUtensorMap tc;
+  memset(&tc, 0, sizeof(tc));
+  if (p.use_tma_store) {
+    rc = make_tmap_c(&tc, p.C, p.N, p.M, p.ldc, p.splits, p.split_stride);
+    if (rc) return rc;
+  }
   auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT3>;
   OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
-  kern<<<pl.grid, L::THREADS, L::BYTES, st>>>(ta, tb, p);
+  kern<<<pl.grid, L::THREADS, L::BYTES, st>>>(ta, tb, tc, p);
   return omni::check_launch("gemm_tf32");
 }
 
@@ -656,12 +757,15 @@ int omni_gemm_f32(int precision, int M, int N, int K, const float* A, long long 
     p.ldc = N;
     p.split_stride = (long long)M * N;
     p.vec_ok = (N % 4 == 0);
+    p.use_tma_store = (N % 4 == 0);
   } else {
     p.C = C;
     p.ldc = ldc;
     p.split_stride = 0;
     p.vec_ok = (ldc % 4 == 0) && (((uintptr_t)C & 15) == 0);
+    p.use_tma_store = p.vec_ok && epilogue != OMNI_EPI_ACCUM;
   }
+  if (getenv("OMNI_NO_TMA_STORE")) p.use_tma_store = 0;
   const int b_mn = b_mn_major ? 1 : 0;
   int rc = precision == OMNI_PREC_3XTF32
                ? gemm::dispatch_major<true>(pl, a_mn_major, b_mn, A, lda, B, ldb, p, st)

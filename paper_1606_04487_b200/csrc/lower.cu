@@ -54,51 +54,56 @@ __global__ void __launch_bounds__(kThreads) lower_nchw_kernel(
 }
 
 // Tap-major lowering from NHWC (pixel stride cs): col = (kx*k + ky)*c + ch.
-// VEC4: c, cs, ld all multiples of 4, so one float4 load feeds one float4 store.
-template <bool VEC4>
-__global__ void __launch_bounds__(kThreads) lower_nhwc_kernel(
+// One warp per lowered row (img, x, y).  For fixed kx the k taps ky = 0..k-1
+// read consecutive input pixels iy0 + ky, so when cs == c the row is k
+// contiguous runs of k*c floats copied from k input rows: coalesced loads,
+// one contiguous 4*ld-byte store per warp.  VEC4 (c % 4 == 0): float4 lanes.
+// With a padded pixel stride (cs > c) the runs break per tap (PER_TAP).
+template <bool VEC4, bool PER_TAP>
+__global__ void __launch_bounds__(kThreads) lower_nhwc_rows_kernel(
     const float* __restrict__ X, int n, int c, int cs, int k, int s, int p, int m,
-    long long rows, int K, long long ld, float* __restrict__ Dhat) {
-  const long long cols_v = ld / 4;
-  const long long total = rows * cols_v;
+    int rows, int K, int ld, float* __restrict__ Dhat) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
   const int mm = m * m;
-  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long row = idx / cols_v;
-    const int col0 = (int)(idx - row * cols_v) * 4;
-    const int img = (int)(row / mm);
-    const int rem = (int)(row - (long long)img * mm);
+  const int kc = k * c;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += warps) {
+    const int img = row / mm;
+    const int rem = row - img * mm;
     const int x = rem / m, y = rem - (rem / m) * m;
+    const int iy0 = y * s - p;
+    float* out = Dhat + (long long)row * ld;
     const float* Ximg = X + (long long)img * n * n * cs;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if constexpr (VEC4) {
-      if (col0 < K) {
-        const int tap = col0 / c;
-        const int ch = col0 - tap * c;
-        const int kx = tap / k, ky = tap - (tap / k) * k;
-        const int ix = x * s + kx - p, iy = y * s + ky - p;
-        if ((unsigned)ix < (unsigned)n && (unsigned)iy < (unsigned)n)
-          v = __ldg(reinterpret_cast<const float4*>(Ximg + ((long long)ix * n + iy) * cs + ch));
-      }
-    } else {
-      float t4[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int col = col0 + j;
-        float val = 0.f;
-        if (col < K) {
-          const int tap = col / c;
-          const int ch = col - tap * c;
-          const int kx = tap / k, ky = tap - (tap / k) * k;
-          const int ix = x * s + kx - p, iy = y * s + ky - p;
-          if ((unsigned)ix < (unsigned)n && (unsigned)iy < (unsigned)n)
-            val = __ldg(Ximg + ((long long)ix * n + iy) * cs + ch);
+    for (int kx = 0; kx < k; ++kx) {
+      const int ix = x * s + kx - p;
+      const bool row_ok = (unsigned)ix < (unsigned)n;
+      const float* src = Ximg + ((long long)ix * n + iy0) * cs;  // pixel iy0 of input row ix
+      float* dst = out + kx * kc;
+      if constexpr (VEC4 && !PER_TAP) {
+        const int c4 = c >> 2;
+        for (int q = lane; q < (kc >> 2); q += 32) {
+          const int ky = q / c4;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (row_ok && (unsigned)(iy0 + ky) < (unsigned)n)
+            v = __ldg(reinterpret_cast<const float4*>(src) + q);
+          reinterpret_cast<float4*>(dst)[q] = v;
         }
-        t4[j] = val;
+      } else if constexpr (!PER_TAP) {
+        for (int j = lane; j < kc; j += 32) {
+          const int ky = j / c;
+          float v = 0.f;
+          if (row_ok && (unsigned)(iy0 + ky) < (unsigned)n) v = __ldg(src + j);
+          dst[j] = v;
+        }
+      } else {
+        for (int ky = 0; ky < k; ++ky) {
+          const bool ok = row_ok && (unsigned)(iy0 + ky) < (unsigned)n;
+          for (int ch = lane; ch < c; ch += 32)
+            dst[ky * c + ch] = ok ? __ldg(src + (long long)ky * cs + ch) : 0.f;
+        }
       }
-      v = make_float4(t4[0], t4[1], t4[2], t4[3]);
     }
-    *reinterpret_cast<float4*>(Dhat + row * ld + col0) = v;
+    for (int j = K + lane; j < ld; j += 32) out[j] = 0.f;
   }
 }
 
@@ -109,7 +114,7 @@ __global__ void __launch_bounds__(kThreads) lower_nhwc_kernel(
 template <bool VEC4>
 __global__ void __launch_bounds__(kThreads) col2im_nhwc_kernel(
     const float* __restrict__ dD, long long ld, int b, int n, int c, int cs, int k, int s, int p,
-    int m, float* __restrict__ dX) {
+    int m, const float* __restrict__ mask_x, float* __restrict__ dX) {
   const int cv = VEC4 ? c / 4 : c;
   const long long total = (long long)b * n * n * cv;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -144,6 +149,16 @@ __global__ void __launch_bounds__(kThreads) col2im_nhwc_kernel(
       }
     }
     float* dst = dX + pix * cs + ch;
+    if (mask_x) {  // fused ReLU backward: gradient flows only where the activation is > 0
+      const float* mx = mask_x + pix * cs + ch;
+      if constexpr (VEC4) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(mx));
+        acc.x = a.x > 0.f ? acc.x : 0.f; acc.y = a.y > 0.f ? acc.y : 0.f;
+        acc.z = a.z > 0.f ? acc.z : 0.f; acc.w = a.w > 0.f ? acc.w : 0.f;
+      } else {
+        acc.x = __ldg(mx) > 0.f ? acc.x : 0.f;
+      }
+    }
     if constexpr (VEC4) *reinterpret_cast<float4*>(dst) = acc;
     else *dst = acc.x;
   }
@@ -275,19 +290,23 @@ int omni_lower_nhwc_f32(const float* X, int b, int n, int c, int cs, int k, int 
   if (rc) return rc;
   const int K = c * k * k;
   OMNI_REQUIRE(cs >= c, "pixel stride cs=%d < channels %d", cs, c);
-  OMNI_REQUIRE(ld >= K && ld % 4 == 0, "ld=%lld must be >= %d and a multiple of 4", ld, K);
+  OMNI_REQUIRE(ld >= K && ld % 4 == 0 && ld < (1LL << 31), "ld=%lld must be >= %d and a multiple of 4",
+               ld, K);
   OMNI_REQUIRE((uintptr_t)Dhat % 16 == 0, "Dhat must be 16-byte aligned");
   if (b == 0) return OMNI_OK;
   const long long rows = (long long)b * m * m;
+  OMNI_REQUIRE(rows < (1LL << 31), "too many lowered rows");
   cudaStream_t st = omni::as_stream(stream);
-  const bool v4 = (c % 4 == 0) && (cs % 4 == 0) && ((uintptr_t)X % 16 == 0);
-  const int grid = omni::grid_for(rows * ld / 4, kThreads);
-  if (v4)
-    lower_nhwc_kernel<true><<<grid, kThreads, 0, st>>>(X, n, c, cs, k, stride, pad, m, rows, K,
-                                                       ld, Dhat);
+  const int grid = omni::grid_for(rows * 32, kThreads);
+  if (cs == c && c % 4 == 0 && ((uintptr_t)X % 16 == 0))
+    lower_nhwc_rows_kernel<true, false><<<grid, kThreads, 0, st>>>(X, n, c, cs, k, stride, pad, m,
+                                                                  (int)rows, K, (int)ld, Dhat);
+  else if (cs == c)
+    lower_nhwc_rows_kernel<false, false><<<grid, kThreads, 0, st>>>(X, n, c, cs, k, stride, pad, m,
+                                                                   (int)rows, K, (int)ld, Dhat);
   else
-    lower_nhwc_kernel<false><<<grid, kThreads, 0, st>>>(X, n, c, cs, k, stride, pad, m, rows, K,
-                                                        ld, Dhat);
+    lower_nhwc_rows_kernel<false, true><<<grid, kThreads, 0, st>>>(X, n, c, cs, k, stride, pad, m,
+                                                                  (int)rows, K, (int)ld, Dhat);
   return omni::check_launch("lower_nhwc");
 }
 
@@ -309,7 +328,7 @@ int omni_lift_nchw_f64(const double* Rhat, long long ld, int b, int m, int d_out
 }
 
 int omni_col2im_nhwc_f32(const float* dDhat, long long ld, int b, int n, int c, int cs, int k,
-                         int stride, int pad, float* dX, void* stream) {
+                         int stride, int pad, const float* relu_mask_x, float* dX, void* stream) {
   int m = 0;
   int rc = check_conv_geom(b, c, n, k, stride, pad, &m);
   if (rc) return rc;
@@ -317,14 +336,15 @@ int omni_col2im_nhwc_f32(const float* dDhat, long long ld, int b, int n, int c, 
   if (b == 0) return OMNI_OK;
   cudaStream_t st = omni::as_stream(stream);
   const bool v4 = (c % 4 == 0) && (cs % 4 == 0) && (ld % 4 == 0) &&
-                  ((uintptr_t)dX % 16 == 0) && ((uintptr_t)dDhat % 16 == 0);
+                  ((uintptr_t)dX % 16 == 0) && ((uintptr_t)dDhat % 16 == 0) &&
+                  ((uintptr_t)relu_mask_x % 16 == 0);
   const long long work = (long long)b * n * n * (v4 ? c / 4 : c);
   if (v4)
     col2im_nhwc_kernel<true><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(
-        dDhat, ld, b, n, c, cs, k, stride, pad, m, dX);
+        dDhat, ld, b, n, c, cs, k, stride, pad, m, relu_mask_x, dX);
   else
     col2im_nhwc_kernel<false><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(
-        dDhat, ld, b, n, c, cs, k, stride, pad, m, dX);
+        dDhat, ld, b, n, c, cs, k, stride, pad, m, relu_mask_x, dX);
   return omni::check_launch("col2im_nhwc");
 }
 

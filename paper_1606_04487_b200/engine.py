@@ -308,11 +308,7 @@ class GpuNet:
                 self._gemm(Mr, op.Kc, d, dZ, op.out.cs, False, op.wstage, op.ldK, True, self.ddhat,
                            op.ldK)
                 K.col2im_nhwc(self.ddhat, op.ldK, b, op.inp.n, op.c_in, op.inp.cs, op.k, op.s, op.p,
-                              op.inp.grad)
-                if op.inp.fused_relu:
-                    n = b * op.inp.grad[0].numel()
-                    K.relu_bwd(op.inp.grad.view(-1)[:n], op.inp.value.view(-1)[:n],
-                               op.inp.grad.view(-1)[:n])
+                              op.inp.grad, op.inp.value if op.inp.fused_relu else None)
             elif op.kind == "pool":
                 if op.inp.grad is None:
                     continue
@@ -354,7 +350,7 @@ class GpuNet:
                 n += 1 + 1       # wgrad gemm, inverse stage
                 n += 2 if op.boff >= 0 else 0
                 if not op.first_param_layer:
-                    n += 2 + (1 if op.inp.fused_relu else 0)
+                    n += 2
             elif op.kind == "fc":
                 n += 1 + 1 + (1 if op.flat is not op.inp else 0)
                 n += 1 + (2 if op.boff >= 0 else 0)

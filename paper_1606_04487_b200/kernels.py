@@ -72,8 +72,10 @@ def lift_nchw(Rhat: torch.Tensor, b: int, m: int, d_out: int) -> torch.Tensor:
 
 
 def col2im_nhwc(dDhat: torch.Tensor, ld: int, b: int, n: int, c: int, cs: int, k: int,
-                stride: int, pad: int, dX: torch.Tensor) -> torch.Tensor:
-    call("omni_col2im_nhwc_f32", _ptr(dDhat), ld, b, n, c, cs, k, stride, pad, _ptr(dX), _stream())
+                stride: int, pad: int, dX: torch.Tensor,
+                relu_mask: torch.Tensor | None = None) -> torch.Tensor:
+    call("omni_col2im_nhwc_f32", _ptr(dDhat), ld, b, n, c, cs, k, stride, pad, _ptr(relu_mask),
+         _ptr(dX), _stream())
     return dX
 
 
