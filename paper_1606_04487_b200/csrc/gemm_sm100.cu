@@ -204,15 +204,47 @@ __device__ __forceinline__ void decode_work(const Params& p, int w, int& mt, int
   }
 }
 
+template <int MODE>
+__device__ __forceinline__ float epi_one(float acc, const Params& p, int row, int col,
+                                         const float* Crow) {
+  if (MODE == OMNI_EPI_BIAS) return acc + __ldg(p.bias + col);
+  if (MODE == OMNI_EPI_BIAS_RELU) return fmaxf(acc + __ldg(p.bias + col), 0.f);
+  if (MODE == OMNI_EPI_ACCUM) return Crow[col] + acc;
+  if (MODE == OMNI_EPI_MASK_AUX) return __ldg(p.aux + (long long)row * p.ld_aux + col) > 0.f ? acc : 0.f;
+  if (MODE == OMNI_EPI_RELU) return fmaxf(acc, 0.f);
+  return acc;
+}
+
+// Runtime-mode wrapper for the (rare) scalar paths.
 __device__ __forceinline__ float epi_apply(int mode, float acc, const Params& p, int row, int col,
                                            const float* Crow) {
   switch (mode) {
-    case OMNI_EPI_BIAS: return acc + __ldg(p.bias + col);
-    case OMNI_EPI_BIAS_RELU: return fmaxf(acc + __ldg(p.bias + col), 0.f);
-    case OMNI_EPI_ACCUM: return Crow[col] + acc;
-    case OMNI_EPI_MASK_AUX: return __ldg(p.aux + (long long)row * p.ld_aux + col) > 0.f ? acc : 0.f;
-    case OMNI_EPI_RELU: return fmaxf(acc, 0.f);
+    case OMNI_EPI_BIAS: return epi_one<OMNI_EPI_BIAS>(acc, p, row, col, Crow);
+    case OMNI_EPI_BIAS_RELU: return epi_one<OMNI_EPI_BIAS_RELU>(acc, p, row, col, Crow);
+    case OMNI_EPI_ACCUM: return epi_one<OMNI_EPI_ACCUM>(acc, p, row, col, Crow);
+    case OMNI_EPI_MASK_AUX: return epi_one<OMNI_EPI_MASK_AUX>(acc, p, row, col, Crow);
+    case OMNI_EPI_RELU: return epi_one<OMNI_EPI_RELU>(acc, p, row, col, Crow);
     default: return acc;
+  }
+}
+
+// Apply the epilogue to N consecutive columns held in registers; the mode
+// dispatch happens once per chunk, not per element.
+template <int MODE, int N>
+__device__ __forceinline__ void epi_chunk_t(float (&v)[N], const uint32_t* r, const Params& p,
+                                            int row, int col0) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) v[j] = epi_one<MODE>(__uint_as_float(r[j]), p, row, col0 + j, nullptr);
+}
+template <int N>
+__device__ __forceinline__ void epi_chunk(int mode, float (&v)[N], const uint32_t* r,
+                                          const Params& p, int row, int col0) {
+  switch (mode) {
+    case OMNI_EPI_BIAS: epi_chunk_t<OMNI_EPI_BIAS, N>(v, r, p, row, col0); break;
+    case OMNI_EPI_BIAS_RELU: epi_chunk_t<OMNI_EPI_BIAS_RELU, N>(v, r, p, row, col0); break;
+    case OMNI_EPI_MASK_AUX: epi_chunk_t<OMNI_EPI_MASK_AUX, N>(v, r, p, row, col0); break;
+    case OMNI_EPI_RELU: epi_chunk_t<OMNI_EPI_RELU, N>(v, r, p, row, col0); break;
+    default: epi_chunk_t<OMNI_EPI_STORE, N>(v, r, p, row, col0); break;
   }
 }
 
@@ -383,15 +415,12 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
           const uint32_t buf = stg + (uint32_t)(st_chunk & 1) * 4096u;
           if (lane == 0) bulk_wait_read<1>();  // the store that last used `buf` has read it
           __syncwarp();
-          const float* Crow_unused = nullptr;
+          float v[32];
+          epi_chunk<32>(mode, v, r, p, row, col0);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float v0 = epi_apply(mode, __uint_as_float(r[4 * j + 0]), p, row, col0 + 4 * j + 0, Crow_unused);
-            float v1 = epi_apply(mode, __uint_as_float(r[4 * j + 1]), p, row, col0 + 4 * j + 1, Crow_unused);
-            float v2 = epi_apply(mode, __uint_as_float(r[4 * j + 2]), p, row, col0 + 4 * j + 2, Crow_unused);
-            float v3 = epi_apply(mode, __uint_as_float(r[4 * j + 3]), p, row, col0 + 4 * j + 3, Crow_unused);
-            st_shared_v4(buf + (uint32_t)lane * 128u + ((uint32_t)(j ^ (lane & 7)) << 4), v0, v1, v2, v3);
-          }
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(buf + (uint32_t)lane * 128u + ((uint32_t)(j ^ (lane & 7)) << 4), v[4 * j],
+                         v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
@@ -415,9 +444,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
         if (row < p.M) {
           if (p.vec_ok && col0 + 16 <= p.N && mode != OMNI_EPI_ACCUM && mode != OMNI_EPI_MASK_AUX) {
             float v[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              v[j] = epi_apply(mode, __uint_as_float(r[j]), p, row, col0 + j, Crow);
+            epi_chunk<16>(mode, v, r, p, row, col0);
             float4* dst = reinterpret_cast<float4*>(Crow + col0);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
@@ -601,13 +628,26 @@ Plan make_plan(int M, int N, int K, int sms) {
         pl.bn = b;
         break;
       }
-  } else {
-    long long best = -1;
+  }
+  if (N > 192) {
+    // Prefer wide tiles (fewer re-reads of A, better MMA/epilogue ratio) unless
+    // they waste more than 8% of the MMA work on padding columns.
+    pl.bn = 0;
     for (int b : {256, 192, 128}) {
       const long long padded = omni::ceil_div(N, b) * b;
-      if (best < 0 || padded < best) {
-        best = padded;
+      if (padded * 100 <= (long long)N * 108) {
         pl.bn = b;
+        break;
+      }
+    }
+    if (!pl.bn) {
+      long long best = -1;
+      for (int b : {256, 192, 128}) {
+        const long long padded = omni::ceil_div(N, b) * b;
+        if (best < 0 || padded < best) {
+          best = padded;
+          pl.bn = b;
+        }
       }
     }
   }
