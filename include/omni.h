@@ -47,9 +47,12 @@ int omni_lower_nchw_f64(const double* D, int b, int c, int n, int k, int stride,
                         int start, int b_p, double* Dhat, long long ld, void* stream);
 /* Training-path lowering from NHWC activations (pixel stride cs >= c) with the
  * tap-major column order (kx*k + ky)*c + ch.  Same values as the reference's
- * lowered matrix up to that fixed column permutation.                      */
+ * lowered matrix up to that fixed column permutation.  ones_col != 0 writes
+ * 1.0 into column c*k*k (the bias column: with the bias staged in the same
+ * column of the weights, the GEMM adds the bias and the weight-gradient GEMM
+ * produces the bias gradient).                                             */
 int omni_lower_nhwc_f32(const float* X, int b, int n, int c, int cs, int k, int stride,
-                        int pad, float* Dhat, long long ld, void* stream);
+                        int pad, int ones_col, float* Dhat, long long ld, void* stream);
 
 /* Lifting: Rhat (b*m^2) x ld -> NCHW (b, d_out, m, m).  Replaces tensors.lift
  * (tensors.py:213-219); index remap only, bit-exact.                        */
@@ -140,9 +143,10 @@ int omni_gather_i32(const int32_t* src, const int64_t* idx, int nidx, int32_t* d
                     void* stream);
 /* Weight layout staging: OIHW (o,c,k,k) <-> tap-major (o, (kx*k+ky)*c + ch)
  * rows of stride ld (pad columns zeroed).  inverse=0 reads W and writes Wt;
- * inverse=1 reads Wt and writes W.                                           */
+ * inverse=1 reads Wt and writes W.  bias (may be NULL) travels in column
+ * c*k*k of Wt in the same direction.                                       */
 int omni_conv_weight_to_tap_f32(float* W, int o, int c, int k, float* Wt, long long ld,
-                                int inverse, void* stream);
+                                int inverse, float* bias, void* stream);
 /* Batched 2-D transpose: dst[bi][j*ldd + i] = src[bi][i*lds + j], i < rows,
  * j < cols; batch strides in elements.  Used for NHWC <-> flattened CHW and
  * for FC weight staging.                                                     */

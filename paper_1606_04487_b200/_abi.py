@@ -44,7 +44,7 @@ SIGNATURES: dict[str, tuple] = {
     "omni_device_sm_count": (_I, [_I]),
     "omni_lower_nchw_f32": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P]),
     "omni_lower_nchw_f64": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P]),
-    "omni_lower_nhwc_f32": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P]),
+    "omni_lower_nhwc_f32": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P]),
     "omni_lift_nchw_f32": (_I, [_P, _L, _I, _I, _I, _P, _P]),
     "omni_lift_nchw_f64": (_I, [_P, _L, _I, _I, _I, _P, _P]),
     "omni_col2im_nhwc_f32": (_I, [_P, _L, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P]),
@@ -67,7 +67,7 @@ SIGNATURES: dict[str, tuple] = {
     "omni_sgd_momentum_f32": (_I, [_P, _P, _P, _P, _F, _F, _F, _L, _P]),
     "omni_gather_rows_f32": (_I, [_P, _L, _P, _I, _P, _P]),
     "omni_gather_i32": (_I, [_P, _P, _I, _P, _P]),
-    "omni_conv_weight_to_tap_f32": (_I, [_P, _I, _I, _I, _P, _L, _I, _P]),
+    "omni_conv_weight_to_tap_f32": (_I, [_P, _I, _I, _I, _P, _L, _I, _P, _P]),
     "omni_transpose_f32": (_I, [_P, _L, _L, _I, _I, _P, _L, _L, _I, _P]),
     "omni_fill_f32": (_I, [_P, _F, _L, _P]),
 }

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kThreads) lower_nchw_kernel(
 template <bool VEC4, bool PER_TAP>
 __global__ void __launch_bounds__(kThreads) lower_nhwc_rows_kernel(
     const float* __restrict__ X, int n, int c, int cs, int k, int s, int p, int m,
-    int rows, int K, int ld, float* __restrict__ Dhat) {
+    int rows, int K, int ld, int ones_col, float* __restrict__ Dhat) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int mm = m * m;
@@ -103,7 +103,54 @@ __global__ void __launch_bounds__(kThreads) lower_nhwc_rows_kernel(
         }
       }
     }
-    for (int j = K + lane; j < ld; j += 32) out[j] = 0.f;
+    for (int j = K + lane; j < ld; j += 32) out[j] = (ones_col && j == K) ? 1.f : 0.f;
+  }
+}
+
+// Scalar-channel lowering (c % 4 != 0, e.g. the 3-channel first layer): each
+// block builds a shared table col -> (kx, ky, ch) once, then one warp per row
+// writes float4 runs of the row with no divisions in the inner loop.
+__global__ void __launch_bounds__(kThreads) lower_nhwc_table_kernel(
+    const float* __restrict__ X, int n, int c, int cs, int k, int s, int p, int m, int rows,
+    int K, int ld, int ones_col, float* __restrict__ Dhat) {
+  extern __shared__ int col_tab[];
+  for (int j = threadIdx.x; j < ld; j += blockDim.x) {
+    int e = -1;
+    if (j < K) {
+      const int tap = j / c, ch = j - (j / c) * c;
+      const int kx = tap / k, ky = tap - (tap / k) * k;
+      e = (kx << 24) | (ky << 16) | ch;
+    } else if (ones_col && j == K) {
+      e = -2;
+    }
+    col_tab[j] = e;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int mm = m * m;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += warps) {
+    const int img = row / mm;
+    const int rem = row - img * mm;
+    const int x = rem / m, y = rem - (rem / m) * m;
+    const int ix0 = x * s - p, iy0 = y * s - p;
+    const float* Ximg = X + (long long)img * n * n * cs;
+    float4* out = reinterpret_cast<float4*>(Dhat + (long long)row * ld);
+    for (int q = lane; q < (ld >> 2); q += 32) {
+      float v[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int e = col_tab[4 * q + t];
+        float val = e == -2 ? 1.f : 0.f;
+        if (e >= 0) {
+          const int ix = ix0 + (e >> 24), iy = iy0 + ((e >> 16) & 0xff);
+          if ((unsigned)ix < (unsigned)n && (unsigned)iy < (unsigned)n)
+            val = __ldg(Ximg + ((long long)ix * n + iy) * cs + (e & 0xffff));
+        }
+        v[t] = val;
+      }
+      out[q] = make_float4(v[0], v[1], v[2], v[3]);
+    }
   }
 }
 
@@ -164,9 +211,11 @@ __global__ void __launch_bounds__(kThreads) col2im_nhwc_kernel(
   }
 }
 
-// OIHW (o, c, k, k) <-> tap-major rows Wt[o*ld + (kx*k+ky)*c + ch].
+// OIHW (o, c, k, k) <-> tap-major rows Wt[o*ld + (kx*k+ky)*c + ch]; optional
+// bias in column c*k*k (paired with the lowered matrix's ones column).
 __global__ void __launch_bounds__(kThreads) weight_to_tap_kernel(
-    const float* __restrict__ W, int o, int c, int k, float* __restrict__ Wt, long long ld) {
+    const float* __restrict__ W, int o, int c, int k, float* __restrict__ Wt, long long ld,
+    const float* __restrict__ bias) {
   const long long total = (long long)o * ld;
   const int K = c * k * k;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -178,14 +227,20 @@ __global__ void __launch_bounds__(kThreads) weight_to_tap_kernel(
       const int tap = col / c, ch = col - (col / c) * c;
       const int kx = tap / k, ky = tap - (tap / k) * k;
       v = W[(((long long)oo * c + ch) * k + kx) * k + ky];
+    } else if (bias && col == K) {
+      v = bias[oo];
     }
     Wt[idx] = v;
   }
 }
 
 __global__ void __launch_bounds__(kThreads) weight_from_tap_kernel(
-    const float* __restrict__ Wt, int o, int c, int k, float* __restrict__ W, long long ld) {
+    const float* __restrict__ Wt, int o, int c, int k, float* __restrict__ W, long long ld,
+    float* __restrict__ bias) {
   const long long total = (long long)o * c * k * k;
+  if (bias)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < o; i += gridDim.x * blockDim.x)
+      bias[i] = Wt[(long long)i * ld + c * k * k];
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     long long r = idx;
@@ -284,29 +339,33 @@ int omni_lower_nchw_f64(const double* D, int b, int c, int n, int k, int stride,
 }
 
 int omni_lower_nhwc_f32(const float* X, int b, int n, int c, int cs, int k, int stride, int pad,
-                        float* Dhat, long long ld, void* stream) {
+                        int ones_col, float* Dhat, long long ld, void* stream) {
   int m = 0;
   int rc = check_conv_geom(b, c, n, k, stride, pad, &m);
   if (rc) return rc;
   const int K = c * k * k;
   OMNI_REQUIRE(cs >= c, "pixel stride cs=%d < channels %d", cs, c);
-  OMNI_REQUIRE(ld >= K && ld % 4 == 0 && ld < (1LL << 31), "ld=%lld must be >= %d and a multiple of 4",
-               ld, K);
+  OMNI_REQUIRE(ld >= K + (ones_col ? 1 : 0) && ld % 4 == 0 && ld < (1LL << 31),
+               "ld=%lld must be >= %d and a multiple of 4", ld, K + (ones_col ? 1 : 0));
   OMNI_REQUIRE((uintptr_t)Dhat % 16 == 0, "Dhat must be 16-byte aligned");
   if (b == 0) return OMNI_OK;
   const long long rows = (long long)b * m * m;
   OMNI_REQUIRE(rows < (1LL << 31), "too many lowered rows");
   cudaStream_t st = omni::as_stream(stream);
   const int grid = omni::grid_for(rows * 32, kThreads);
-  if (cs == c && c % 4 == 0 && ((uintptr_t)X % 16 == 0))
-    lower_nhwc_rows_kernel<true, false><<<grid, kThreads, 0, st>>>(X, n, c, cs, k, stride, pad, m,
-                                                                  (int)rows, K, (int)ld, Dhat);
-  else if (cs == c)
-    lower_nhwc_rows_kernel<false, false><<<grid, kThreads, 0, st>>>(X, n, c, cs, k, stride, pad, m,
-                                                                   (int)rows, K, (int)ld, Dhat);
-  else
-    lower_nhwc_rows_kernel<false, true><<<grid, kThreads, 0, st>>>(X, n, c, cs, k, stride, pad, m,
-                                                                  (int)rows, K, (int)ld, Dhat);
+  if (cs == c && c % 4 == 0 && ((uintptr_t)X % 16 == 0)) {
+    lower_nhwc_rows_kernel<true, false><<<grid, kThreads, 0, st>>>(
+        X, n, c, cs, k, stride, pad, m, (int)rows, K, (int)ld, ones_col, Dhat);
+  } else if (ld <= 16384) {
+    lower_nhwc_table_kernel<<<grid, kThreads, ld * sizeof(int), st>>>(
+        X, n, c, cs, k, stride, pad, m, (int)rows, K, (int)ld, ones_col, Dhat);
+  } else if (cs == c) {
+    lower_nhwc_rows_kernel<false, false><<<grid, kThreads, 0, st>>>(
+        X, n, c, cs, k, stride, pad, m, (int)rows, K, (int)ld, ones_col, Dhat);
+  } else {
+    lower_nhwc_rows_kernel<false, true><<<grid, kThreads, 0, st>>>(
+        X, n, c, cs, k, stride, pad, m, (int)rows, K, (int)ld, ones_col, Dhat);
+  }
   return omni::check_launch("lower_nhwc");
 }
 
@@ -349,15 +408,16 @@ int omni_col2im_nhwc_f32(const float* dDhat, long long ld, int b, int n, int c, 
 }
 
 int omni_conv_weight_to_tap_f32(float* W, int o, int c, int k, float* Wt, long long ld,
-                                int inverse, void* stream) {
-  OMNI_REQUIRE(o >= 1 && c >= 1 && k >= 1 && ld >= (long long)c * k * k, "weight staging: bad shape");
+                                int inverse, float* bias, void* stream) {
+  OMNI_REQUIRE(o >= 1 && c >= 1 && k >= 1 && ld >= (long long)c * k * k + (bias ? 1 : 0),
+               "weight staging: bad shape");
   cudaStream_t st = omni::as_stream(stream);
   if (!inverse) {
     weight_to_tap_kernel<<<omni::grid_for((long long)o * ld, kThreads), kThreads, 0, st>>>(
-        W, o, c, k, Wt, ld);
+        W, o, c, k, Wt, ld, bias);
   } else {
     weight_from_tap_kernel<<<omni::grid_for((long long)o * c * k * k, kThreads), kThreads, 0,
-                             st>>>(Wt, o, c, k, W, ld);
+                             st>>>(Wt, o, c, k, W, ld, bias);
   }
   return omni::check_launch("conv_weight_to_tap");
 }

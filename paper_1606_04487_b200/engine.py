@@ -16,10 +16,11 @@ Layout in HBM (all fp32):
   * the flat parameter / gradient vectors use the reference's packing
     (problems.py:201-204 generalised in nets.py).
 
-Fusion: conv/FC + bias + ReLU in the GEMM epilogue; the ReLU mask of the
-backward pass is applied by whichever kernel produces the gradient (pool
-backward, FC dgrad epilogue) and only falls back to a separate pass after
-col2im.  Per-step launches are static, so the whole step can be captured in a
+Fusion: the conv bias rides in the GEMM itself (a ones column in Dhat and
+the bias in the matching column of the staged weights, so the weight-gradient
+GEMM also yields the bias gradient); ReLU in the GEMM epilogue; the ReLU mask
+of the backward pass is applied by whichever kernel produces the gradient
+(pool backward, col2im, FC dgrad epilogue).  Per-step launches are static, so the whole step can be captured in a
 CUDA graph (``capture``).
 """
 
@@ -68,7 +69,9 @@ class Op:
     p: int = 0
     m: int = 0
     Kc: int = 0
+    Kf: int = 0
     ldK: int = 0
+    w_inplace: bool = False
     dhat: torch.Tensor | None = None
     wstage: torch.Tensor | None = None
     dwstage: torch.Tensor | None = None
@@ -115,7 +118,9 @@ class GpuNet:
                         boff=g.param_offsets[1], relu=nxt_relu, first_param_layer=first_param,
                         c_in=c, k=L.k, s=L.stride, p=L.pad, m=m)
                 op.Kc = c * L.k * L.k
-                op.ldK = ru4(op.Kc)
+                # bias folded into the GEMM: ones column Kc in Dhat, bias in column Kc of W
+                op.Kf = op.Kc + (1 if op.boff >= 0 else 0)
+                op.ldK = ru4(op.Kf)
                 op.dhat = z(self.b * m * m, op.ldK)
                 op.wstage = z(d, op.ldK)
                 op.dwstage = z(d, op.ldK)
@@ -131,7 +136,10 @@ class GpuNet:
                     op.flat.value = z(self.b, ru4(f))
                 else:
                     op.flat = cur
-                op.wstage = z(L.d_out, ru4(f))
+                # FC weights (in, out) serve directly as the GEMM's B operand
+                # (MN-major forward, K-major data gradient) when TMA can read them.
+                op.w_inplace = L.d_out % 4 == 0 and g.param_offsets[0] % 4 == 0
+                op.wstage = None if op.w_inplace else z(L.d_out, ru4(f))
                 first_param = False
                 i += 2 if nxt_relu else 1
             elif L.kind == "pool":
@@ -166,9 +174,8 @@ class GpuNet:
         for op in self.ops:
             for M, N, Kd in self._gemm_shapes(op, self.b):
                 ws = max(ws, K.gemm_workspace_bytes(self.prec, M, N, Kd, False, False))
-            if op.kind in ("conv", "fc") and op.boff >= 0:
-                M = self.b * op.m * op.m if op.kind == "conv" else self.b
-                bws = max(bws, K.bias_grad_ws_elems(M, op.layer.d_out))
+            if op.kind == "fc" and op.boff >= 0:
+                bws = max(bws, K.bias_grad_ws_elems(self.b, op.layer.d_out))
             if op.kind == "conv" and not op.first_param_layer:
                 dd = max(dd, self.b * op.m * op.m * op.ldK)
         self.gemm_ws = z(max(ws // 4, 4))
@@ -182,7 +189,7 @@ class GpuNet:
         if op.kind == "conv":
             Mr = b * op.m * op.m
             d = op.layer.d_out
-            out = [(Mr, d, op.Kc), (d, op.Kc, Mr)]
+            out = [(Mr, d, op.Kf), (d, op.Kf, Mr)]
             if not op.first_param_layer:
                 out.append((Mr, op.Kc, d))
             return out
@@ -201,13 +208,18 @@ class GpuNet:
 
     # ----------------------------------------------------------- staging --
     def stage_weights(self, W: torch.Tensor) -> None:
-        """Flat fp32 parameters -> GEMM-ready layouts (tap-major conv rows,
-        transposed FC weights)."""
+        """Flat fp32 parameters -> GEMM-ready layouts (tap-major conv rows with the
+        bias in column Kc; transposed FC weights only when they cannot be used in place)."""
+        if W.data_ptr() % 16:
+            raise ValueError("the flat parameter vector must be 16-byte aligned")
+        self._W = W
         for op in self.ops:
             if op.kind == "conv":
                 d = op.layer.d_out
-                K.conv_weight_to_tap(W[op.woff:op.woff + op.wsz], d, op.c_in, op.k, op.wstage, op.ldK)
-            elif op.kind == "fc":
+                bias = W[op.boff:op.boff + d] if op.boff >= 0 else None
+                K.conv_weight_to_tap(W[op.woff:op.woff + op.wsz], d, op.c_in, op.k, op.wstage,
+                                     op.ldK, bias=bias)
+            elif op.kind == "fc" and not op.w_inplace:
                 d = op.layer.d_out
                 K.transpose(W[op.woff:op.woff + op.wsz], d, 0, op.f_in, d, op.wstage, op.flat.cs, 0, 1)
 
@@ -223,15 +235,11 @@ class GpuNet:
             if op.kind == "conv":
                 d = L.d_out
                 Mr = b * op.m * op.m
-                K.lower_nhwc(op.inp.value[:b], op.c_in, op.k, op.s, op.p, op.ldK, out=op.dhat)
-                if op.boff >= 0:
-                    epi = _abi.EPI_BIAS_RELU if op.relu else _abi.EPI_BIAS
-                    bias = W[op.boff:op.boff + d]
-                else:
-                    epi = _abi.EPI_RELU if op.relu else _abi.EPI_STORE
-                    bias = None
-                self._gemm(Mr, d, op.Kc, op.dhat, op.ldK, False, op.wstage, op.ldK, False,
-                           op.out.value, op.out.cs, epi, bias)
+                K.lower_nhwc(op.inp.value[:b], op.c_in, op.k, op.s, op.p, op.ldK, out=op.dhat,
+                             ones_col=op.boff >= 0)
+                epi = _abi.EPI_RELU if op.relu else _abi.EPI_STORE
+                self._gemm(Mr, d, op.Kf, op.dhat, op.ldK, False, op.wstage, op.ldK, False,
+                           op.out.value, op.out.cs, epi)
             elif op.kind == "pool":
                 mode = 0 if L.mode == "max" else 1
                 K.pool_fwd(mode, op.inp.value[:b], op.inp.c, op.k, op.s, op.p, L.ceil,
@@ -251,8 +259,12 @@ class GpuNet:
                 else:
                     epi = _abi.EPI_RELU if op.relu else _abi.EPI_STORE
                     bias = None
-                self._gemm(b, d, op.f_in, op.flat.value, op.flat.cs, False, op.wstage, op.flat.cs,
-                           False, op.out.value, op.out.cs, epi, bias)
+                if op.w_inplace:
+                    self._gemm(b, d, op.f_in, op.flat.value, op.flat.cs, False,
+                               W[op.woff:op.woff + op.wsz], d, True, op.out.value, op.out.cs, epi, bias)
+                else:
+                    self._gemm(b, d, op.f_in, op.flat.value, op.flat.cs, False, op.wstage,
+                               op.flat.cs, False, op.out.value, op.out.cs, epi, bias)
         C = self.net.classes
         K.softmax_xent(self.logits.value, self.logits.cs, self.labels, b, C, self.loss_buf,
                        self.logits.grad if need_grad else None, self.logits.cs, 1.0 / b)
@@ -275,16 +287,20 @@ class GpuNet:
                     K.bias_grad(dZ, op.out.cs, b, d, G[op.boff:op.boff + d], self.bias_ws)
                 if op.first_param_layer:
                     continue
+                if op.w_inplace:   # B(j=f, r=o) = W[f*d + o]: K-major, ld = d
+                    Bop, ldb, bmn = self._W[op.woff:op.woff + op.wsz], d, False
+                else:              # B(j=f, r=o) = Wt[o*ld_in + f]: MN-major
+                    Bop, ldb, bmn = op.wstage, op.flat.cs, True
                 if op.flat is op.inp:
                     if op.inp.fused_relu:
-                        self._gemm(b, op.f_in, d, dZ, op.out.cs, False, op.wstage, op.flat.cs, True,
+                        self._gemm(b, op.f_in, d, dZ, op.out.cs, False, Bop, ldb, bmn,
                                    op.inp.grad, op.inp.cs, _abi.EPI_MASK_AUX, aux=op.inp.value,
                                    ld_aux=op.inp.cs)
                     else:
-                        self._gemm(b, op.f_in, d, dZ, op.out.cs, False, op.wstage, op.flat.cs, True,
+                        self._gemm(b, op.f_in, d, dZ, op.out.cs, False, Bop, ldb, bmn,
                                    op.inp.grad, op.inp.cs)
                 else:
-                    self._gemm(b, op.f_in, d, dZ, op.out.cs, False, op.wstage, op.flat.cs, True,
+                    self._gemm(b, op.f_in, d, dZ, op.out.cs, False, Bop, ldb, bmn,
                                op.flat.grad, op.flat.cs)
                     hw = op.inp.n * op.inp.n
                     K.transpose(op.flat.grad, hw, op.flat.cs, op.inp.c, hw, op.inp.grad,
@@ -297,12 +313,12 @@ class GpuNet:
                 d = L.d_out
                 Mr = b * op.m * op.m
                 dZ = op.out.grad
-                self._gemm(d, op.Kc, Mr, dZ, op.out.cs, True, op.dhat, op.ldK, True, op.dwstage,
+                # weight (and, via the ones column, bias) gradient in one GEMM
+                self._gemm(d, op.Kf, Mr, dZ, op.out.cs, True, op.dhat, op.ldK, True, op.dwstage,
                            op.ldK)
                 K.conv_weight_to_tap(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k, op.dwstage,
-                                     op.ldK, inverse=True)
-                if op.boff >= 0:
-                    K.bias_grad(dZ, op.out.cs, Mr, d, G[op.boff:op.boff + d], self.bias_ws)
+                                     op.ldK, inverse=True,
+                                     bias=G[op.boff:op.boff + d] if op.boff >= 0 else None)
                 if op.first_param_layer:
                     continue
                 self._gemm(Mr, op.Kc, d, dZ, op.out.cs, False, op.wstage, op.ldK, True, self.ddhat,
@@ -347,12 +363,11 @@ class GpuNet:
         for op in self.ops:
             if op.kind == "conv":
                 n += 1 + 1 + 1   # stage, lower, gemm
-                n += 1 + 1       # wgrad gemm, inverse stage
-                n += 2 if op.boff >= 0 else 0
+                n += 1 + 1       # wgrad gemm (+ bias column), inverse stage
                 if not op.first_param_layer:
-                    n += 2
+                    n += 2       # dgrad gemm, col2im (+ fused ReLU mask)
             elif op.kind == "fc":
-                n += 1 + 1 + (1 if op.flat is not op.inp else 0)
+                n += (0 if op.w_inplace else 1) + 1 + (1 if op.flat is not op.inp else 0)
                 n += 1 + (2 if op.boff >= 0 else 0)
                 if not op.first_param_layer:
                     n += 1 + (1 if op.flat is not op.inp else 0)

@@ -51,14 +51,16 @@ def lower_nchw(D: torch.Tensor, k: int, stride: int, pad: int, start: int, b_p: 
 
 
 def lower_nhwc(X: torch.Tensor, c: int, k: int, stride: int, pad: int, ld: int,
-               out: torch.Tensor | None = None) -> torch.Tensor:
-    """Tap-major lowering of NHWC activations (pixel stride X.shape[3])."""
+               out: torch.Tensor | None = None, ones_col: bool = False) -> torch.Tensor:
+    """Tap-major lowering of NHWC activations (pixel stride X.shape[3]); ones_col
+    writes 1.0 into column c*k*k (bias folded into the GEMM)."""
     _require_cuda(X)
     b, n, _, cs = X.shape
     m = (n + 2 * pad - k) // stride + 1
     if out is None:
         out = torch.empty((b * m * m, ld), dtype=torch.float32, device=X.device)
-    call("omni_lower_nhwc_f32", _ptr(X), b, n, c, cs, k, stride, pad, _ptr(out), ld, _stream())
+    call("omni_lower_nhwc_f32", _ptr(X), b, n, c, cs, k, stride, pad, int(ones_col), _ptr(out), ld,
+         _stream())
     return out
 
 
@@ -210,8 +212,9 @@ def gather_i32(src: torch.Tensor, idx: torch.Tensor, dst: torch.Tensor) -> None:
 
 
 def conv_weight_to_tap(W: torch.Tensor, o: int, c: int, k: int, Wt: torch.Tensor, ld: int,
-                       inverse: bool = False) -> None:
-    call("omni_conv_weight_to_tap_f32", _ptr(W), o, c, k, _ptr(Wt), ld, int(inverse), _stream())
+                       inverse: bool = False, bias: torch.Tensor | None = None) -> None:
+    call("omni_conv_weight_to_tap_f32", _ptr(W), o, c, k, _ptr(Wt), ld, int(inverse), _ptr(bias),
+         _stream())
 
 
 def transpose(src: torch.Tensor, lds: int, src_bstride: int, rows: int, cols: int,

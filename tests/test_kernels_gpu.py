@@ -267,3 +267,27 @@ def test_conv_weight_tap_roundtrip():
     back = torch.empty(o, c, k, k, device=DEV)
     K.conv_weight_to_tap(back, o, c, k, Wt, ld, inverse=True)
     assert torch.equal(back.cpu(), W)
+
+
+@pytest.mark.parametrize("geom", [(2, 3, 27, 11, 4, 0), (2, 8, 10, 3, 1, 1), (1, 5, 9, 3, 1, 1)])
+def test_bias_ones_column(geom):
+    """The bias rides in the GEMM: Dhat column c*k*k is 1.0 and the staged weights
+    carry the bias there; the inverse staging returns the bias (gradient)."""
+    b, c, n, k, s, p = geom
+    Kc = c * k * k
+    ld = K.round_up(Kc + 1, 4)
+    X = torch.randn(b, n, n, c, device=DEV)
+    D = K.lower_nhwc(X, c, k, s, p, ld, ones_col=True)
+    assert torch.all(D[:, Kc] == 1.0) and not D[:, Kc + 1:].any()
+    ref = K.lower_nhwc(X, c, k, s, p, K.round_up(Kc, 4))
+    assert torch.equal(D[:, :Kc], ref[:, :Kc])
+    o = 6
+    W = torch.randn(o, c, k, k, device=DEV)
+    bias = torch.randn(o, device=DEV)
+    Wt = torch.empty(o, ld, device=DEV)
+    K.conv_weight_to_tap(W, o, c, k, Wt, ld, bias=bias)
+    assert torch.equal(Wt[:, Kc], bias)
+    W2 = torch.empty_like(W)
+    b2 = torch.empty_like(bias)
+    K.conv_weight_to_tap(W2, o, c, k, Wt, ld, inverse=True, bias=b2)
+    assert torch.equal(W2, W) and torch.equal(b2, bias)

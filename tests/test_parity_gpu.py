@@ -138,6 +138,23 @@ def scaled_weights(net, seed):
     return W
 
 
+def argmax_flips(engine, net, W, X, b):
+    """Per max-pool layer index: how many windows picked a different argmax on the
+    GPU than in the float64 oracle, for the same inputs."""
+    _, cache = R.forward(net.to_dicts(), net.in_channels, net.in_size, W, X)
+    ref_args = [data[1] for kind, data in cache if kind == "pool"]
+    geo_pools = [g.index for g in net.geometry() if g.layer.kind == "pool"]
+    out = {}
+    gpu_pools = [op for op in engine.ops if op.kind == "pool"]
+    for li, op, ra in zip(geo_pools, gpu_pools, ref_args):
+        if ra is None:
+            continue
+        o, c = op.m, op.inp.c
+        ga = op.argmax[: b * o * o * c].view(b, o, o, c).permute(0, 3, 1, 2).cpu().numpy()
+        out[li] = int((ga != ra).sum())
+    return out
+
+
 def per_param_errors(net, g, ref):
     errs = []
     for geo in net.geometry():
@@ -162,11 +179,17 @@ def test_network_grad_vs_oracle(name, b, gtol, ltol):
     ref = R.grad(net.to_dicts(), net.in_channels, net.in_size, W, X, y, workers=os.cpu_count() or 1)
     ref_loss = R.loss(net.to_dicts(), net.in_channels, net.in_size, W, X, y)
     g = prob.grad(W, batch)
+    flips = argmax_flips(prob.engine(b), net, W, X, b)
     loss = prob.loss(W, batch)
     assert abs(loss - ref_loss) <= ltol * max(1.0, abs(ref_loss)), (loss, ref_loss)
     errs = per_param_errors(net, g, ref)
-    worst = max(e for _, _, e in errs)
-    assert worst < gtol, errs
+    # A max-pool near-tie that fp32 and fp64 resolve differently re-routes the
+    # gradient of one window to another pixel (problems.py:215-216); only the
+    # conv layers below that pool see it, as a local O(1/sqrt(n)) perturbation.
+    first_flip = min((li for li, nf in flips.items() if nf), default=None)
+    for kind, li, e in errs:
+        bound = 5e-3 if first_flip is not None and li < first_flip else gtol
+        assert e < bound, (kind, li, e, flips, errs)
     # tf32 (throughput) mode, reported with a loose bound
     p32 = CNNProblem(net, n_examples=max(16, b), seed=1, precision="tf32")
     g32 = p32.grad(W, batch)
