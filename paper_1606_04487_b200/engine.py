@@ -8,8 +8,9 @@ sgd.py:92-101 update, for any NetSpec.
 Layout in HBM (all fp32):
   * activations NHWC, pixel stride cs = round_up(c, 4) (16-byte rows for TMA
     and float4 kernels); FC activations (b, round_up(f, 4));
-  * lowered matrices Dhat (b*m^2, round_up(c*k*k, 4)) in tap-major column
-    order (kx*k + ky)*c + ch, kept from forward for the weight gradient;
+  * lowered matrices Dhat (b*m^2, round_up(c*k*k + bias, 32)) in tap-major
+    column order (kx*k + ky)*c + ch (128-byte row pitch), kept from forward for
+    the weight gradient;
   * conv weights staged each step from the flat OIHW vector into tap-major
     rows (the GEMM's K-major B operand); FC weights staged transposed
     (out, in) so the forward product is K-major x K-major;
@@ -120,7 +121,8 @@ class GpuNet:
                 op.Kc = c * L.k * L.k
                 # bias folded into the GEMM: ones column Kc in Dhat, bias in column Kc of W
                 op.Kf = op.Kc + (1 if op.boff >= 0 else 0)
-                op.ldK = ru4(op.Kf)
+                # 128-byte row pitch: TMA boxes and TMA-stored rows stay line-aligned
+                op.ldK = K.round_up(op.Kf, 32)
                 op.dhat = z(self.b * m * m, op.ldK)
                 op.wstage = z(d, op.ldK)
                 op.dwstage = z(d, op.ldK)
