@@ -1,0 +1,138 @@
+"""Compute groups across GPUs: g groups of k = N/g ranks (one process per GPU).
+
+Semantics are the reference's deterministic schedule (simulator.py:123-213
+with service_mode="deterministic", cluster.py:54-73), which is strict round
+robin: write step t >= 1 is made by group (t-1) mod g with the gradient of
+draw floor((t-1)/g) of that group's batch stream, evaluated at the model
+W(max(0, t-g)) -- the state right after the group's own previous write
+(SURVEY.md section 3(C)).  That makes g updates per round independent, so
+they run concurrently:
+
+  round r, on every rank of group i:
+    1. gradient at the group's snapshot on this rank's slice of the group batch
+       (data parallel inside the group: k ranks x b/k images);
+    2. allreduce (sum) inside the group -> the group gradient (mean over b);
+    3. all-gather across groups (one rank per group per member index) ->
+       G_0 .. G_{g-1} on every rank;
+    4. replay the g momentum updates in group order (sgd.py:104-112: the
+       regulariser also uses the writer's snapshot), keeping W after update i
+       as group i's next snapshot.
+
+Every rank therefore holds the master model and all g snapshots; no rank
+waits on another except in the two collectives.  g = 1 degenerates to
+synchronous data-parallel SGD with one allreduce per step.
+
+The gradient/update provider is pluggable: ``CudaBackend`` (the B200 engine,
+NCCL) is the product path; tests plug a CPU backend into the same runtime to
+check the collective logic with gloo.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Protocol
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .cluster import ExecutionPlan
+from .sgd import Hyperparams, batch_stream
+
+
+class Backend(Protocol):
+    device: torch.device
+
+    def grad(self, W: torch.Tensor, idx: np.ndarray) -> torch.Tensor:
+        """Mean-over-batch gradient at W of the examples ``idx`` (a fresh tensor)."""
+
+    def sgd(self, W: torch.Tensor, V: torch.Tensor, G: torch.Tensor, w_read: torch.Tensor,
+            hp: Hyperparams) -> None:
+        """In place: V = mu V - eta (G + lam w_read); W += V."""
+
+
+class CudaBackend:
+    """B200 engine: device gather + fused forward/backward + K8 update."""
+
+    def __init__(self, problem, batch: int):
+        self.problem = problem
+        self.device = problem.device
+        self.engine = problem.engine(batch)
+
+    def grad(self, W, idx):
+        from .problems import Batch
+
+        b = self.problem.load_batch(self.engine, Batch(self.problem, idx))
+        _, G = self.engine.loss_and_grad(W, b)
+        return G.clone()
+
+    def sgd(self, W, V, G, w_read, hp):
+        from . import kernels as K
+
+        K.sgd_momentum(W, V, G, w_read, hp.eta, hp.mu, hp.lam)
+
+
+@dataclass(frozen=True)
+class GroupEvent:
+    group_id: int
+    read_step: int
+    write_step: int
+    staleness: int
+
+
+class GroupRuntime:
+    def __init__(self, plan: ExecutionPlan, backend: Backend, hp: Hyperparams, W0: torch.Tensor,
+                 n_examples: int, seed: int):
+        if not dist.is_initialized():
+            raise RuntimeError("GroupRuntime needs torch.distributed initialised (one rank per GPU)")
+        world, rank = dist.get_world_size(), dist.get_rank()
+        if plan.N != world:
+            raise ValueError(f"plan.N={plan.N} != world size {world}")
+        if hp.b % plan.k:
+            raise ValueError(f"group batch b={hp.b} is not divisible by k={plan.k}")
+        self.plan, self.backend, self.hp = plan, backend, hp
+        self.rank = rank
+        self.group = plan.group_of(rank)
+        self.member = plan.member_of(rank)
+        self.n_examples = n_examples
+        # every rank creates every subgroup, in the same order (torch.distributed rule)
+        self.group_pgs = [dist.new_group(plan.group_ranks(i)) for i in range(plan.g)]
+        self.cross_pgs = [dist.new_group([i * plan.k + j for i in range(plan.g)]) for j in range(plan.k)]
+        self.W = W0.clone()
+        self.V = torch.zeros_like(self.W)
+        self.snaps = [self.W.clone() for _ in range(plan.g)]
+        self.snap_step = [0] * plan.g
+        self.t = 0
+        self.rng = batch_stream(seed, self.group)
+        self.events: list[GroupEvent] = []
+        self._gather = [torch.empty_like(self.W) for _ in range(plan.g)]
+        # gradients arrive as the SUM of k slice means; fold the 1/k into the fused
+        # update: eta (G/k + lam w) = (eta/k) (G + k lam w)
+        self._hp_sum = hp.replace(eta=hp.eta / plan.k, lam=hp.lam * plan.k)
+
+    def _my_slice(self, idx: np.ndarray) -> np.ndarray:
+        per = self.hp.b // self.plan.k
+        return idx[self.member * per:(self.member + 1) * per]
+
+    def run(self, rounds: int) -> None:
+        for _ in range(rounds):
+            self.round()
+
+    def round(self) -> None:
+        """One round = g master updates, one per group, in group order."""
+        plan = self.plan
+        idx = self.rng.integers(0, self.n_examples, size=self.hp.b)
+        G = self.backend.grad(self.snaps[self.group], self._my_slice(idx))
+        if plan.k > 1:
+            dist.all_reduce(G, group=self.group_pgs[self.group])   # sum of k slice means
+        if plan.g > 1:
+            dist.all_gather(self._gather, G, group=self.cross_pgs[self.member])
+            grads = self._gather
+        else:
+            grads = [G]
+        for i in range(plan.g):
+            self.backend.sgd(self.W, self.V, grads[i], self.snaps[i], self._hp_sum)
+            self.t += 1
+            self.events.append(GroupEvent(i, self.snap_step[i], self.t, self.t - 1 - self.snap_step[i]))
+            self.snaps[i].copy_(self.W)       # group i reads W(t) next round
+            self.snap_step[i] = self.t
