@@ -25,6 +25,9 @@ import time
 
 import numpy as np
 
+# keep stdout to the one JSON line: NCCL's version banner goes to stdout otherwise
+os.environ["NCCL_DEBUG"] = os.environ.get("BENCH_NCCL_DEBUG", "WARN")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -180,9 +183,8 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1606_04487_b200 import _abi, kernels as K, nets
-    from paper_1606_04487_b200.engine import GpuNet
-    from paper_1606_04487_b200.problems import CNNProblem, HostBatch
+    from paper_1606_04487_b200 import _abi, nets
+    from paper_1606_04487_b200.problems import CNNProblem, DeviceBatch, HostBatch
     from paper_1606_04487_b200.sgd import Hyperparams, SGDState
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -196,36 +198,28 @@ def run_ours(args):
     b = args.batch
     _abi.load()
 
-    # Synthetic dataset resident in HBM (NHWC), distinct per rank; shared init W.
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(args.seed * 1000 + rank)
-    s, c = net.in_size, net.in_channels
-    data = torch.randn((args.n_examples, s, s, c), generator=gen, device=dev)
-    labels = torch.randint(0, net.classes, (args.n_examples,), generator=gen, device=dev,
-                           dtype=torch.int32)
-    gw = torch.Generator(device=dev)
-    gw.manual_seed(args.seed)
-    W = 0.01 * torch.randn(net.dim, generator=gw, device=dev)
-    V = torch.zeros_like(W)
-    eng = GpuNet(net, b, dev, args.precision)
-    total = args.warmup + args.steps
-    rng = np.random.default_rng(np.random.SeedSequence(args.seed, spawn_key=(1, rank)))
-    idx_all = torch.from_numpy(rng.integers(0, args.n_examples, size=(total, b))).to(dev)
-    eta, mu, lam = args.eta, args.mu, args.lam
-
     if args.groups > 1:
         return run_groups(args, net, dev, world, rank, local)
 
+    # Public API: CNNProblem (synthetic dataset resident in HBM, distinct per
+    # rank) + DeviceSession (W, V in HBM; data parallel over NCCL when N > 1).
+    s, c = net.in_size, net.in_channels
+    prob = CNNProblem(net, n_examples=args.n_examples, seed=args.seed * 1000 + rank,
+                      labels="uniform", precision=args.precision, device=dev)
+    hp = Hyperparams(eta=args.eta, mu=args.mu, lam=args.lam, b=b)
+    sess = prob.device_session(SGDState.fresh(np.zeros(1)), hp,
+                               process_group=dist.group.WORLD if world > 1 else None)
+    gw = torch.Generator(device=dev)
+    gw.manual_seed(args.seed)                     # identical initial model on every rank
+    sess.W = 0.01 * torch.randn(net.dim, generator=gw, device=dev)
+    sess.V = torch.zeros_like(sess.W)
+    eng = sess.engine
+    total = args.warmup + args.steps
+    rng = np.random.default_rng(np.random.SeedSequence(args.seed, spawn_key=(1, rank)))
+    idx_all = torch.from_numpy(rng.integers(0, args.n_examples, size=(total, b))).to(dev)
+
     def step(i):
-        eng.gather_batch(data, labels, idx_all[i])
-        eng.forward(W)
-        eng.backward()
-        if world > 1:
-            dist.all_reduce(eng.grad)
-            # mean over ranks folded into the update: V = mu V - (eta/N)(g_sum + N lam W)
-            K.sgd_momentum(W, V, eng.grad, W, eta / world, mu, lam * world)
-        else:
-            K.sgd_momentum(W, V, eng.grad, W, eta, mu, lam)
+        sess.step(DeviceBatch(idx_all[i]))
 
     for i in range(args.warmup):
         step(i)
@@ -250,7 +244,7 @@ def run_ours(args):
         ms = float(t.item())
         dist.barrier()
     value = args.steps * b * world / (ms / 1000.0)
-    loss_now = float(eng.loss_buf.item())
+    loss_now = sess.last_loss()
 
     # ---- per-GEMM breakdown (one instrumented step, after the timed region)
     records = []
@@ -271,25 +265,21 @@ def run_ours(args):
     torch.cuda.synchronize()
     eng._gemm = orig
     per_step = len(records) // reps
-    # classify: GEMMs of conv layers vs FC layers (engine issues them in a fixed order)
     conv_shapes = set()
     for op in eng.ops:
         if op.kind == "conv":
             for shp in eng._gemm_shapes(op, b):
                 conv_shapes.add(shp)
     conv_ms = fc_ms = 0.0
-    conv_flop = fc_flop = 0.0
     rows = []
     for M, N, Kd, a0, a1 in records:
         t = a0.elapsed_time(a1) / reps
-        fl = 2.0 * M * N * Kd / reps
         if (M, N, Kd) in conv_shapes:
             conv_ms += t
-            conv_flop += fl
         else:
             fc_ms += t
-            fc_flop += fl
-        rows.append({"M": M, "N": N, "K": Kd, "ms": a0.elapsed_time(a1), "tflops": 2.0 * M * N * Kd / (a0.elapsed_time(a1) * 1e9)})
+        rows.append({"M": M, "N": N, "K": Kd, "ms": a0.elapsed_time(a1),
+                     "tflops": 2.0 * M * N * Kd / (a0.elapsed_time(a1) * 1e9)})
     conv_flops_step = net.conv_flops_per_image() * b
     achieved = conv_flops_step / (conv_ms * 1e-3) / 1e12 if conv_ms > 0 else 0.0
     peaks = measured_peaks()
@@ -299,13 +289,9 @@ def run_ours(args):
             json.dump({"gemms_one_step": rows[:per_step], "conv_gemm_ms": conv_ms,
                        "fc_gemm_ms": fc_ms, "step_ms": ms / args.steps}, f, indent=1)
 
-    # ---- e2e: through the public API with host buffers (pinned H2D in the timed region)
+    # ---- e2e: the same public call with HOST buffers (pinned H2D in the timed region)
     e2e = None
     if not args.no_e2e:
-        prob = CNNProblem(net, n_examples=b, seed=args.seed + rank, precision=args.precision, device=dev)
-        hp = Hyperparams(eta=eta, mu=mu, lam=lam, b=b)
-        sess = prob.device_session(SGDState.fresh(np.zeros(net.dim, dtype=np.float32)), hp)
-        sess.W.copy_(W)
         Xh = torch.randn((b, s, s, c), generator=torch.Generator().manual_seed(rank)).pin_memory()
         yh = torch.randint(0, net.classes, (b,), dtype=torch.int32).pin_memory()
         host_batch = HostBatch(Xh, yh)
@@ -329,7 +315,6 @@ def run_ours(args):
         e2e = {"value": n_e2e * b * world / dt, "unit": "images/s",
                "h2d_bytes_per_step": Xh.numel() * 4 + yh.numel() * 4, "d2h_bytes_per_step": 4,
                "path": "CNNProblem.device_session().step(HostBatch(pinned X, y)) + last_loss()"}
-        del sess, prob
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -273,10 +273,20 @@ class GpuNet:
         return self.loss_buf
 
     # ---------------------------------------------------------- backward --
-    def backward(self, b: int | None = None) -> torch.Tensor:
-        """Gradient of the mean loss w.r.t. the flat parameters -> self.grad."""
+    def backward(self, b: int | None = None, on_grad=None) -> torch.Tensor:
+        """Gradient of the mean loss w.r.t. the flat parameters -> self.grad.
+
+        ``on_grad(lo, hi)`` (optional) is called as soon as the launches that
+        write G[lo:hi] (one layer's weight + bias gradient) are enqueued, in
+        backward order -- the hook a data-parallel caller uses to overlap the
+        gradient allreduce of finished layers with the rest of the backward."""
         b = self.b if b is None else int(b)
         G = self.grad
+
+        def done(op):
+            if on_grad is not None:
+                hi = op.boff + op.layer.d_out if op.boff >= 0 else op.woff + op.wsz
+                on_grad(op.woff, hi)
         for op in reversed(self.ops):
             L = op.layer
             if op.kind == "fc":
@@ -287,6 +297,7 @@ class GpuNet:
                            G[op.woff:op.woff + op.wsz], d)
                 if op.boff >= 0:
                     K.bias_grad(dZ, op.out.cs, b, d, G[op.boff:op.boff + d], self.bias_ws)
+                done(op)
                 if op.first_param_layer:
                     continue
                 if op.w_inplace:   # B(j=f, r=o) = W[f*d + o]: K-major, ld = d
@@ -321,6 +332,7 @@ class GpuNet:
                 K.conv_weight_to_tap(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k, op.dwstage,
                                      op.ldK, inverse=True,
                                      bias=G[op.boff:op.boff + d] if op.boff >= 0 else None)
+                done(op)
                 if op.first_param_layer:
                     continue
                 self._gemm(Mr, op.Kc, d, dZ, op.out.cs, False, op.wstage, op.ldK, True, self.ddhat,

@@ -75,10 +75,30 @@ class HostBatch:
         return int(self.X.shape[0])
 
 
-class DeviceSession:
-    """W, V resident in HBM; one step = gather + forward + backward + K8."""
+class DeviceBatch:
+    """Indices (int64, already on the device) into the problem's dataset."""
 
-    def __init__(self, problem: "CNNProblem", state: SGDState, hp: Hyperparams):
+    __slots__ = ("idx",)
+
+    def __init__(self, idx: torch.Tensor):
+        self.idx = idx
+
+    @property
+    def size(self) -> int:
+        return int(self.idx.numel())
+
+
+class DeviceSession:
+    """W, V resident in HBM; one step = batch load + forward + backward + K8.
+
+    With ``process_group`` (a torch.distributed NCCL group; one process per
+    GPU) the session is synchronous data parallel over that group: each rank
+    steps on its own batch, every layer's gradient is allreduced as soon as
+    the backward has produced it (async, overlapping the remaining backward),
+    and the mean over ranks is folded into the fused update."""
+
+    def __init__(self, problem: "CNNProblem", state: SGDState, hp: Hyperparams,
+                 process_group=None):
         self.problem = problem
         self.hp = hp
         dev = problem.device
@@ -86,15 +106,40 @@ class DeviceSession:
         self.V = torch.from_numpy(np.ascontiguousarray(state.V, dtype=np.float32)).to(dev)
         self.t = state.t
         self.engine = problem.engine(hp.b)
+        self.pg = process_group
+        self.world = 1
+        if process_group is not None:
+            import torch.distributed as dist
+
+            self.world = dist.get_world_size(process_group)
+
+    def _allreduce_hook(self, works):
+        import torch.distributed as dist
+
+        G = self.engine.grad
+
+        def hook(lo, hi):
+            works.append(dist.all_reduce(G[lo:hi], group=self.pg, async_op=True))
+
+        return hook
 
     def step(self, batch: Any, w_read: torch.Tensor | None = None) -> None:
         """V = mu V - eta (grad(w_read) + lam w_read); W += V, with w_read = W when
         synchronous (sgd.py:104-112)."""
         wr = self.W if w_read is None else w_read
         b = self.problem.load_batch(self.engine, batch)
-        self.engine.loss_and_grad(wr, b)
         hp = self.hp
-        K.sgd_momentum(self.W, self.V, self.engine.grad, wr, hp.eta, hp.mu, hp.lam)
+        if self.world > 1:
+            works = []
+            self.engine.forward(wr, b)
+            self.engine.backward(b, on_grad=self._allreduce_hook(works))
+            for w in works:
+                w.wait()   # the compute stream waits for the NCCL stream
+            n = self.world   # eta (G_sum/n + lam w) = (eta/n) (G_sum + n lam w)
+            K.sgd_momentum(self.W, self.V, self.engine.grad, wr, hp.eta / n, hp.mu, hp.lam * n)
+        else:
+            self.engine.loss_and_grad(wr, b)
+            K.sgd_momentum(self.W, self.V, self.engine.grad, wr, hp.eta, hp.mu, hp.lam)
         self.t += 1
 
     def full_loss(self) -> float:
@@ -176,6 +221,9 @@ class CNNProblem(TrainingProblem):
             idx = torch.from_numpy(batch.idx).to(self.device, non_blocking=True)
             engine.gather_batch(self.data, self.data_labels, idx)
             return batch.size
+        if isinstance(batch, DeviceBatch):
+            engine.gather_batch(self.data, self.data_labels, batch.idx)
+            return batch.size
         if isinstance(batch, HostBatch):
             b = batch.size
             engine.input.value[:b].copy_(batch.X, non_blocking=True)
@@ -196,7 +244,7 @@ class CNNProblem(TrainingProblem):
         return torch.from_numpy(W.astype(np.float32)).to(self.device)
 
     def _batch_size(self, batch) -> int:
-        return batch.size if isinstance(batch, (Batch, HostBatch)) else len(batch[1])
+        return batch.size if isinstance(batch, (Batch, HostBatch, DeviceBatch)) else len(batch[1])
 
     def loss(self, W, batch) -> float:
         e = self.engine(self._batch_size(batch))
@@ -236,8 +284,8 @@ class CNNProblem(TrainingProblem):
             acc += G.double() * (b / n)
         return acc.cpu().numpy()
 
-    def device_session(self, state: SGDState, hp: Hyperparams) -> DeviceSession:
-        return DeviceSession(self, state, hp)
+    def device_session(self, state: SGDState, hp: Hyperparams, process_group=None) -> DeviceSession:
+        return DeviceSession(self, state, hp, process_group)
 
 
 def make_cnn(net: str, n_examples: int = 128, seed: int = 0, **kw) -> CNNProblem:
