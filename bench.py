@@ -25,8 +25,15 @@ import time
 
 import numpy as np
 
-# keep stdout to the one JSON line: NCCL's version banner goes to stdout otherwise
+# stdout carries exactly one JSON line: keep the real stdout for it and send
+# everything else that writes to fd 1 (NCCL's version banner, library chatter) to stderr.
 os.environ["NCCL_DEBUG"] = os.environ.get("BENCH_NCCL_DEBUG", "WARN")
+_JSON_FD = os.dup(1)
+os.dup2(2, 1)
+
+
+def emit(obj) -> None:
+    os.write(_JSON_FD, (json.dumps(obj) + "\n").encode())
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -175,7 +182,7 @@ def run_reference(args):
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "images/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------ ours --
@@ -341,7 +348,7 @@ def run_ours(args):
             "clocks": clk,
             "loss_after": loss_now,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 
@@ -387,7 +394,7 @@ def run_groups(args, net, dev, world, rank, local):
     value = args.steps * args.batch * world / (ms / 1000.0)
     if rank == 0:
         st_ = [e.staleness for e in rt.events[plan.g:]]
-        print(json.dumps({
+        emit({
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -400,7 +407,7 @@ def run_groups(args, net, dev, world, rank, local):
                        "step": "one round = g master updates"},
             "staleness_mean": float(np.mean(st_)) if st_ else 0.0,
             "gpu_launches": None, "clocks": clk, "e2e": None, "cpu_baseline": None,
-            "roofline": None}), flush=True)
+            "roofline": None})
     dist.destroy_process_group()
 
 

@@ -98,6 +98,26 @@ int omni_gemm_f32(int precision, int M, int N, int K, const float* A, long long 
                   long long ldc, int epilogue, const float* bias, const float* aux,
                   long long ld_aux, float* workspace, long long ws_bytes, void* stream);
 
+/* Implicit-GEMM convolution on tcgen05, operands gathered by TMA im2col from
+ * the NHWC activation X (b, n, n, cs) -- no lowered matrix in HBM.  The GEMM
+ * K index is (tap, channel) tap-major, i.e. the column order of
+ * omni_lower_nhwc_f32.  Requires d_in = c multiple of 32.
+ *   OMNI_CONV_FPROP: Y[pix, o] (op)= sum_{tap,ch} X(pix, tap, ch) G[o*ldg + tap*c + ch]
+ *                    (G = tap-major weights d_out x ldg; Y = b*m*m rows, ld ldy)
+ *   OMNI_CONV_WGRAD: Y[o*ldy + tap*c + ch] = sum_pix G[pix*ldg + o] X(pix, tap, ch)
+ *                    (G = output gradient dY, b*m*m rows, ld ldg)
+ * The data gradient of a stride-1 conv is OMNI_CONV_FPROP on dY with pad
+ * k-1-pad and the spatially flipped, transposed weights.                     */
+#define OMNI_CONV_FPROP 0
+#define OMNI_CONV_WGRAD 1
+long long omni_conv_implicit_plan(int precision, int op, int b, int n, int c, int k, int stride,
+                                  int pad, int d_out);
+int omni_conv_implicit_f32(int precision, int op, const float* X, int b, int n, int c, int cs,
+                           int k, int stride, int pad, int d_out, const float* G, long long ldg,
+                           float* Y, long long ldy, int epilogue, const float* bias,
+                           const float* aux, long long ld_aux, float* workspace,
+                           long long ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- K3 --
  * Pooling over NHWC (pixel strides cs_in / cs_out).  mode 0 = max (first max in
  * (dy,dx) window order, argmax = input pixel index iy*w + ix, as
@@ -147,6 +167,10 @@ int omni_gather_i32(const int32_t* src, const int64_t* idx, int nidx, int32_t* d
  * c*k*k of Wt in the same direction.                                       */
 int omni_conv_weight_to_tap_f32(float* W, int o, int c, int k, float* Wt, long long ld,
                                 int inverse, float* bias, void* stream);
+/* Data-gradient weights of a stride-1 conv: Wf (c rows, ld >= o*k*k) with
+ * Wf[ch*ld + (kx*k + ky)*o + oo] = W[oo, ch, k-1-kx, k-1-ky] (W is OIHW).     */
+int omni_conv_weight_flip_f32(const float* W, int o, int c, int k, float* Wf, long long ld,
+                              void* stream);
 /* Batched 2-D transpose: dst[bi][j*ldd + i] = src[bi][i*lds + j], i < rows,
  * j < cols; batch strides in elements.  Used for NHWC <-> flattened CHW and
  * for FC weight staging.                                                     */

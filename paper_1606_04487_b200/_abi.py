@@ -32,6 +32,9 @@ EPI_ACCUM = 3
 EPI_MASK_AUX = 4
 EPI_RELU = 5
 
+CONV_FPROP = 0
+CONV_WGRAD = 1
+
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 _L = ctypes.c_longlong
@@ -53,6 +56,12 @@ SIGNATURES: dict[str, tuple] = {
         _I,
         [_I, _I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _P, _P, _L, _P, _L, _P],
     ),
+    "omni_conv_implicit_plan": (_L, [_I, _I, _I, _I, _I, _I, _I, _I, _I]),
+    "omni_conv_implicit_f32": (
+        _I,
+        [_I, _I, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P, _L, _I, _P, _P, _L, _P, _L, _P],
+    ),
+    "omni_conv_weight_flip_f32": (_I, [_P, _I, _I, _I, _P, _L, _P]),
     "omni_pool_out_size": (_I, [_I, _I, _I, _I, _I]),
     "omni_pool_fwd_nhwc_f32": (_I, [_I, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "omni_pool_bwd_nhwc_f32": (

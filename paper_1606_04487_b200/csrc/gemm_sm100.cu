@@ -49,6 +49,9 @@ struct Params {
   const float* bias;
   const float* aux;
   long long ld_aux;
+  // implicit-GEMM convolution (IM2COL != 0): output size m, m*m, stride, pad,
+  // kernel size, 32-channel blocks per filter tap
+  int conv_m, conv_mm, conv_s, conv_pad, conv_k, conv_cblocks;
 };
 
 template <int BN, bool SPLIT3>
@@ -105,6 +108,18 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint32_t dst
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+// TMA im2col load (4-D NHWC tensor map): `pixels` consecutive output pixels
+// starting at the window corner (w, h) of image n, 32 channels from c, filter
+// tap offsets (ow, oh); out-of-image taps read as zero (the conv padding).
+__device__ __forceinline__ void tma_load_im2col(const CUtensorMap* map, uint32_t dst, uint32_t bar,
+                                                int c, int w, int h, int n, uint16_t ow, uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow),
+      "h"(oh)
       : "memory");
 }
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1,
@@ -248,7 +263,7 @@ __device__ __forceinline__ void epi_chunk(int mode, float (&v)[N], const uint32_
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, bool SPLIT3>
+template <int BN, bool A_MN, bool B_MN, bool SPLIT3, int IM2COL>
 __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB,
@@ -307,20 +322,52 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
         decode_work(p, w, mt, nt, sp);
         const int kt0 = sp * p.kt_per_split;
         const int kt1 = min(p.k_tiles, kt0 + p.kt_per_split);
+        // im2col A: window corner of this tile's first output pixel
+        int a_img = 0, a_h0 = 0, a_w0 = 0;
+        if (IM2COL == 1) {
+          const int m0 = mt * BM;
+          a_img = m0 / p.conv_mm;
+          const int r = m0 - a_img * p.conv_mm;
+          a_h0 = (r / p.conv_m) * p.conv_s - p.conv_pad;
+          a_w0 = (r - (r / p.conv_m) * p.conv_m) * p.conv_s - p.conv_pad;
+        }
         for (int kt = kt0; kt < kt1; ++kt) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           mbar_expect_tx(full_bar(stage), (uint32_t)L::STAGE);
           const uint32_t a_dst = sbase + stage * L::STAGE_ALL;
           const uint32_t b_dst = a_dst + L::A_BYTES;
           const int kc = kt * BK;
-          if (!A_MN) {
+          if (IM2COL == 1) {
+            // K index = (tap, channel): tap-major, 32-channel blocks
+            const int cb = kt % p.conv_cblocks, tap = kt / p.conv_cblocks;
+            const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
+            tma_load_im2col(&tmA, a_dst, full_bar(stage), cb * 32, a_w0, a_h0, a_img,
+                            (uint16_t)ky, (uint16_t)kx);
+          } else if (!A_MN) {
             tma_load_2d(&tmA, a_dst, full_bar(stage), kc, mt * BM);
           } else {
 #pragma unroll
             for (int j = 0; j < BM / 32; ++j)
               tma_load_2d(&tmA, a_dst + j * (BK * 128), full_bar(stage), mt * BM + 32 * j, kc);
           }
-          if (!B_MN) {
+          if (IM2COL == 2) {
+            // B(j = (tap, ch), r = pixel): BK output pixels x 32 channels per chunk
+            const int img = kc / p.conv_mm;
+            const int r = kc - img * p.conv_mm;
+            const int h0 = (r / p.conv_m) * p.conv_s - p.conv_pad;
+            const int w0 = (r - (r / p.conv_m) * p.conv_m) * p.conv_s - p.conv_pad;
+            const int taps = p.conv_k * p.conv_k;
+#pragma unroll
+            for (int j = 0; j < BN / 32; ++j) {
+              const int blk = nt * (BN / 32) + j;
+              int tap = blk / p.conv_cblocks;
+              const int cb = blk - tap * p.conv_cblocks;
+              if (tap >= taps) tap = taps - 1;  // columns past N: any valid load, discarded
+              const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
+              tma_load_im2col(&tmB, b_dst + j * (BK * 128), full_bar(stage), cb * 32, w0, h0, img,
+                              (uint16_t)ky, (uint16_t)kx);
+            }
+          } else if (!B_MN) {
             tma_load_2d(&tmB, b_dst, full_bar(stage), kc, nt * BN);
           } else {
 #pragma unroll
@@ -670,16 +717,60 @@ Plan make_plan(int M, int N, int K, int sms) {
   return pl;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool SPLIT3>
+// Activation tensor behind an im2col operand (NHWC, pixel stride cs).
+struct ConvGeom {
+  const float* X;
+  int b, n, c, cs, k, s, pad, m;
+};
+
+int make_tmap_im2col(CUtensorMap* map, const ConvGeom& g, int pixels, bool mn_major) {
+  static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(ptr);
+  });
+  if (!fn) {
+    omni::set_error("cuTensorMapEncodeIm2col unavailable");
+    return OMNI_ECUDA;
+  }
+  // dims (C, W, H, N) of the NHWC tensor; W is the fastest spatial index.
+  cuuint64_t dims[4] = {(cuuint64_t)g.c, (cuuint64_t)g.n, (cuuint64_t)g.n, (cuuint64_t)g.b};
+  cuuint64_t strides[3] = {(cuuint64_t)g.cs * 4, (cuuint64_t)g.n * g.cs * 4,
+                           (cuuint64_t)g.n * g.n * g.cs * 4};
+  // fprop bounding box (CUTLASS convention): lower = -pad, upper = pad - (k - 1)
+  int lower[2] = {-g.pad, -g.pad};
+  int upper[2] = {g.pad - (g.k - 1), g.pad - (g.k - 1)};
+  cuuint32_t estr[4] = {1, (cuuint32_t)g.s, (cuuint32_t)g.s, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(g.X), dims, strides,
+                  lower, upper, 32, (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    omni::set_error("cuTensorMapEncodeIm2col failed (%d): b=%d n=%d c=%d cs=%d k=%d s=%d pad=%d",
+                    (int)r, g.b, g.n, g.c, g.cs, g.k, g.s, g.pad);
+    return OMNI_ECUDA;
+  }
+  return OMNI_OK;
+}
+
+template <int BN, bool A_MN, bool B_MN, bool SPLIT3, int IM2COL>
 int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, long long ldb,
-              const Params& p, cudaStream_t st) {
+              const Params& p, cudaStream_t st, const ConvGeom* cg) {
   using L = Layout<BN, SPLIT3>;
   CUtensorMap ta, tb;
-  int rc = A_MN ? make_tmap(&ta, A, p.M, p.K, lda, 32, BK, true)
-                : make_tmap(&ta, A, p.K, p.M, lda, 32, BM, false);
+  int rc;
+  if (IM2COL == 1) rc = make_tmap_im2col(&ta, *cg, BM, false);
+  else rc = A_MN ? make_tmap(&ta, A, p.M, p.K, lda, 32, BK, true)
+                 : make_tmap(&ta, A, p.K, p.M, lda, 32, BM, false);
   if (rc) return rc;
-  rc = B_MN ? make_tmap(&tb, B, p.N, p.K, ldb, 32, BK, true)
-            : make_tmap(&tb, B, p.K, p.N, ldb, 32, BN, false);
+  if (IM2COL == 2) rc = make_tmap_im2col(&tb, *cg, BK, true);
+  else rc = B_MN ? make_tmap(&tb, B, p.N, p.K, ldb, 32, BK, true)
+                 : make_tmap(&tb, B, p.K, p.N, ldb, 32, BN, false);
   if (rc) return rc;
   CUtensorMap tc;
   memset(&tc, 0, sizeof(tc));
@@ -687,22 +778,22 @@ int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, lon
     rc = make_tmap_c(&tc, p.C, p.N, p.M, p.ldc, p.splits, p.split_stride);
     if (rc) return rc;
   }
-  auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT3>;
+  auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT3, IM2COL>;
   OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
   kern<<<pl.grid, L::THREADS, L::BYTES, st>>>(ta, tb, tc, p);
   return omni::check_launch("gemm_tf32");
 }
 
-template <bool A_MN, bool B_MN, bool SPLIT3>
+template <bool A_MN, bool B_MN, bool SPLIT3, int IM2COL>
 int dispatch_bn(const Plan& pl, const float* A, long long lda, const float* B, long long ldb,
-                const Params& p, cudaStream_t st) {
+                const Params& p, cudaStream_t st, const ConvGeom* cg = nullptr) {
   switch (pl.bn) {
-    case 32: return launch_tc<32, A_MN, B_MN, SPLIT3>(pl, A, lda, B, ldb, p, st);
-    case 64: return launch_tc<64, A_MN, B_MN, SPLIT3>(pl, A, lda, B, ldb, p, st);
-    case 96: return launch_tc<96, A_MN, B_MN, SPLIT3>(pl, A, lda, B, ldb, p, st);
-    case 128: return launch_tc<128, A_MN, B_MN, SPLIT3>(pl, A, lda, B, ldb, p, st);
-    case 192: return launch_tc<192, A_MN, B_MN, SPLIT3>(pl, A, lda, B, ldb, p, st);
-    case 256: return launch_tc<256, A_MN, B_MN, SPLIT3>(pl, A, lda, B, ldb, p, st);
+    case 32: return launch_tc<32, A_MN, B_MN, SPLIT3, IM2COL>(pl, A, lda, B, ldb, p, st, cg);
+    case 64: return launch_tc<64, A_MN, B_MN, SPLIT3, IM2COL>(pl, A, lda, B, ldb, p, st, cg);
+    case 96: return launch_tc<96, A_MN, B_MN, SPLIT3, IM2COL>(pl, A, lda, B, ldb, p, st, cg);
+    case 128: return launch_tc<128, A_MN, B_MN, SPLIT3, IM2COL>(pl, A, lda, B, ldb, p, st, cg);
+    case 192: return launch_tc<192, A_MN, B_MN, SPLIT3, IM2COL>(pl, A, lda, B, ldb, p, st, cg);
+    case 256: return launch_tc<256, A_MN, B_MN, SPLIT3, IM2COL>(pl, A, lda, B, ldb, p, st, cg);
   }
   omni::set_error("gemm: no kernel for BN=%d", pl.bn);
   return OMNI_EUNSUPPORTED;
@@ -711,10 +802,82 @@ int dispatch_bn(const Plan& pl, const float* A, long long lda, const float* B, l
 template <bool SPLIT3>
 int dispatch_major(const Plan& pl, int a_mn, int b_mn, const float* A, long long lda,
                    const float* B, long long ldb, const Params& p, cudaStream_t st) {
-  if (!a_mn && !b_mn) return dispatch_bn<false, false, SPLIT3>(pl, A, lda, B, ldb, p, st);
-  if (!a_mn && b_mn) return dispatch_bn<false, true, SPLIT3>(pl, A, lda, B, ldb, p, st);
-  if (a_mn && !b_mn) return dispatch_bn<true, false, SPLIT3>(pl, A, lda, B, ldb, p, st);
-  return dispatch_bn<true, true, SPLIT3>(pl, A, lda, B, ldb, p, st);
+  if (!a_mn && !b_mn) return dispatch_bn<false, false, SPLIT3, 0>(pl, A, lda, B, ldb, p, st);
+  if (!a_mn && b_mn) return dispatch_bn<false, true, SPLIT3, 0>(pl, A, lda, B, ldb, p, st);
+  if (a_mn && !b_mn) return dispatch_bn<true, false, SPLIT3, 0>(pl, A, lda, B, ldb, p, st);
+  return dispatch_bn<true, true, SPLIT3, 0>(pl, A, lda, B, ldb, p, st);
+}
+
+// Shared tail of omni_gemm_f32 / omni_conv_implicit_f32: plan, workspace,
+// output mode, launch (im2col variant when cg != nullptr), split-K reduce.
+int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, int a_mn,
+             const float* B, long long ldb, int b_mn, float* C, long long ldc, int epilogue,
+             const float* bias, const float* aux, long long ld_aux, float* workspace,
+             long long ws_bytes, cudaStream_t st, const ConvGeom* cg, int im2col) {
+  Params p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.epilogue = epilogue;
+  p.bias = bias;
+  p.aux = aux;
+  p.ld_aux = ld_aux;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const Plan pl = make_plan(M, N, K, omni::sm_count_cached(dev));
+  p.m_tiles = pl.m_tiles;
+  p.n_tiles = pl.n_tiles;
+  p.k_tiles = pl.k_tiles;
+  p.splits = pl.splits;
+  p.kt_per_split = pl.kps;
+  p.raster_m_inner = pl.raster_m_inner;
+  if (cg) {
+    p.conv_m = cg->m;
+    p.conv_mm = cg->m * cg->m;
+    p.conv_s = cg->s;
+    p.conv_pad = cg->pad;
+    p.conv_k = cg->k;
+    p.conv_cblocks = cg->c / 32;
+  }
+  if (pl.splits > 1) {
+    const long long need = (long long)pl.splits * M * N * 4;
+    OMNI_REQUIRE(workspace && ws_bytes >= need,
+                 "gemm: split-K workspace of %lld bytes required (got %lld)", need, ws_bytes);
+    OMNI_REQUIRE(((uintptr_t)workspace & 15) == 0, "gemm: workspace must be 16-byte aligned");
+    p.C = workspace;
+    p.ldc = N;
+    p.split_stride = (long long)M * N;
+    p.vec_ok = (N % 4 == 0);
+    p.use_tma_store = (N % 4 == 0);
+  } else {
+    p.C = C;
+    p.ldc = ldc;
+    p.split_stride = 0;
+    p.vec_ok = (ldc % 4 == 0) && (((uintptr_t)C & 15) == 0);
+    p.use_tma_store = p.vec_ok && epilogue != OMNI_EPI_ACCUM;
+  }
+  if (getenv("OMNI_NO_TMA_STORE")) p.use_tma_store = 0;
+  int rc;
+  const bool s3 = precision == OMNI_PREC_3XTF32;
+  if (im2col == 1)
+    rc = s3 ? dispatch_bn<false, false, true, 1>(pl, A, lda, B, ldb, p, st, cg)
+            : dispatch_bn<false, false, false, 1>(pl, A, lda, B, ldb, p, st, cg);
+  else if (im2col == 2)
+    rc = s3 ? dispatch_bn<true, true, true, 2>(pl, A, lda, B, ldb, p, st, cg)
+            : dispatch_bn<true, true, false, 2>(pl, A, lda, B, ldb, p, st, cg);
+  else
+    rc = s3 ? dispatch_major<true>(pl, a_mn, b_mn ? 1 : 0, A, lda, B, ldb, p, st)
+            : dispatch_major<false>(pl, a_mn, b_mn ? 1 : 0, A, lda, B, ldb, p, st);
+  if (rc) return rc;
+  if (pl.splits > 1) {
+    Params q = p;
+    q.C = C;
+    q.ldc = ldc;
+    splitk_reduce_kernel<<<omni::grid_for((long long)M * N, 256), 256, 0, st>>>(workspace,
+                                                                              pl.splits, M, N, q);
+    rc = omni::check_launch("splitk_reduce");
+  }
+  return rc;
 }
 
 }  // namespace gemm
@@ -753,15 +916,15 @@ int omni_gemm_f32(int precision, int M, int N, int K, const float* A, long long 
   OMNI_REQUIRE(epilogue != OMNI_EPI_MASK_AUX || (aux && ld_aux >= N),
                "gemm: mask epilogue needs aux");
   cudaStream_t st = omni::as_stream(stream);
-  gemm::Params p{};
-  p.M = M;
-  p.N = N;
-  p.K = K;
-  p.epilogue = epilogue;
-  p.bias = bias;
-  p.aux = aux;
-  p.ld_aux = ld_aux;
   if (precision == OMNI_PREC_FP32_SIMT) {
+    gemm::Params p{};
+    p.M = M;
+    p.N = N;
+    p.K = K;
+    p.epilogue = epilogue;
+    p.bias = bias;
+    p.aux = aux;
+    p.ld_aux = ld_aux;
     p.C = C;
     p.ldc = ldc;
     dim3 grid((unsigned)omni::ceil_div(N, 16), (unsigned)omni::ceil_div(M, 16));
@@ -779,47 +942,66 @@ int omni_gemm_f32(int precision, int M, int N, int K, const float* A, long long 
                "gemm: lda/ldb must be multiples of 4 for TMA (lda=%lld ldb=%lld)", lda, ldb);
   OMNI_REQUIRE(((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0,
                "gemm: A and B must be 16-byte aligned for TMA");
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const gemm::Plan pl = gemm::make_plan(M, N, K, omni::sm_count_cached(dev));
-  p.m_tiles = pl.m_tiles;
-  p.n_tiles = pl.n_tiles;
-  p.k_tiles = pl.k_tiles;
-  p.splits = pl.splits;
-  p.kt_per_split = pl.kps;
-  p.raster_m_inner = pl.raster_m_inner;
-  if (pl.splits > 1) {
-    const long long need = (long long)pl.splits * M * N * 4;
-    OMNI_REQUIRE(workspace && ws_bytes >= need,
-                 "gemm: split-K workspace of %lld bytes required (got %lld)", need, ws_bytes);
-    OMNI_REQUIRE(((uintptr_t)workspace & 15) == 0, "gemm: workspace must be 16-byte aligned");
-    p.C = workspace;
-    p.ldc = N;
-    p.split_stride = (long long)M * N;
-    p.vec_ok = (N % 4 == 0);
-    p.use_tma_store = (N % 4 == 0);
+  return gemm::run_gemm(precision, M, N, K, A, lda, a_mn_major, B, ldb, b_mn_major, C, ldc,
+                        epilogue, bias, aux, ld_aux, workspace, ws_bytes, st, nullptr, 0);
+}
+
+static int conv_shape(int op, int b, int n, int c, int k, int stride, int pad, int d_out, int* M,
+                      int* N, int* K, int* m) {
+  OMNI_REQUIRE(op == OMNI_CONV_FPROP || op == OMNI_CONV_WGRAD, "conv: unknown op %d", op);
+  OMNI_REQUIRE(b >= 1 && n >= 1 && k >= 1 && stride >= 1 && pad >= 0 && d_out >= 1,
+               "n, k, d_in, d_out, stride must be positive");
+  OMNI_REQUIRE(c % 32 == 0, "implicit conv needs d_in %% 32 == 0 (got %d)", c);
+  OMNI_REQUIRE(k <= n + 2 * pad && (n + 2 * pad - k) % stride == 0, "conv: bad geometry");
+  OMNI_REQUIRE(pad <= 127 && k - 1 - pad <= 128, "conv: padding outside the im2col box range");
+  *m = (n + 2 * pad - k) / stride + 1;
+  const long long pix = (long long)b * (*m) * (*m);
+  OMNI_REQUIRE(pix < (1LL << 31), "conv: too many output pixels");
+  if (op == OMNI_CONV_FPROP) {
+    *M = (int)pix;
+    *N = d_out;
+    *K = k * k * c;
   } else {
-    p.C = C;
-    p.ldc = ldc;
-    p.split_stride = 0;
-    p.vec_ok = (ldc % 4 == 0) && (((uintptr_t)C & 15) == 0);
-    p.use_tma_store = p.vec_ok && epilogue != OMNI_EPI_ACCUM;
+    *M = d_out;
+    *N = k * k * c;
+    *K = (int)pix;
   }
-  if (getenv("OMNI_NO_TMA_STORE")) p.use_tma_store = 0;
-  const int b_mn = b_mn_major ? 1 : 0;
-  int rc = precision == OMNI_PREC_3XTF32
-               ? gemm::dispatch_major<true>(pl, a_mn_major, b_mn, A, lda, B, ldb, p, st)
-               : gemm::dispatch_major<false>(pl, a_mn_major, b_mn, A, lda, B, ldb, p, st);
+  return OMNI_OK;
+}
+
+long long omni_conv_implicit_plan(int precision, int op, int b, int n, int c, int k, int stride,
+                                  int pad, int d_out) {
+  int M, N, K, m;
+  if (conv_shape(op, b, n, c, k, stride, pad, d_out, &M, &N, &K, &m)) return -1;
+  return omni_gemm_plan(precision, M, N, K, 0, 0, nullptr, nullptr);
+}
+
+int omni_conv_implicit_f32(int precision, int op, const float* X, int b, int n, int c, int cs,
+                           int k, int stride, int pad, int d_out, const float* G, long long ldg,
+                           float* Y, long long ldy, int epilogue, const float* bias,
+                           const float* aux, long long ld_aux, float* workspace,
+                           long long ws_bytes, void* stream) {
+  int M, N, K, m;
+  int rc = conv_shape(op, b, n, c, k, stride, pad, d_out, &M, &N, &K, &m);
   if (rc) return rc;
-  if (pl.splits > 1) {
-    gemm::Params q = p;
-    q.C = C;
-    q.ldc = ldc;
-    gemm::splitk_reduce_kernel<<<omni::grid_for((long long)M * N, 256), 256, 0, st>>>(
-        workspace, pl.splits, M, N, q);
-    rc = omni::check_launch("splitk_reduce");
-  }
-  return rc;
+  OMNI_REQUIRE(precision == OMNI_PREC_TF32 || precision == OMNI_PREC_3XTF32,
+               "conv: precision must be TF32 or 3xTF32");
+  OMNI_REQUIRE(cs >= c && cs % 4 == 0 && ((uintptr_t)X & 15) == 0,
+               "conv: X must be 16-byte aligned NHWC with cs %% 4 == 0");
+  OMNI_REQUIRE(ldg % 4 == 0 && ((uintptr_t)G & 15) == 0, "conv: G must be 16-byte aligned, ldg %% 4 == 0");
+  OMNI_REQUIRE(ldg >= (op == OMNI_CONV_FPROP ? K : d_out) && ldy >= N, "conv: leading dimension too small");
+  OMNI_REQUIRE(epilogue >= 0 && epilogue <= 5, "conv: unknown epilogue %d", epilogue);
+  OMNI_REQUIRE(!(epilogue == OMNI_EPI_BIAS || epilogue == OMNI_EPI_BIAS_RELU) || bias,
+               "conv: bias epilogue needs a bias vector");
+  OMNI_REQUIRE(epilogue != OMNI_EPI_MASK_AUX || (aux && ld_aux >= N), "conv: mask epilogue needs aux");
+  gemm::ConvGeom cg{X, b, n, c, cs, k, stride, pad, m};
+  cudaStream_t st = omni::as_stream(stream);
+  if (op == OMNI_CONV_FPROP)   // A = im2col(X) (K-major), B = G weights (d_out x ldg, K-major)
+    return gemm::run_gemm(precision, M, N, K, nullptr, 0, 0, G, ldg, 0, Y, ldy, epilogue, bias, aux,
+                          ld_aux, workspace, ws_bytes, st, &cg, 1);
+  // WGRAD: A = G = dY (pixels x ldg, MN-major), B = im2col(X) (MN-major)
+  return gemm::run_gemm(precision, M, N, K, G, ldg, 1, nullptr, 0, 1, Y, ldy, epilogue, bias, aux,
+                        ld_aux, workspace, ws_bytes, st, &cg, 2);
 }
 
 }  // extern "C"

@@ -252,6 +252,28 @@ __global__ void __launch_bounds__(kThreads) weight_from_tap_kernel(
   }
 }
 
+// Data-gradient weights of a stride-1 conv: the spatially flipped, in/out
+// transposed kernel in tap-major rows,
+//   Wf[ch*ld + (kx*k + ky)*o + oo] = W[oo, ch, k-1-kx, k-1-ky]   (W is OIHW),
+// so dX = conv(dY, Wf) with padding k-1-pad is one implicit forward GEMM.
+__global__ void __launch_bounds__(kThreads) weight_flip_kernel(
+    const float* __restrict__ W, int o, int c, int k, float* __restrict__ Wf, long long ld) {
+  const long long total = (long long)c * ld;
+  const int K = o * k * k;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int ch = (int)(idx / ld);
+    const int col = (int)(idx - (long long)ch * ld);
+    float v = 0.f;
+    if (col < K) {
+      const int tap = col / o, oo = col - (col / o) * o;
+      const int kx = tap / k, ky = tap - (tap / k) * k;
+      v = W[(((long long)oo * c + ch) * k + (k - 1 - kx)) * k + (k - 1 - ky)];
+    }
+    Wf[idx] = v;
+  }
+}
+
 // Batched tiled transpose through shared memory (32x33 tile: no bank conflicts).
 template <typename T>
 __global__ void __launch_bounds__(256) transpose_kernel(
@@ -420,6 +442,14 @@ int omni_conv_weight_to_tap_f32(float* W, int o, int c, int k, float* Wt, long l
                              st>>>(Wt, o, c, k, W, ld, bias);
   }
   return omni::check_launch("conv_weight_to_tap");
+}
+
+int omni_conv_weight_flip_f32(const float* W, int o, int c, int k, float* Wf, long long ld,
+                              void* stream) {
+  OMNI_REQUIRE(o >= 1 && c >= 1 && k >= 1 && ld >= (long long)o * k * k, "weight flip: bad shape");
+  weight_flip_kernel<<<omni::grid_for((long long)c * ld, kThreads), kThreads, 0,
+                       omni::as_stream(stream)>>>(W, o, c, k, Wf, ld);
+  return omni::check_launch("conv_weight_flip");
 }
 
 int omni_transpose_f32(const float* src, long long lds, long long src_bstride, int rows, int cols,

@@ -148,6 +148,33 @@ def matmul(A: torch.Tensor, B: torch.Tensor, precision: int = _abi.PREC_3XTF32) 
     return gemm(M, N, K, Ap, lda, False, Bp, ldb, True, C, N, precision=precision)
 
 
+def conv_implicit_workspace_bytes(precision: int, op: int, b: int, n: int, c: int, k: int,
+                                  stride: int, pad: int, d_out: int) -> int:
+    return int(query("omni_conv_implicit_plan", precision, op, b, n, c, k, stride, pad, d_out))
+
+
+def conv_implicit(op: int, X: torch.Tensor, c: int, k: int, stride: int, pad: int, d_out: int,
+                  G: torch.Tensor, ldg: int, Y: torch.Tensor, ldy: int, *,
+                  precision: int = _abi.PREC_TF32, epilogue: int = _abi.EPI_STORE,
+                  bias: torch.Tensor | None = None, aux: torch.Tensor | None = None,
+                  ld_aux: int = 0, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Implicit-GEMM conv (TMA im2col operands) -- see include/omni.h.  X is NHWC
+    (b, n, n, cs); op = _abi.CONV_FPROP or _abi.CONV_WGRAD."""
+    _require_cuda(X, G, Y)
+    b, n, _, cs = X.shape
+    need = conv_implicit_workspace_bytes(precision, op, b, n, c, k, stride, pad, d_out)
+    if need > 0 and (workspace is None or workspace.numel() * 4 < need):
+        workspace = _workspace(need, Y.device)
+    call("omni_conv_implicit_f32", precision, op, _ptr(X), b, n, c, cs, k, stride, pad, d_out,
+         _ptr(G), ldg, _ptr(Y), ldy, epilogue, _ptr(bias), _ptr(aux), ld_aux, _ptr(workspace),
+         0 if workspace is None else workspace.numel() * 4, _stream())
+    return Y
+
+
+def conv_weight_flip(W: torch.Tensor, o: int, c: int, k: int, Wf: torch.Tensor, ld: int) -> None:
+    call("omni_conv_weight_flip_f32", _ptr(W), o, c, k, _ptr(Wf), ld, _stream())
+
+
 # ----------------------------------------------------------------- K3 ----
 def pool_out_size(n: int, k: int, stride: int, pad: int, ceil_mode: bool) -> int:
     v = query("omni_pool_out_size", n, k, stride, pad, int(ceil_mode))

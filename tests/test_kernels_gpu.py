@@ -291,3 +291,81 @@ def test_bias_ones_column(geom):
     b2 = torch.empty_like(bias)
     K.conv_weight_to_tap(W2, o, c, k, Wt, ld, inverse=True, bias=b2)
     assert torch.equal(W2, W) and torch.equal(b2, bias)
+
+
+IMPLICIT_GEOMS = [  # b, n, c, k, s, p, d_out
+    (2, 27, 96, 5, 1, 2, 256),
+    (3, 13, 64, 3, 1, 1, 96),
+    (2, 16, 32, 3, 2, 1, 64),
+    (1, 9, 32, 1, 1, 0, 32),
+    (2, 13, 384, 3, 1, 1, 256),
+]
+
+
+def _conv_inputs(b, n, c, k, d, seed):
+    gen = torch.Generator().manual_seed(seed)
+    X = torch.randn(b, n, n, c, generator=gen)
+    W = torch.randn(d, c, k, k, generator=gen) / (c * k * k) ** 0.5
+    return X.to(DEV), W.to(DEV)
+
+
+@pytest.mark.parametrize("geom", IMPLICIT_GEOMS)
+@pytest.mark.parametrize("prec", ["tf32", "3xtf32"])
+def test_conv_implicit_fprop(geom, prec):
+    """TMA-im2col implicit GEMM == explicit lowering + GEMM (same operands, same
+    K order) and == torch conv2d in float64 within the precision's bound."""
+    b, n, c, k, s, p, d = geom
+    X, W = _conv_inputs(b, n, c, k, d, 11)
+    m = (n + 2 * p - k) // s + 1
+    Kc = c * k * k
+    ld = K.round_up(Kc, 32)
+    Wt = torch.zeros(d, ld, device=DEV)
+    K.conv_weight_to_tap(W, d, c, k, Wt, ld)
+    pr = _abi.PRECISIONS[prec]
+    Y = torch.full((b * m * m, d), float("nan"), device=DEV)
+    K.conv_implicit(_abi.CONV_FPROP, X, c, k, s, p, d, Wt, ld, Y, d, precision=pr)
+    D = K.lower_nhwc(X, c, k, s, p, ld)
+    Yr = torch.empty(b * m * m, d, device=DEV)
+    K.gemm(b * m * m, d, Kc, D, ld, False, Wt, ld, False, Yr, d, precision=pr)
+    torch.cuda.synchronize()
+    assert rel_err(Y.cpu(), Yr.cpu()) < 1e-6, rel_err(Y.cpu(), Yr.cpu())
+    ref = torch.nn.functional.conv2d(X.permute(0, 3, 1, 2).double().cpu(), W.double().cpu(),
+                                     stride=s, padding=p).permute(0, 2, 3, 1).reshape(b * m * m, d)
+    assert rel_err(Y.cpu(), ref) < (3e-3 if prec == "tf32" else 2e-6)
+
+
+@pytest.mark.parametrize("geom", IMPLICIT_GEOMS)
+def test_conv_implicit_wgrad(geom):
+    b, n, c, k, s, p, d = geom
+    X, _ = _conv_inputs(b, n, c, k, d, 12)
+    m = (n + 2 * p - k) // s + 1
+    Kc = c * k * k
+    ld = K.round_up(Kc, 32)
+    dY = torch.randn(b * m * m, d, device=DEV)
+    dW = torch.full((d, ld), float("nan"), device=DEV)
+    K.conv_implicit(_abi.CONV_WGRAD, X, c, k, s, p, d, dY, d, dW, ld, precision=_abi.PREC_3XTF32)
+    D = K.lower_nhwc(X, c, k, s, p, ld)
+    ref = (dY.double().t() @ D[:, :Kc].double()).cpu()
+    torch.cuda.synchronize()
+    assert rel_err(dW[:, :Kc].cpu(), ref) < 2e-6 * max(1.0, (b * m * m / 1000) ** 0.5)
+
+
+@pytest.mark.parametrize("geom", [g for g in IMPLICIT_GEOMS if g[4] == 1 and g[6] % 32 == 0])
+def test_conv_implicit_dgrad_via_flipped_weights(geom):
+    """Stride-1 data gradient as one implicit forward conv of dY with the flipped,
+    transposed kernel (padding k-1-p) == col2im of the explicit dgrad GEMM."""
+    b, n, c, k, s, p, d = geom
+    X, W = _conv_inputs(b, n, c, k, d, 13)
+    m = n + 2 * p - k + 1
+    dY = torch.randn(b, m, m, d, device=DEV)
+    ldf = K.round_up(d * k * k, 32)
+    Wf = torch.zeros(c, ldf, device=DEV)
+    K.conv_weight_flip(W, d, c, k, Wf, ldf)
+    dX = torch.full((b, n, n, c), float("nan"), device=DEV)
+    K.conv_implicit(_abi.CONV_FPROP, dY, d, k, 1, k - 1 - p, c, Wf, ldf, dX.view(-1, c), c,
+                    precision=_abi.PREC_3XTF32)
+    Xd = X.permute(0, 3, 1, 2).double().cpu().requires_grad_(True)
+    out = torch.nn.functional.conv2d(Xd, W.double().cpu(), padding=p)
+    out.backward(dY.permute(0, 3, 1, 2).double().cpu())
+    torch.cuda.synchronize()
+    assert rel_err(dX.cpu(), Xd.grad.permute(0, 2, 3, 1)) < 2e-6
