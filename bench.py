@@ -253,40 +253,26 @@ def run_ours(args):
     value = args.steps * b * world / (ms / 1000.0)
     loss_now = sess.last_loss()
 
-    # ---- per-GEMM breakdown (one instrumented step, after the timed region)
-    records = []
-    orig = eng._gemm
-
-    def timed_gemm(M, N, Kd, *a, **kw):
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        orig(M, N, Kd, *a, **kw)
-        ev1.record()
-        records.append((M, N, Kd, ev0, ev1))
-
-    eng._gemm = timed_gemm
+    # ---- per-GEMM breakdown (one instrumented step, after the timed region):
+    # CUDA events around every conv / FC GEMM launch (explicit or implicit).
+    eng.timer = []
     torch.cuda.synchronize()
     reps = 3
     for r in range(reps):
         step(total - 1)
     torch.cuda.synchronize()
-    eng._gemm = orig
+    records, eng.timer = eng.timer, None
     per_step = len(records) // reps
-    conv_shapes = set()
-    for op in eng.ops:
-        if op.kind == "conv":
-            for shp in eng._gemm_shapes(op, b):
-                conv_shapes.add(shp)
     conv_ms = fc_ms = 0.0
     rows = []
-    for M, N, Kd, a0, a1 in records:
-        t = a0.elapsed_time(a1) / reps
-        if (M, N, Kd) in conv_shapes:
-            conv_ms += t
+    for M, N, Kd, kind, a0, a1 in records:
+        t = a0.elapsed_time(a1)
+        if kind == "conv":
+            conv_ms += t / reps
         else:
-            fc_ms += t
-        rows.append({"M": M, "N": N, "K": Kd, "ms": a0.elapsed_time(a1),
-                     "tflops": 2.0 * M * N * Kd / (a0.elapsed_time(a1) * 1e9)})
+            fc_ms += t / reps
+        rows.append({"M": M, "N": N, "K": Kd, "kind": kind, "ms": t,
+                     "tflops": 2.0 * M * N * Kd / (t * 1e9)})
     conv_flops_step = net.conv_flops_per_image() * b
     achieved = conv_flops_step / (conv_ms * 1e-3) / 1e12 if conv_ms > 0 else 0.0
     peaks = measured_peaks()

@@ -73,6 +73,9 @@ class Op:
     Kf: int = 0
     ldK: int = 0
     w_inplace: bool = False
+    implicit: bool = False
+    ldF: int = 0
+    wflip: torch.Tensor | None = None
     dhat: torch.Tensor | None = None
     wstage: torch.Tensor | None = None
     dwstage: torch.Tensor | None = None
@@ -87,7 +90,8 @@ class Op:
 class GpuNet:
     """Device buffers + launch sequence for one NetSpec at a fixed max batch."""
 
-    def __init__(self, net: NetSpec, batch: int, device=None, precision: str = "tf32"):
+    def __init__(self, net: NetSpec, batch: int, device=None, precision: str = "tf32",
+                 explicit_only: bool = False):
         if precision not in ("tf32", "3xtf32"):
             raise ValueError("precision must be 'tf32' or '3xtf32'")
         self.net = net
@@ -119,11 +123,24 @@ class GpuNet:
                         boff=g.param_offsets[1], relu=nxt_relu, first_param_layer=first_param,
                         c_in=c, k=L.k, s=L.stride, p=L.pad, m=m)
                 op.Kc = c * L.k * L.k
-                # bias folded into the GEMM: ones column Kc in Dhat, bias in column Kc of W
-                op.Kf = op.Kc + (1 if op.boff >= 0 else 0)
-                # 128-byte row pitch: TMA boxes and TMA-stored rows stay line-aligned
-                op.ldK = K.round_up(op.Kf, 32)
-                op.dhat = z(self.b * m * m, op.ldK)
+                # Implicit GEMM (TMA im2col straight from the NHWC activation, no
+                # lowered matrix) when the channels tile into 32-wide K blocks; the
+                # data gradient then runs as a forward conv of dY with the flipped
+                # kernel, which needs stride 1 and d_out % 32 == 0.
+                op.implicit = (c % 32 == 0 and cur.cs % 4 == 0 and not explicit_only and
+                               (first_param or (L.stride == 1 and d % 32 == 0)))
+                if op.implicit:
+                    op.Kf = op.Kc
+                    op.ldK = K.round_up(op.Kf, 32)
+                    if not first_param:
+                        op.ldF = K.round_up(d * L.k * L.k, 32)
+                        op.wflip = z(c, op.ldF)
+                else:
+                    # bias folded into the GEMM: ones column Kc in Dhat, bias in column Kc of W
+                    op.Kf = op.Kc + (1 if op.boff >= 0 else 0)
+                    # 128-byte row pitch: TMA boxes and TMA-stored rows stay line-aligned
+                    op.ldK = K.round_up(op.Kf, 32)
+                    op.dhat = z(self.b * m * m, op.ldK)
                 op.wstage = z(d, op.ldK)
                 op.dwstage = z(d, op.ldK)
                 first_param = False
@@ -178,12 +195,15 @@ class GpuNet:
                 ws = max(ws, K.gemm_workspace_bytes(self.prec, M, N, Kd, False, False))
             if op.kind == "fc" and op.boff >= 0:
                 bws = max(bws, K.bias_grad_ws_elems(self.b, op.layer.d_out))
-            if op.kind == "conv" and not op.first_param_layer:
+            if op.kind == "conv" and op.implicit and op.boff >= 0:
+                bws = max(bws, K.bias_grad_ws_elems(self.b * op.m * op.m, op.layer.d_out))
+            if op.kind == "conv" and not op.first_param_layer and not op.implicit:
                 dd = max(dd, self.b * op.m * op.m * op.ldK)
         self.gemm_ws = z(max(ws // 4, 4))
         self.bias_ws = z(max(bws, 4))
         self.ddhat = z(max(dd, 4))
         self.graph = None
+        self.timer = None   # list -> (M, N, K, kind, ev0, ev1) per GEMM launch
 
     # ------------------------------------------------------------ shapes --
     @staticmethod
@@ -193,7 +213,10 @@ class GpuNet:
             d = op.layer.d_out
             out = [(Mr, d, op.Kf), (d, op.Kf, Mr)]
             if not op.first_param_layer:
-                out.append((Mr, op.Kc, d))
+                if op.implicit:
+                    out.append((b * op.inp.n * op.inp.n, op.c_in, d * op.k * op.k))
+                else:
+                    out.append((Mr, op.Kc, d))
             return out
         if op.kind == "fc":
             d = op.layer.d_out
@@ -203,10 +226,33 @@ class GpuNet:
             return out
         return []
 
+    def _timed(self, M, N, Kd, kind, fn):
+        if self.timer is None:
+            fn()
+            return
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        self.timer.append((M, N, Kd, kind, e0, e1))
+
     def _gemm(self, M, N, Kd, A, lda, a_mn, B, ldb, b_mn, C, ldc, epi=_abi.EPI_STORE, bias=None,
+              aux=None, ld_aux=0, kind="gemm"):
+        self._timed(M, N, Kd, kind, lambda: K.gemm(
+            M, N, Kd, A, lda, a_mn, B, ldb, b_mn, C, ldc, precision=self.prec, epilogue=epi,
+            bias=bias, aux=aux, ld_aux=ld_aux, workspace=self.gemm_ws))
+
+    def _conv(self, op_code, X, c, k, s, p, d, G, ldg, Y, ldy, epi=_abi.EPI_STORE, bias=None,
               aux=None, ld_aux=0):
-        K.gemm(M, N, Kd, A, lda, a_mn, B, ldb, b_mn, C, ldc, precision=self.prec, epilogue=epi,
-               bias=bias, aux=aux, ld_aux=ld_aux, workspace=self.gemm_ws)
+        b, n = X.shape[0], X.shape[1]
+        m = (n + 2 * p - k) // s + 1
+        if op_code == _abi.CONV_FPROP:
+            M, N, Kd = b * m * m, d, c * k * k
+        else:
+            M, N, Kd = d, c * k * k, b * m * m
+        self._timed(M, N, Kd, "conv", lambda: K.conv_implicit(
+            op_code, X, c, k, s, p, d, G, ldg, Y, ldy, precision=self.prec, epilogue=epi,
+            bias=bias, aux=aux, ld_aux=ld_aux, workspace=self.gemm_ws))
 
     # ----------------------------------------------------------- staging --
     def stage_weights(self, W: torch.Tensor) -> None:
@@ -218,9 +264,12 @@ class GpuNet:
         for op in self.ops:
             if op.kind == "conv":
                 d = op.layer.d_out
-                bias = W[op.boff:op.boff + d] if op.boff >= 0 else None
+                bias = W[op.boff:op.boff + d] if op.boff >= 0 and not op.implicit else None
                 K.conv_weight_to_tap(W[op.woff:op.woff + op.wsz], d, op.c_in, op.k, op.wstage,
                                      op.ldK, bias=bias)
+                if op.wflip is not None:
+                    K.conv_weight_flip(W[op.woff:op.woff + op.wsz], d, op.c_in, op.k, op.wflip,
+                                       op.ldF)
             elif op.kind == "fc" and not op.w_inplace:
                 d = op.layer.d_out
                 K.transpose(W[op.woff:op.woff + op.wsz], d, 0, op.f_in, d, op.wstage, op.flat.cs, 0, 1)
@@ -237,11 +286,21 @@ class GpuNet:
             if op.kind == "conv":
                 d = L.d_out
                 Mr = b * op.m * op.m
+                if op.implicit:
+                    if op.boff >= 0:
+                        epi = _abi.EPI_BIAS_RELU if op.relu else _abi.EPI_BIAS
+                        bias = W[op.boff:op.boff + d]
+                    else:
+                        epi = _abi.EPI_RELU if op.relu else _abi.EPI_STORE
+                        bias = None
+                    self._conv(_abi.CONV_FPROP, op.inp.value[:b], op.c_in, op.k, op.s, op.p, d,
+                               op.wstage, op.ldK, op.out.value, op.out.cs, epi, bias)
+                    continue
                 K.lower_nhwc(op.inp.value[:b], op.c_in, op.k, op.s, op.p, op.ldK, out=op.dhat,
                              ones_col=op.boff >= 0)
                 epi = _abi.EPI_RELU if op.relu else _abi.EPI_STORE
                 self._gemm(Mr, d, op.Kf, op.dhat, op.ldK, False, op.wstage, op.ldK, False,
-                           op.out.value, op.out.cs, epi)
+                           op.out.value, op.out.cs, epi, kind="conv")
             elif op.kind == "pool":
                 mode = 0 if L.mode == "max" else 1
                 K.pool_fwd(mode, op.inp.value[:b], op.inp.c, op.k, op.s, op.p, L.ceil,
@@ -326,9 +385,28 @@ class GpuNet:
                 d = L.d_out
                 Mr = b * op.m * op.m
                 dZ = op.out.grad
+                if op.implicit:
+                    self._conv(_abi.CONV_WGRAD, op.inp.value[:b], op.c_in, op.k, op.s, op.p, d, dZ,
+                               op.out.cs, op.dwstage, op.ldK)
+                    K.conv_weight_to_tap(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k, op.dwstage,
+                                         op.ldK, inverse=True)
+                    if op.boff >= 0:
+                        K.bias_grad(dZ, op.out.cs, Mr, d, G[op.boff:op.boff + d], self.bias_ws)
+                    done(op)
+                    if op.first_param_layer:
+                        continue
+                    # dX = conv(dY, flipped kernel, pad k-1-p) with the ReLU mask of X fused
+                    if op.inp.fused_relu:
+                        self._conv(_abi.CONV_FPROP, dZ[:b], d, op.k, 1, op.k - 1 - op.p, op.c_in,
+                                   op.wflip, op.ldF, op.inp.grad, op.inp.cs, _abi.EPI_MASK_AUX,
+                                   aux=op.inp.value, ld_aux=op.inp.cs)
+                    else:
+                        self._conv(_abi.CONV_FPROP, dZ[:b], d, op.k, 1, op.k - 1 - op.p, op.c_in,
+                                   op.wflip, op.ldF, op.inp.grad, op.inp.cs)
+                    continue
                 # weight (and, via the ones column, bias) gradient in one GEMM
                 self._gemm(d, op.Kf, Mr, dZ, op.out.cs, True, op.dhat, op.ldK, True, op.dwstage,
-                           op.ldK)
+                           op.ldK, kind="conv")
                 K.conv_weight_to_tap(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k, op.dwstage,
                                      op.ldK, inverse=True,
                                      bias=G[op.boff:op.boff + d] if op.boff >= 0 else None)
@@ -336,7 +414,7 @@ class GpuNet:
                 if op.first_param_layer:
                     continue
                 self._gemm(Mr, op.Kc, d, dZ, op.out.cs, False, op.wstage, op.ldK, True, self.ddhat,
-                           op.ldK)
+                           op.ldK, kind="conv")
                 K.col2im_nhwc(self.ddhat, op.ldK, b, op.inp.n, op.c_in, op.inp.cs, op.k, op.s, op.p,
                               op.inp.grad, op.inp.value if op.inp.fused_relu else None)
             elif op.kind == "pool":
@@ -375,7 +453,12 @@ class GpuNet:
         """Launches of libomni kernels in one gather + fwd + bwd + SGD step."""
         n = 2 + 1 + 1  # gathers, softmax, sgd
         for op in self.ops:
-            if op.kind == "conv":
+            if op.kind == "conv" and op.implicit:
+                n += 1 + 1 + 1   # stage, implicit fprop, implicit wgrad
+                n += 1 + (2 if op.boff >= 0 else 0)   # inverse stage, bias gradient
+                if not op.first_param_layer:
+                    n += 2       # flipped-weight stage, implicit dgrad (+ fused ReLU mask)
+            elif op.kind == "conv":
                 n += 1 + 1 + 1   # stage, lower, gemm
                 n += 1 + 1       # wgrad gemm (+ bias column), inverse stage
                 if not op.first_param_layer:
