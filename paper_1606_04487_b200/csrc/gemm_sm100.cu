@@ -52,6 +52,7 @@ struct Params {
   // implicit-GEMM convolution (IM2COL != 0): output size m, m*m, stride, pad,
   // kernel size, 32-channel blocks per filter tap
   int conv_m, conv_mm, conv_s, conv_pad, conv_k, conv_cblocks;
+  int transpose_c;  // store C^T: C[j*ldc + i] (weight gradient with im2col as the A operand)
 };
 
 template <int BN, bool SPLIT3>
@@ -343,6 +344,23 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
             const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
             tma_load_im2col(&tmA, a_dst, full_bar(stage), cb * 32, a_w0, a_h0, a_img,
                             (uint16_t)ky, (uint16_t)kx);
+          } else if (IM2COL == 3) {
+            // A(i = (tap, ch), r = pixel): BK output pixels x 32 channels per 32-row chunk
+            const int img = kc / p.conv_mm;
+            const int r = kc - img * p.conv_mm;
+            const int h0 = (r / p.conv_m) * p.conv_s - p.conv_pad;
+            const int w0 = (r - (r / p.conv_m) * p.conv_m) * p.conv_s - p.conv_pad;
+            const int taps = p.conv_k * p.conv_k;
+#pragma unroll
+            for (int j = 0; j < BM / 32; ++j) {
+              const int blk = mt * (BM / 32) + j;
+              int tap = blk / p.conv_cblocks;
+              const int cb = blk - tap * p.conv_cblocks;
+              if (tap >= taps) tap = taps - 1;  // rows past M: any valid load, discarded
+              const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
+              tma_load_im2col(&tmA, a_dst + j * (BK * 128), full_bar(stage), cb * 32, w0, h0, img,
+                              (uint16_t)ky, (uint16_t)kx);
+            }
           } else if (!A_MN) {
             tma_load_2d(&tmA, a_dst, full_bar(stage), kc, mt * BM);
           } else {
@@ -488,7 +506,14 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
         uint32_t r[16];
         tmem_ld16(t_row + (uint32_t)c0, r);
         tmem_wait_ld();
-        if (row < p.M) {
+        if (p.transpose_c && row < p.M) {
+          // C^T: for each column the warp's 32 lanes (consecutive rows) write 128 contiguous bytes
+          float v[16];
+          epi_chunk<16>(mode, v, r, p, row, col0);
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (col0 + j < p.N) p.C[(long long)(col0 + j) * p.ldc + row] = v[j];
+        } else if (row < p.M) {
           if (p.vec_ok && col0 + 16 <= p.N && mode != OMNI_EPI_ACCUM && mode != OMNI_EPI_MASK_AUX) {
             float v[16];
             epi_chunk<16>(mode, v, r, p, row, col0);
@@ -565,8 +590,12 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
     const int row = (int)(idx / N), col = (int)(idx - (idx / N) * N);
     float acc = 0.f;
     for (int s = 0; s < S; ++s) acc += ws[(long long)s * MN + idx];
-    float* Crow = p.C + (long long)row * p.ldc;
-    Crow[col] = epi_apply(p.epilogue, acc, p, row, col, Crow);
+    if (p.transpose_c) {
+      p.C[(long long)col * p.ldc + row] = acc;
+    } else {
+      float* Crow = p.C + (long long)row * p.ldc;
+      Crow[col] = epi_apply(p.epilogue, acc, p, row, col, Crow);
+    }
   }
 }
 
@@ -765,6 +794,7 @@ int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, lon
   CUtensorMap ta, tb;
   int rc;
   if (IM2COL == 1) rc = make_tmap_im2col(&ta, *cg, BM, false);
+  else if (IM2COL == 3) rc = make_tmap_im2col(&ta, *cg, BK, true);
   else rc = A_MN ? make_tmap(&ta, A, p.M, p.K, lda, 32, BK, true)
                  : make_tmap(&ta, A, p.K, p.M, lda, 32, BM, false);
   if (rc) return rc;
@@ -857,6 +887,10 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
     p.use_tma_store = p.vec_ok && epilogue != OMNI_EPI_ACCUM;
   }
   if (getenv("OMNI_NO_TMA_STORE")) p.use_tma_store = 0;
+  if (im2col == 3) {
+    p.transpose_c = pl.splits > 1 ? 0 : 1;  // partials are natural; the reduce transposes
+    if (p.transpose_c) p.use_tma_store = 0;
+  }
   int rc;
   const bool s3 = precision == OMNI_PREC_3XTF32;
   if (im2col == 1)
@@ -865,6 +899,9 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
   else if (im2col == 2)
     rc = s3 ? dispatch_bn<true, true, true, 2>(pl, A, lda, B, ldb, p, st, cg)
             : dispatch_bn<true, true, false, 2>(pl, A, lda, B, ldb, p, st, cg);
+  else if (im2col == 3)
+    rc = s3 ? dispatch_bn<true, true, true, 3>(pl, A, lda, B, ldb, p, st, cg)
+            : dispatch_bn<true, true, false, 3>(pl, A, lda, B, ldb, p, st, cg);
   else
     rc = s3 ? dispatch_major<true>(pl, a_mn, b_mn ? 1 : 0, A, lda, B, ldb, p, st)
             : dispatch_major<false>(pl, a_mn, b_mn ? 1 : 0, A, lda, B, ldb, p, st);
@@ -873,6 +910,7 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
     Params q = p;
     q.C = C;
     q.ldc = ldc;
+    q.transpose_c = (im2col == 3);
     splitk_reduce_kernel<<<omni::grid_for((long long)M * N, 256), 256, 0, st>>>(workspace,
                                                                               pl.splits, M, N, q);
     rc = omni::check_launch("splitk_reduce");
@@ -973,6 +1011,7 @@ long long omni_conv_implicit_plan(int precision, int op, int b, int n, int c, in
                                   int pad, int d_out) {
   int M, N, K, m;
   if (conv_shape(op, b, n, c, k, stride, pad, d_out, &M, &N, &K, &m)) return -1;
+  if (op == OMNI_CONV_WGRAD) return omni_gemm_plan(precision, N, M, K, 0, 0, nullptr, nullptr);
   return omni_gemm_plan(precision, M, N, K, 0, 0, nullptr, nullptr);
 }
 
@@ -999,9 +1038,13 @@ int omni_conv_implicit_f32(int precision, int op, const float* X, int b, int n, 
   if (op == OMNI_CONV_FPROP)   // A = im2col(X) (K-major), B = G weights (d_out x ldg, K-major)
     return gemm::run_gemm(precision, M, N, K, nullptr, 0, 0, G, ldg, 0, Y, ldy, epilogue, bias, aux,
                           ld_aux, workspace, ws_bytes, st, &cg, 1);
-  // WGRAD: A = G = dY (pixels x ldg, MN-major), B = im2col(X) (MN-major)
-  return gemm::run_gemm(precision, M, N, K, G, ldg, 1, nullptr, 0, 1, Y, ldy, epilogue, bias, aux,
-                        ld_aux, workspace, ws_bytes, st, &cg, 2);
+  // WGRAD: computed as C^T = im2col(X)^T dY with im2col as the MN-major A
+  // operand (128 (tap, ch) rows = 128 im2col pixel-rows per stage, half of what
+  // the B-side form needs) and dY (pixels x ldg) as the MN-major B operand;
+  // the epilogue stores C^T, i.e. Y[o*ldy + (tap, ch)].
+  OMNI_REQUIRE(epilogue == OMNI_EPI_STORE, "conv wgrad supports the plain store epilogue only");
+  return gemm::run_gemm(precision, N, M, K, nullptr, 0, 1, G, ldg, 1, Y, ldy, epilogue, bias, aux,
+                        ld_aux, workspace, ws_bytes, st, &cg, 3);
 }
 
 }  // extern "C"
