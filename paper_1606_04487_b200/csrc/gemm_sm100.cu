@@ -55,10 +55,10 @@ struct Params {
   int transpose_c;  // store C^T: C[j*ldc + i] (weight gradient with im2col as the A operand)
 };
 
-template <int BN, bool SPLIT3>
+template <int BN, bool SPLIT3, int BKT = BK>
 struct Layout {
-  static constexpr int A_BYTES = BM * BK * 4;
-  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int A_BYTES = BM * BKT * 4;
+  static constexpr int B_BYTES = BN * BKT * 4;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGE_ALL = SPLIT3 ? 2 * STAGE : STAGE;
   static constexpr int STG_BYTES = 4 * 2 * 32 * 32 * 4;  // 4 epilogue warps x 2 x (32x32 fp32)
@@ -191,9 +191,9 @@ __device__ __forceinline__ void tmem_wait_ld() {
 //            TMA mode 128B_ATOM_32B): 128 B along MN per K row; MN atoms of 32
 //            elements are a whole BK-row chunk apart (LBO = 32 rows * 128 B),
 //            4-row K groups 512 B apart (SBO).
-template <bool MN>
+template <bool MN, int BKT = BK>
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
-  const uint64_t lbo = MN ? (uint64_t)((BK * 128) >> 4) : 1ull;
+  const uint64_t lbo = MN ? (uint64_t)((BKT * 128) >> 4) : 1ull;
   const uint64_t sbo = MN ? (512 >> 4) : (1024 >> 4);
   const uint64_t layout = MN ? 1ull : 2ull;
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | (lbo << 16) | (sbo << 32) | (1ull << 46) |
@@ -264,12 +264,15 @@ __device__ __forceinline__ void epi_chunk(int mode, float (&v)[N], const uint32_
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, bool SPLIT3, int IM2COL>
-__global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
+template <int BN, bool A_MN, bool B_MN, bool SPLIT3, int IM2COL, int BKT>
+__global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const Params p) {
-  using L = Layout<BN, SPLIT3>;
+  // K-major operands hold exactly one 128-byte swizzle row (32 fp32) per stage;
+  // deeper stages are for MN-major operands only.
+  static_assert(BKT == BK || (A_MN && B_MN), "BKT > 32 needs MN-major operands");
+  using L = Layout<BN, SPLIT3, BKT>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
@@ -337,7 +340,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
           mbar_expect_tx(full_bar(stage), (uint32_t)L::STAGE);
           const uint32_t a_dst = sbase + stage * L::STAGE_ALL;
           const uint32_t b_dst = a_dst + L::A_BYTES;
-          const int kc = kt * BK;
+          const int kc = kt * BKT;
           if (IM2COL == 1) {
             // K index = (tap, channel): tap-major, 32-channel blocks
             const int cb = kt % p.conv_cblocks, tap = kt / p.conv_cblocks;
@@ -358,7 +361,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
               const int cb = blk - tap * p.conv_cblocks;
               if (tap >= taps) tap = taps - 1;  // rows past M: any valid load, discarded
               const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
-              tma_load_im2col(&tmA, a_dst + j * (BK * 128), full_bar(stage), cb * 32, w0, h0, img,
+              tma_load_im2col(&tmA, a_dst + j * (BKT * 128), full_bar(stage), cb * 32, w0, h0, img,
                               (uint16_t)ky, (uint16_t)kx);
             }
           } else if (!A_MN) {
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
           } else {
 #pragma unroll
             for (int j = 0; j < BM / 32; ++j)
-              tma_load_2d(&tmA, a_dst + j * (BK * 128), full_bar(stage), mt * BM + 32 * j, kc);
+              tma_load_2d(&tmA, a_dst + j * (BKT * 128), full_bar(stage), mt * BM + 32 * j, kc);
           }
           if (IM2COL == 2) {
             // B(j = (tap, ch), r = pixel): BK output pixels x 32 channels per chunk
@@ -382,7 +385,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
               const int cb = blk - tap * p.conv_cblocks;
               if (tap >= taps) tap = taps - 1;  // columns past N: any valid load, discarded
               const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
-              tma_load_im2col(&tmB, b_dst + j * (BK * 128), full_bar(stage), cb * 32, w0, h0, img,
+              tma_load_im2col(&tmB, b_dst + j * (BKT * 128), full_bar(stage), cb * 32, w0, h0, img,
                               (uint16_t)ky, (uint16_t)kx);
             }
           } else if (!B_MN) {
@@ -390,7 +393,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
           } else {
 #pragma unroll
             for (int j = 0; j < BN / 32; ++j)
-              tma_load_2d(&tmB, b_dst + j * (BK * 128), full_bar(stage), nt * BN + 32 * j, kc);
+              tma_load_2d(&tmB, b_dst + j * (BKT * 128), full_bar(stage), nt * BN + 32 * j, kc);
           }
           if (++stage == L::STAGES) {
             stage = 0;
@@ -421,15 +424,15 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3>::THREADS, 1)
           const uint32_t a_addr = sbase + stage * L::STAGE_ALL;
           const uint32_t b_addr = a_addr + L::A_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
+          for (int kk = 0; kk < BKT / 8; ++kk) {
             const uint32_t a_off = A_MN ? kk * 1024u : kk * 32u;
             const uint32_t b_off = B_MN ? kk * 1024u : kk * 32u;
-            const uint64_t ad = smem_desc<A_MN>(a_addr + a_off);
-            const uint64_t bd = smem_desc<B_MN>(b_addr + b_off);
+            const uint64_t ad = smem_desc<A_MN, BKT>(a_addr + a_off);
+            const uint64_t bd = smem_desc<B_MN, BKT>(b_addr + b_off);
             tc_mma_tf32(d_tmem, ad, bd, idesc, (kt > kt0 || kk > 0) ? 1u : 0u);
             if (SPLIT3) {
-              const uint64_t ad_lo = smem_desc<A_MN>(a_addr + L::STAGE + a_off);
-              const uint64_t bd_lo = smem_desc<B_MN>(b_addr + L::STAGE + b_off);
+              const uint64_t ad_lo = smem_desc<A_MN, BKT>(a_addr + L::STAGE + a_off);
+              const uint64_t bd_lo = smem_desc<B_MN, BKT>(b_addr + L::STAGE + b_off);
               tc_mma_tf32(d_tmem, ad_lo, bd, idesc, 1u);
               tc_mma_tf32(d_tmem, ad, bd_lo, idesc, 1u);
             }
@@ -696,7 +699,7 @@ struct Plan {
 
 constexpr int kBNs[] = {32, 64, 96, 128, 192, 256};
 
-Plan make_plan(int M, int N, int K, int sms) {
+Plan make_plan(int M, int N, int K, int sms, int bkt = BK) {
   Plan pl{};
   if (N <= 256) {
     for (int b : kBNs)
@@ -729,7 +732,7 @@ Plan make_plan(int M, int N, int K, int sms) {
   }
   pl.m_tiles = (int)omni::ceil_div(M, BM);
   pl.n_tiles = (int)omni::ceil_div(N, pl.bn);
-  pl.k_tiles = (int)omni::ceil_div(K, BK);
+  pl.k_tiles = (int)omni::ceil_div(K, bkt);
   const long long tiles = (long long)pl.m_tiles * pl.n_tiles;
   int splits = 1;
   if (tiles < sms && pl.k_tiles >= 8) {
@@ -787,19 +790,19 @@ int make_tmap_im2col(CUtensorMap* map, const ConvGeom& g, int pixels, bool mn_ma
   return OMNI_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool SPLIT3, int IM2COL>
+template <int BN, bool A_MN, bool B_MN, bool SPLIT3, int IM2COL, int BKT = BK>
 int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, long long ldb,
               const Params& p, cudaStream_t st, const ConvGeom* cg) {
-  using L = Layout<BN, SPLIT3>;
+  using L = Layout<BN, SPLIT3, BKT>;
   CUtensorMap ta, tb;
   int rc;
   if (IM2COL == 1) rc = make_tmap_im2col(&ta, *cg, BM, false);
-  else if (IM2COL == 3) rc = make_tmap_im2col(&ta, *cg, BK, true);
-  else rc = A_MN ? make_tmap(&ta, A, p.M, p.K, lda, 32, BK, true)
+  else if (IM2COL == 3) rc = make_tmap_im2col(&ta, *cg, BKT, true);
+  else rc = A_MN ? make_tmap(&ta, A, p.M, p.K, lda, 32, BKT, true)
                  : make_tmap(&ta, A, p.K, p.M, lda, 32, BM, false);
   if (rc) return rc;
-  if (IM2COL == 2) rc = make_tmap_im2col(&tb, *cg, BK, true);
-  else rc = B_MN ? make_tmap(&tb, B, p.N, p.K, ldb, 32, BK, true)
+  if (IM2COL == 2) rc = make_tmap_im2col(&tb, *cg, BKT, true);
+  else rc = B_MN ? make_tmap(&tb, B, p.N, p.K, ldb, 32, BKT, true)
                  : make_tmap(&tb, B, p.K, p.N, ldb, 32, BN, false);
   if (rc) return rc;
   CUtensorMap tc;
@@ -808,22 +811,22 @@ int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, lon
     rc = make_tmap_c(&tc, p.C, p.N, p.M, p.ldc, p.splits, p.split_stride);
     if (rc) return rc;
   }
-  auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT3, IM2COL>;
+  auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT3, IM2COL, BKT>;
   OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
   kern<<<pl.grid, L::THREADS, L::BYTES, st>>>(ta, tb, tc, p);
   return omni::check_launch("gemm_tf32");
 }
 
-template <bool A_MN, bool B_MN, bool SPLIT3, int IM2COL>
+template <bool A_MN, bool B_MN, bool SPLIT3, int IM2COL, int BKT = BK>
 int dispatch_bn(const Plan& pl, const float* A, long long lda, const float* B, long long ldb,
                 const Params& p, cudaStream_t st, const ConvGeom* cg = nullptr) {
   switch (pl.bn) {
-    case 32: return launch_tc<32, A_MN, B_MN, SPLIT3, IM2COL>(pl, A, lda, B, ldb, p, st, cg);
-    case 64: return launch_tc<64, A_MN, B_MN, SPLIT3, IM2COL>(pl, A, lda, B, ldb, p, st, cg);
-    case 96: return launch_tc<96, A_MN, B_MN, SPLIT3, IM2COL>(pl, A, lda, B, ldb, p, st, cg);
-    case 128: return launch_tc<128, A_MN, B_MN, SPLIT3, IM2COL>(pl, A, lda, B, ldb, p, st, cg);
-    case 192: return launch_tc<192, A_MN, B_MN, SPLIT3, IM2COL>(pl, A, lda, B, ldb, p, st, cg);
-    case 256: return launch_tc<256, A_MN, B_MN, SPLIT3, IM2COL>(pl, A, lda, B, ldb, p, st, cg);
+    case 32: return launch_tc<32, A_MN, B_MN, SPLIT3, IM2COL, BKT>(pl, A, lda, B, ldb, p, st, cg);
+    case 64: return launch_tc<64, A_MN, B_MN, SPLIT3, IM2COL, BKT>(pl, A, lda, B, ldb, p, st, cg);
+    case 96: return launch_tc<96, A_MN, B_MN, SPLIT3, IM2COL, BKT>(pl, A, lda, B, ldb, p, st, cg);
+    case 128: return launch_tc<128, A_MN, B_MN, SPLIT3, IM2COL, BKT>(pl, A, lda, B, ldb, p, st, cg);
+    case 192: return launch_tc<192, A_MN, B_MN, SPLIT3, IM2COL, BKT>(pl, A, lda, B, ldb, p, st, cg);
+    case 256: return launch_tc<256, A_MN, B_MN, SPLIT3, IM2COL, BKT>(pl, A, lda, B, ldb, p, st, cg);
   }
   omni::set_error("gemm: no kernel for BN=%d", pl.bn);
   return OMNI_EUNSUPPORTED;
@@ -854,7 +857,10 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
   p.ld_aux = ld_aux;
   int dev = 0;
   cudaGetDevice(&dev);
-  const Plan pl = make_plan(M, N, K, omni::sm_count_cached(dev));
+  // The implicit weight gradient (im2col A, both operands MN-major) runs 64-deep
+  // K stages in TF32 mode: half the TMA ops per byte, 64-pixel im2col boxes.
+  const int bkt = (im2col == 3 && precision == OMNI_PREC_TF32) ? 64 : BK;
+  const Plan pl = make_plan(M, N, K, omni::sm_count_cached(dev), bkt);
   p.m_tiles = pl.m_tiles;
   p.n_tiles = pl.n_tiles;
   p.k_tiles = pl.k_tiles;
@@ -896,12 +902,9 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
   if (im2col == 1)
     rc = s3 ? dispatch_bn<false, false, true, 1>(pl, A, lda, B, ldb, p, st, cg)
             : dispatch_bn<false, false, false, 1>(pl, A, lda, B, ldb, p, st, cg);
-  else if (im2col == 2)
-    rc = s3 ? dispatch_bn<true, true, true, 2>(pl, A, lda, B, ldb, p, st, cg)
-            : dispatch_bn<true, true, false, 2>(pl, A, lda, B, ldb, p, st, cg);
   else if (im2col == 3)
     rc = s3 ? dispatch_bn<true, true, true, 3>(pl, A, lda, B, ldb, p, st, cg)
-            : dispatch_bn<true, true, false, 3>(pl, A, lda, B, ldb, p, st, cg);
+            : dispatch_bn<true, true, false, 3, 64>(pl, A, lda, B, ldb, p, st, cg);
   else
     rc = s3 ? dispatch_major<true>(pl, a_mn, b_mn ? 1 : 0, A, lda, B, ldb, p, st)
             : dispatch_major<false>(pl, a_mn, b_mn ? 1 : 0, A, lda, B, ldb, p, st);
@@ -1011,7 +1014,13 @@ long long omni_conv_implicit_plan(int precision, int op, int b, int n, int c, in
                                   int pad, int d_out) {
   int M, N, K, m;
   if (conv_shape(op, b, n, c, k, stride, pad, d_out, &M, &N, &K, &m)) return -1;
-  if (op == OMNI_CONV_WGRAD) return omni_gemm_plan(precision, N, M, K, 0, 0, nullptr, nullptr);
+  if (op == OMNI_CONV_WGRAD) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int bkt = precision == OMNI_PREC_TF32 ? 64 : gemm::BK;
+    const gemm::Plan pl = gemm::make_plan(N, M, K, omni::sm_count_cached(dev), bkt);
+    return pl.splits > 1 ? (long long)pl.splits * M * N * 4 : 0;
+  }
   return omni_gemm_plan(precision, M, N, K, 0, 0, nullptr, nullptr);
 }
 
