@@ -135,21 +135,19 @@ __global__ void __launch_bounds__(kThreads) lower_nhwc_table_kernel(
     const int x = rem / m, y = rem - (rem / m) * m;
     const int ix0 = x * s - p, iy0 = y * s - p;
     const float* Ximg = X + (long long)img * n * n * cs;
-    float4* out = reinterpret_cast<float4*>(Dhat + (long long)row * ld);
-    for (int q = lane; q < (ld >> 2); q += 32) {
-      float v[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int e = col_tab[4 * q + t];
-        float val = e == -2 ? 1.f : 0.f;
-        if (e >= 0) {
-          const int ix = ix0 + (e >> 24), iy = iy0 + ((e >> 16) & 0xff);
-          if ((unsigned)ix < (unsigned)n && (unsigned)iy < (unsigned)n)
-            val = __ldg(Ximg + ((long long)ix * n + iy) * cs + (e & 0xffff));
-        }
-        v[t] = val;
+    float* out = Dhat + (long long)row * ld;
+    // lane j writes column j: one coalesced 128-byte store per warp instruction;
+    // consecutive columns of a tap run read consecutive input addresses
+#pragma unroll 4
+    for (int j = lane; j < ld; j += 32) {
+      const int e = col_tab[j];
+      float val = e == -2 ? 1.f : 0.f;
+      if (e >= 0) {
+        const int ix = ix0 + (e >> 24), iy = iy0 + ((e >> 16) & 0xff);
+        if ((unsigned)ix < (unsigned)n && (unsigned)iy < (unsigned)n)
+          val = __ldg(Ximg + ((long long)ix * n + iy) * cs + (e & 0xffff));
       }
-      out[q] = make_float4(v[0], v[1], v[2], v[3]);
+      out[j] = val;
     }
   }
 }

@@ -107,6 +107,11 @@ class DeviceSession:
         self.t = state.t
         self.engine = problem.engine(hp.b)
         self.pg = process_group
+        self._staged: dict[int, tuple] = {}   # id(HostBatch) -> (slot, ready event)
+        self._slots = None
+        self._slot_free = [None, None]
+        self._next_slot = 0
+        self._copy_stream = None
         self.world = 1
         if process_group is not None:
             import torch.distributed as dist
@@ -123,11 +128,50 @@ class DeviceSession:
 
         return hook
 
+    def prefetch(self, batch: "HostBatch") -> None:
+        """Start the host->device copy of a future step's batch on a side stream
+        (double-buffered), so it overlaps the current step's compute."""
+        if not isinstance(batch, HostBatch):
+            raise ValueError("prefetch takes a HostBatch")
+        eng = self.engine
+        if self._slots is None:
+            self._copy_stream = torch.cuda.Stream(device=self.problem.device)
+            self._slots = [(torch.empty_like(eng.input.value), torch.empty_like(eng.labels))
+                           for _ in range(2)]
+        slot = self._next_slot
+        self._next_slot ^= 1
+        X, y = self._slots[slot]
+        b = batch.size
+        with torch.cuda.stream(self._copy_stream):
+            if self._slot_free[slot] is not None:       # the step that read this slot is done
+                self._copy_stream.wait_event(self._slot_free[slot])
+            X[:b].copy_(batch.X, non_blocking=True)
+            y[:b].copy_(batch.y, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(self._copy_stream)
+        self._staged[id(batch)] = (slot, ready)
+
+    def _load(self, batch) -> int:
+        staged = self._staged.pop(id(batch), None) if isinstance(batch, HostBatch) else None
+        if staged is None:
+            return self.problem.load_batch(self.engine, batch)
+        slot, ready = staged
+        cur = torch.cuda.current_stream()
+        cur.wait_event(ready)
+        X, y = self._slots[slot]
+        eng = self.engine
+        self._own = (eng.input.value, eng.labels)
+        eng.input.value, eng.labels = X, y          # consume the staged buffers in place
+        free = torch.cuda.Event()
+        self._pending_free = (slot, free)
+        return batch.size
+
     def step(self, batch: Any, w_read: torch.Tensor | None = None) -> None:
         """V = mu V - eta (grad(w_read) + lam w_read); W += V, with w_read = W when
         synchronous (sgd.py:104-112)."""
         wr = self.W if w_read is None else w_read
-        b = self.problem.load_batch(self.engine, batch)
+        self._pending_free = None
+        b = self._load(batch)
         hp = self.hp
         if self.world > 1:
             works = []
@@ -140,6 +184,11 @@ class DeviceSession:
         else:
             self.engine.loss_and_grad(wr, b)
             K.sgd_momentum(self.W, self.V, self.engine.grad, wr, hp.eta, hp.mu, hp.lam)
+        if self._pending_free is not None:
+            slot, free = self._pending_free
+            free.record(torch.cuda.current_stream())
+            self._slot_free[slot] = free
+            self.engine.input.value, self.engine.labels = self._own   # launches already hold the pointers
         self.t += 1
 
     def full_loss(self) -> float:
