@@ -3,6 +3,7 @@
 // the batch gather (K9).  Every reduction is a fixed-order gather or a
 // two-pass tree so results are bit-reproducible run to run (no atomics).
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -168,6 +169,91 @@ __global__ void __launch_bounds__(kThreads) pool_bwd_kernel(
   }
 }
 
+// Stride-2 backward: one thread per 2x2 input block x 4 channels.  The four
+// pixels of an aligned 2x2 block are covered by the same <= (k/2+1)^2 windows,
+// so each window's dY and argmax are read once per block instead of once per
+// pixel.  Per pixel the windows are still summed in ascending (oy, ox) order:
+// bit-identical to pool_bwd_kernel.
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) pool_bwd_s2_kernel(
+    const float* __restrict__ dY, int b, int h, int w, int c, int cs_in, int k, int p, int oh,
+    int ow, int cs_out, const int32_t* __restrict__ argmax, const float* __restrict__ X,
+    int relu_mask_x, float* __restrict__ dX) {
+  const int cv = c / 4;
+  const int bh = (h + 1) / 2, bw = (w + 1) / 2;
+  const int total = b * bh * bw * cv;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int blk = idx / cv;
+    const int ch = (idx - blk * cv) * 4;
+    const int img = blk / (bh * bw);
+    const int r = blk - img * bh * bw;
+    const int by = r / bw, bx = r - (r / bw) * bw;
+    const int y0 = 2 * by, x0 = 2 * bx;
+    const int y1 = min(y0 + 1, h - 1), x1 = min(x0 + 1, w - 1);
+    const int oy0 = (y0 + p < k) ? 0 : (y0 + p - k) / 2 + 1;
+    const int oy1 = min((y1 + p) / 2 + 1, oh);
+    const int ox0 = (x0 + p < k) ? 0 : (x0 + p - k) / 2 + 1;
+    const int ox1 = min((x1 + p) / 2 + 1, ow);
+    float acc[2][2][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[a][e][v] = 0.f;
+    const int obase = img * oh * ow;
+    for (int oy = oy0; oy < oy1; ++oy)
+      for (int ox = ox0; ox < ox1; ++ox) {
+        const int o = obase + oy * ow + ox;
+        const float4 g = __ldg(reinterpret_cast<const float4*>(dY + (long long)o * cs_out + ch));
+        const float gv[4] = {g.x, g.y, g.z, g.w};
+        if (MODE == 0) {
+          const int4 t = __ldg(reinterpret_cast<const int4*>(argmax + (long long)o * c + ch));
+          const int av[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int me = (y0 + a) * w + (x0 + e);
+#pragma unroll
+              for (int v = 0; v < 4; ++v)
+                if (av[v] == me) acc[a][e][v] += gv[v];
+            }
+        } else {
+          const int hs = oy * 2 - p, ws = ox * 2 - p;
+          const int he = min(hs + k, h + p), we = min(ws + k, w + p);
+          const float inv = 1.f / (float)((he - hs) * (we - ws));
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int yy = y0 + a, xx = x0 + e;
+              if (yy >= hs && yy < hs + k && xx >= ws && xx < ws + k)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[a][e][v] += gv[v] * inv;
+            }
+        }
+      }
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int yy = y0 + a, xx = x0 + e;
+        if (yy >= h || xx >= w) continue;
+        const long long pix = (long long)img * h * w + (long long)yy * w + xx;
+        float4 out = make_float4(acc[a][e][0], acc[a][e][1], acc[a][e][2], acc[a][e][3]);
+        if (relu_mask_x) {
+          const float4 m = __ldg(reinterpret_cast<const float4*>(X + pix * cs_in + ch));
+          out.x = m.x > 0.f ? out.x : 0.f;
+          out.y = m.y > 0.f ? out.y : 0.f;
+          out.z = m.z > 0.f ? out.z : 0.f;
+          out.w = m.w > 0.f ? out.w : 0.f;
+        }
+        *reinterpret_cast<float4*>(dX + pix * cs_in + ch) = out;
+      }
+  }
+}
+
 // Softmax cross-entropy: one CTA of 32 warps; warp w owns rows w, w+32, ...
 // Row losses are summed per warp in row order, then across warps in warp
 // order: a fixed reduction tree, so the loss is bit-reproducible.
@@ -177,6 +263,42 @@ __global__ void __launch_bounds__(1024) softmax_xent_kernel(
   __shared__ float warp_loss[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float my_loss = 0.f;
+  if (C <= 1024) {
+    // each lane keeps its <= 32 logits in registers: one batch of independent
+    // loads per row instead of three dependent sweeps over memory
+    for (int row = warp; row < b; row += 32) {
+      const float* z = Z + (long long)row * ld;
+      float v[32];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int j = lane + 32 * i;
+        v[i] = j < C ? __ldg(z + j) : -INFINITY;
+        mx = fmaxf(mx, v[i]);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      float sum = 0.f;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        v[i] = (lane + 32 * i) < C ? expf(v[i] - mx) : 0.f;
+        sum += v[i];
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const int label = y[row];
+      if (lane == 0) my_loss += (logf(sum) + mx) - z[label];
+      if (dZ) {
+        const float inv = 1.f / sum;
+        float* d = dZ + (long long)row * ldd;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int j = lane + 32 * i;
+          if (j < C) d[j] = (v[i] * inv - (j == label ? 1.f : 0.f)) * scale;
+        }
+      }
+    }
+  } else
   for (int row = warp; row < b; row += 32) {
     const float* z = Z + (long long)row * ld;
     float mx = -INFINITY;
@@ -246,13 +368,18 @@ __global__ void __launch_bounds__(256) bias_grad_pass1(const float* __restrict__
   }
 }
 
+// Pass 2: one warp per column; lane l sums partials l, l+32, ... then a fixed
+// xor-shuffle tree -- deterministic, and G loads in flight instead of a chain.
 __global__ void __launch_bounds__(256) bias_grad_pass2(const float* __restrict__ ws, int G, int N,
                                                        float* __restrict__ db) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int col = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (col >= N) return;
   float s = 0.f;
-  for (int g = 0; g < G; ++g) s += ws[(long long)g * N + col];
-  db[col] = s;
+  for (int g = lane; g < G; g += 32) s += ws[(long long)g * N + col];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) db[col] = s;
 }
 
 inline void bias_grad_geometry(int M, int* G, int* rpb) {
@@ -303,22 +430,23 @@ __global__ void __launch_bounds__(kThreads) sgd_kernel_scalar(float* W, float* V
   }
 }
 
+// One block-stride loop per gathered row: no per-element division.
 template <bool VEC4>
 __global__ void __launch_bounds__(kThreads) gather_rows_kernel(const float* __restrict__ src,
                                                                long long row_elems,
                                                                const int64_t* __restrict__ idx,
                                                                int nidx, float* __restrict__ dst) {
   const long long per = VEC4 ? row_elems / 4 : row_elems;
-  const long long total = per * nidx;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const long long i = t / per, j = t - (t / per) * per;
+  for (int i = blockIdx.y; i < nidx; i += gridDim.y) {
     const long long srow = idx[i];
-    if (VEC4)
-      reinterpret_cast<float4*>(dst)[i * per + j] =
-          reinterpret_cast<const float4*>(src)[srow * per + j];
-    else
-      dst[i * per + j] = src[srow * per + j];
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < per;
+         j += (long long)gridDim.x * blockDim.x) {
+      if (VEC4)
+        reinterpret_cast<float4*>(dst)[i * per + j] =
+            __ldg(reinterpret_cast<const float4*>(src) + srow * per + j);
+      else
+        dst[i * per + j] = __ldg(src + srow * per + j);
+    }
   }
 }
 
@@ -387,6 +515,17 @@ int omni_pool_bwd_nhwc_f32(int mode, const float* dY, int b, int h, int w, int c
   cudaStream_t st = omni::as_stream(stream);
   const bool v4 = c % 4 == 0 && cs_in % 4 == 0 && cs_out % 4 == 0 && aligned16(dY) && aligned16(dX) &&
                   (mode == 1 || aligned16(argmax)) && (!relu_mask_x || aligned16(X));
+  if (v4 && stride == 2 && !getenv("OMNI_POOL_BWD_PIXEL")) {
+    const long long blocks = (long long)b * ((h + 1) / 2) * ((w + 1) / 2) * (c / 4);
+    const int g2 = omni::grid_for(blocks, kThreads);
+    if (mode == 0)
+      pool_bwd_s2_kernel<0><<<g2, kThreads, 0, st>>>(dY, b, h, w, c, cs_in, k, pad, oh, ow, cs_out,
+                                                     argmax, X, relu_mask_x, dX);
+    else
+      pool_bwd_s2_kernel<1><<<g2, kThreads, 0, st>>>(dY, b, h, w, c, cs_in, k, pad, oh, ow, cs_out,
+                                                     argmax, X, relu_mask_x, dX);
+    return omni::check_launch("pool_bwd_s2");
+  }
   const int grid = omni::grid_for(v4 ? work / 4 : work, kThreads);
 #define OMNI_POOL_BWD(M, V)                                                                     \
   pool_bwd_kernel<M, V><<<grid, kThreads, 0, st>>>(dY, b, h, w, c, cs_in, k, stride, pad, oh, ow, \
@@ -437,7 +576,7 @@ int omni_bias_grad_f32(const float* dY, long long ld, int M, int N, float* db, f
   bias_grad_pass1<<<dim3(G, (N + 31) / 32), 256, 0, st>>>(dY, ld, M, N, rpb, ws);
   int rc = omni::check_launch("bias_grad_pass1");
   if (rc) return rc;
-  bias_grad_pass2<<<(N + 255) / 256, 256, 0, st>>>(ws, G, N, db);
+  bias_grad_pass2<<<(N * 32 + 255) / 256, 256, 0, st>>>(ws, G, N, db);
   return omni::check_launch("bias_grad_pass2");
 }
 
@@ -461,13 +600,13 @@ int omni_gather_rows_f32(const float* src, long long row_elems, const int64_t* i
   if (nidx == 0) return OMNI_OK;
   cudaStream_t st = omni::as_stream(stream);
   const bool v4 = (row_elems % 4 == 0) && aligned16(src) && aligned16(dst);
-  const long long work = (v4 ? row_elems / 4 : row_elems) * nidx;
+  const long long per = v4 ? row_elems / 4 : row_elems;
+  const int gx = (int)omni::ceil_div(per, kThreads * 4) > 0 ? (int)omni::ceil_div(per, kThreads * 4) : 1;
+  const dim3 grid(gx < 65535 ? gx : 65535, nidx < 65535 ? nidx : 65535);
   if (v4)
-    gather_rows_kernel<true><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(src, row_elems,
-                                                                                 idx, nidx, dst);
+    gather_rows_kernel<true><<<grid, kThreads, 0, st>>>(src, row_elems, idx, nidx, dst);
   else
-    gather_rows_kernel<false><<<omni::grid_for(work, kThreads), kThreads, 0, st>>>(src, row_elems,
-                                                                                  idx, nidx, dst);
+    gather_rows_kernel<false><<<grid, kThreads, 0, st>>>(src, row_elems, idx, nidx, dst);
   return omni::check_launch("gather_rows");
 }
 
