@@ -107,23 +107,30 @@ __global__ void __launch_bounds__(kThreads) lower_nhwc_rows_kernel(
   }
 }
 
-// Scalar-channel lowering (c % 4 != 0, e.g. the 3-channel first layer): each
-// block builds a shared table col -> (kx, ky, ch) once, then one warp per row
-// writes float4 runs of the row with no divisions in the inner loop.
+// Scalar-channel lowering (c % 4 != 0, e.g. the 3-channel first layer).  Each
+// block builds two shared tables once: col -> offset of the source element
+// relative to the window origin ((kx*n + ky)*cs + ch), and col -> (kx, ky).
+// Rows whose window lies inside the image (all rows when pad == 0) take the
+// fast path -- one table load, one global load, one store per element, lane
+// j on column j for coalesced 128-byte stores; border rows check bounds.
 __global__ void __launch_bounds__(kThreads) lower_nhwc_table_kernel(
     const float* __restrict__ X, int n, int c, int cs, int k, int s, int p, int m, int rows,
     int K, int ld, int ones_col, float* __restrict__ Dhat) {
-  extern __shared__ int col_tab[];
+  extern __shared__ int tab[];
+  int* off = tab;       // [ld]
+  int* kxy = tab + ld;  // [ld]: (kx << 16) | ky, or -1 (zero) / -2 (ones column)
   for (int j = threadIdx.x; j < ld; j += blockDim.x) {
-    int e = -1;
+    int o = 0, e = -1;
     if (j < K) {
       const int tap = j / c, ch = j - (j / c) * c;
       const int kx = tap / k, ky = tap - (tap / k) * k;
-      e = (kx << 24) | (ky << 16) | ch;
+      o = (kx * n + ky) * cs + ch;
+      e = (kx << 16) | ky;
     } else if (ones_col && j == K) {
       e = -2;
     }
-    col_tab[j] = e;
+    off[j] = o;
+    kxy[j] = e;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -134,20 +141,26 @@ __global__ void __launch_bounds__(kThreads) lower_nhwc_table_kernel(
     const int rem = row - img * mm;
     const int x = rem / m, y = rem - (rem / m) * m;
     const int ix0 = x * s - p, iy0 = y * s - p;
-    const float* Ximg = X + (long long)img * n * n * cs;
     float* out = Dhat + (long long)row * ld;
-    // lane j writes column j: one coalesced 128-byte store per warp instruction;
-    // consecutive columns of a tap run read consecutive input addresses
+    if (ix0 >= 0 && iy0 >= 0 && ix0 + k <= n && iy0 + k <= n) {
+      const float* org = X + (((long long)img * n + ix0) * n + iy0) * cs;
 #pragma unroll 4
-    for (int j = lane; j < ld; j += 32) {
-      const int e = col_tab[j];
-      float val = e == -2 ? 1.f : 0.f;
-      if (e >= 0) {
-        const int ix = ix0 + (e >> 24), iy = iy0 + ((e >> 16) & 0xff);
-        if ((unsigned)ix < (unsigned)n && (unsigned)iy < (unsigned)n)
-          val = __ldg(Ximg + ((long long)ix * n + iy) * cs + (e & 0xffff));
+      for (int j = lane; j < ld; j += 32) {
+        const int e = kxy[j];
+        out[j] = e >= 0 ? __ldg(org + off[j]) : (e == -2 ? 1.f : 0.f);
       }
-      out[j] = val;
+    } else {
+      const float* Ximg = X + (long long)img * n * n * cs;
+      for (int j = lane; j < ld; j += 32) {
+        const int e = kxy[j];
+        float val = e == -2 ? 1.f : 0.f;
+        if (e >= 0) {
+          const int ix = ix0 + (e >> 16), iy = iy0 + (e & 0xffff);
+          if ((unsigned)ix < (unsigned)n && (unsigned)iy < (unsigned)n)
+            val = __ldg(Ximg + ((long long)ix * n + iy) * cs + (off[j] - ((e >> 16) * n + (e & 0xffff)) * cs));
+        }
+        out[j] = val;
+      }
     }
   }
 }
@@ -376,8 +389,12 @@ int omni_lower_nhwc_f32(const float* X, int b, int n, int c, int cs, int k, int 
   if (cs == c && c % 4 == 0 && ((uintptr_t)X % 16 == 0)) {
     lower_nhwc_rows_kernel<true, false><<<grid, kThreads, 0, st>>>(
         X, n, c, cs, k, stride, pad, m, (int)rows, K, (int)ld, ones_col, Dhat);
-  } else if (ld <= 16384) {
-    lower_nhwc_table_kernel<<<grid, kThreads, ld * sizeof(int), st>>>(
+  } else if (ld <= 8192) {
+    const int smem = 2 * (int)ld * (int)sizeof(int);
+    if (smem > 48 * 1024)
+      OMNI_CUDA_TRY(cudaFuncSetAttribute(lower_nhwc_table_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    lower_nhwc_table_kernel<<<grid, kThreads, smem, st>>>(
         X, n, c, cs, k, stride, pad, m, (int)rows, K, (int)ld, ones_col, Dhat);
   } else if (cs == c) {
     lower_nhwc_rows_kernel<false, false><<<grid, kThreads, 0, st>>>(
