@@ -200,6 +200,9 @@ class GpuNet:
             if op.kind == "conv" and not op.first_param_layer and not op.implicit:
                 dd = max(dd, self.b * op.m * op.m * op.ldK)
         self.gemm_ws = z(max(ws // 4, 4))
+        self.gemm_ws_side = z(max(ws // 4, 4))   # weight-gradient GEMMs run on a side stream
+        self._ws_active = self.gemm_ws
+        self.side_stream = torch.cuda.Stream(device=self.device)
         self.bias_ws = z(max(bws, 4))
         self.ddhat = z(max(dd, 4))
         self.graph = None
@@ -240,7 +243,7 @@ class GpuNet:
               aux=None, ld_aux=0, kind="gemm"):
         self._timed(M, N, Kd, kind, lambda: K.gemm(
             M, N, Kd, A, lda, a_mn, B, ldb, b_mn, C, ldc, precision=self.prec, epilogue=epi,
-            bias=bias, aux=aux, ld_aux=ld_aux, workspace=self.gemm_ws))
+            bias=bias, aux=aux, ld_aux=ld_aux, workspace=self._ws_active))
 
     def _conv(self, op_code, X, c, k, s, p, d, G, ldg, Y, ldy, epi=_abi.EPI_STORE, bias=None,
               aux=None, ld_aux=0):
@@ -252,7 +255,7 @@ class GpuNet:
             M, N, Kd = d, c * k * k, b * m * m
         self._timed(M, N, Kd, "conv", lambda: K.conv_implicit(
             op_code, X, c, k, s, p, d, G, ldg, Y, ldy, precision=self.prec, epilogue=epi,
-            bias=bias, aux=aux, ld_aux=ld_aux, workspace=self.gemm_ws))
+            bias=bias, aux=aux, ld_aux=ld_aux, workspace=self._ws_active))
 
     # ----------------------------------------------------------- staging --
     def stage_weights(self, W: torch.Tensor) -> None:
@@ -341,22 +344,44 @@ class GpuNet:
         gradient allreduce of finished layers with the rest of the backward."""
         b = self.b if b is None else int(b)
         G = self.grad
+        main = torch.cuda.current_stream(self.device)
+        side = self.side_stream
+        net = self
 
         def done(op):
             if on_grad is not None:
                 hi = op.boff + op.layer.d_out if op.boff >= 0 else op.woff + op.wsz
                 on_grad(op.woff, hi)
+
+        class wgrad_stream:
+            """Weight/bias gradients only feed the update, so they run on a side
+            stream (own split-K workspace) while the data-gradient chain continues
+            on the main stream; joined at the end of backward."""
+
+            def __enter__(self):
+                ev = torch.cuda.Event()
+                ev.record(main)
+                side.wait_event(ev)
+                self.ctx = torch.cuda.stream(side)
+                self.ctx.__enter__()
+                net._ws_active = net.gemm_ws_side
+
+            def __exit__(self, *exc):
+                net._ws_active = net.gemm_ws
+                return self.ctx.__exit__(*exc)
+
         for op in reversed(self.ops):
             L = op.layer
             if op.kind == "fc":
                 d = L.d_out
                 dZ = op.out.grad
-                # weight gradient straight into the flat (in, out) slice
-                self._gemm(op.f_in, d, b, op.flat.value, op.flat.cs, True, dZ, op.out.cs, True,
-                           G[op.woff:op.woff + op.wsz], d)
-                if op.boff >= 0:
-                    K.bias_grad(dZ, op.out.cs, b, d, G[op.boff:op.boff + d], self.bias_ws)
-                done(op)
+                with wgrad_stream():
+                    # weight gradient straight into the flat (in, out) slice
+                    self._gemm(op.f_in, d, b, op.flat.value, op.flat.cs, True, dZ, op.out.cs, True,
+                               G[op.woff:op.woff + op.wsz], d)
+                    if op.boff >= 0:
+                        K.bias_grad(dZ, op.out.cs, b, d, G[op.boff:op.boff + d], self.bias_ws)
+                    done(op)
                 if op.first_param_layer:
                     continue
                 if op.w_inplace:   # B(j=f, r=o) = W[f*d + o]: K-major, ld = d
@@ -386,13 +411,14 @@ class GpuNet:
                 Mr = b * op.m * op.m
                 dZ = op.out.grad
                 if op.implicit:
-                    self._conv(_abi.CONV_WGRAD, op.inp.value[:b], op.c_in, op.k, op.s, op.p, d, dZ,
-                               op.out.cs, op.dwstage, op.ldK)
-                    K.conv_weight_to_tap(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k, op.dwstage,
-                                         op.ldK, inverse=True)
-                    if op.boff >= 0:
-                        K.bias_grad(dZ, op.out.cs, Mr, d, G[op.boff:op.boff + d], self.bias_ws)
-                    done(op)
+                    with wgrad_stream():
+                        self._conv(_abi.CONV_WGRAD, op.inp.value[:b], op.c_in, op.k, op.s, op.p, d,
+                                   dZ, op.out.cs, op.dwstage, op.ldK)
+                        K.conv_weight_to_tap(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k,
+                                             op.dwstage, op.ldK, inverse=True)
+                        if op.boff >= 0:
+                            K.bias_grad(dZ, op.out.cs, Mr, d, G[op.boff:op.boff + d], self.bias_ws)
+                        done(op)
                     if op.first_param_layer:
                         continue
                     # dX = conv(dY, flipped kernel, pad k-1-p) with the ReLU mask of X fused
@@ -404,13 +430,14 @@ class GpuNet:
                         self._conv(_abi.CONV_FPROP, dZ[:b], d, op.k, 1, op.k - 1 - op.p, op.c_in,
                                    op.wflip, op.ldF, op.inp.grad, op.inp.cs)
                     continue
-                # weight (and, via the ones column, bias) gradient in one GEMM
-                self._gemm(d, op.Kf, Mr, dZ, op.out.cs, True, op.dhat, op.ldK, True, op.dwstage,
-                           op.ldK, kind="conv")
-                K.conv_weight_to_tap(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k, op.dwstage,
-                                     op.ldK, inverse=True,
-                                     bias=G[op.boff:op.boff + d] if op.boff >= 0 else None)
-                done(op)
+                with wgrad_stream():
+                    # weight (and, via the ones column, bias) gradient in one GEMM
+                    self._gemm(d, op.Kf, Mr, dZ, op.out.cs, True, op.dhat, op.ldK, True, op.dwstage,
+                               op.ldK, kind="conv")
+                    K.conv_weight_to_tap(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k, op.dwstage,
+                                         op.ldK, inverse=True,
+                                         bias=G[op.boff:op.boff + d] if op.boff >= 0 else None)
+                    done(op)
                 if op.first_param_layer:
                     continue
                 self._gemm(Mr, op.Kc, d, dZ, op.out.cs, False, op.wstage, op.ldK, True, self.ddhat,
@@ -430,6 +457,7 @@ class GpuNet:
                 n = b * op.out.grad[0].numel()
                 K.relu_bwd(op.out.grad.view(-1)[:n], op.out.value.view(-1)[:n],
                            op.inp.grad.view(-1)[:n])
+        main.wait_stream(side)
         return G
 
     # ------------------------------------------------------------- input --
