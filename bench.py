@@ -255,13 +255,14 @@ def run_ours(args):
 
     # ---- per-GEMM breakdown (one instrumented step, after the timed region):
     # CUDA events around every conv / FC GEMM launch (explicit or implicit).
-    eng.timer = []
+    # Serial chains here so every launch is timed alone (no stream overlap).
+    eng.timer, eng.overlap = [], False
     torch.cuda.synchronize()
     reps = 3
     for r in range(reps):
         step(total - 1)
     torch.cuda.synchronize()
-    records, eng.timer = eng.timer, None
+    records, eng.timer, eng.overlap = eng.timer, None, True
     per_step = len(records) // reps
     conv_ms = fc_ms = 0.0
     rows = []

@@ -207,6 +207,7 @@ class GpuNet:
         self.ddhat = z(max(dd, 4))
         self.graph = None
         self.timer = None   # list -> (M, N, K, kind, ev0, ev1) per GEMM launch
+        self.overlap = True  # False: weight gradients on the main stream (isolated kernel timing)
 
     # ------------------------------------------------------------ shapes --
     @staticmethod
@@ -362,7 +363,7 @@ class GpuNet:
                 ev = torch.cuda.Event()
                 ev.record(main)
                 side.wait_event(ev)
-                self.ctx = torch.cuda.stream(side)
+                self.ctx = torch.cuda.stream(side if net.overlap else main)
                 self.ctx.__enter__()
                 net._ws_active = net.gemm_ws_side
 
