@@ -278,6 +278,14 @@ def run_ours(args):
     achieved = conv_flops_step / (conv_ms * 1e-3) / 1e12 if conv_ms > 0 else 0.0
     peaks = measured_peaks()
     peak, peak_src = tf32_peak(peaks)
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "r01_traffic_summary.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            ts = json.load(f)
+        if ts.get("net") == args.net and ts.get("per_gpu_batch") == b and ts.get("precision") == args.precision:
+            traffic = ts["conv_gemm_dram_bytes_per_step"]
+            traffic_src = ("DRAM bytes (read+write) of the conv GEMM launches of one step, " + ts["source"])
     if args.profile_out and rank == 0:
         with open(args.profile_out, "w") as f:
             json.dump({"gemms_one_step": rows[:per_step], "conv_gemm_ms": conv_ms,
@@ -334,7 +342,10 @@ def run_ours(args):
                        "parallelism": f"dp{world}", "precision": args.precision,
                        "l2": "inputs larger than L2 (lowered matrices ~4.2 GiB per step)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "conv GEMMs (gemm_tf32_kernel)",
+                         "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per step",
+                         "traffic_source": traffic_src,
+                         "algorithmic": f"{net.conv_flops_per_image() / 1e9:.4f} GFLOP/img conv FW+BW x {b} img",
+                         "kernel": "conv GEMMs (gemm_tf32_kernel: implicit im2col + explicit layer 1)",
                          "peak_source": peak_src, "conv_gemm_ms_per_step": conv_ms,
                          "fc_gemm_ms_per_step": fc_ms,
                          "conv_gemm_share_of_step": conv_ms / (ms / args.steps)},
