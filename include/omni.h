@@ -171,6 +171,18 @@ int omni_conv_weight_to_tap_f32(float* W, int o, int c, int k, float* Wt, long l
  * Wf[ch*ld + (kx*k + ky)*o + oo] = W[oo, ch, k-1-kx, k-1-ky] (W is OIHW).     */
 int omni_conv_weight_flip_f32(const float* W, int o, int c, int k, float* Wf, long long ld,
                               void* stream);
+/* Space-to-depth with channel padding (first-layer implicit GEMM): X (b, n, n,
+ * pixel stride cs, c channels) -> Y (b, n2, n2, cp),
+ * Y[img, X, Y, (dx*s + dy)*c + ch] = X[img, s*X + dx, s*Y + dy, ch], zero outside
+ * the image and in channels >= s*s*c.  A stride-s k x k conv of X equals a
+ * stride-1 ceil(k/s) x ceil(k/s) conv of Y with the weights below.            */
+int omni_space_to_depth_f32(const float* X, int b, int n, int c, int cs, int s, float* Y, int n2,
+                            int cp, void* stream);
+/* Weights of that conv, tap-major rows Wt (o x ld, ld >= ceil(k/s)^2 * cp):
+ * Wt[o*ld + (kx2*k2 + ky2)*cp + (dx*s + dy)*c + ch] = W[o, ch, s*kx2+dx, s*ky2+dy]
+ * (0 past the kernel).  inverse=1 maps a gradient in that layout back to OIHW. */
+int omni_conv_weight_s2d_f32(float* W, int o, int c, int k, int s, int cp, float* Wt, long long ld,
+                             int inverse, void* stream);
 /* Batched 2-D transpose: dst[bi][j*ldd + i] = src[bi][i*lds + j], i < rows,
  * j < cols; batch strides in elements.  Used for NHWC <-> flattened CHW and
  * for FC weight staging.                                                     */

@@ -285,6 +285,84 @@ __global__ void __launch_bounds__(kThreads) weight_flip_kernel(
   }
 }
 
+// Space-to-depth with channel padding: X (b, n, n, cs) NHWC, c channels ->
+// Y (b, n2, n2, cp) with Y[img, X, Y, (dx*s + dy)*c + ch] = X[img, s*X+dx, s*Y+dy, ch]
+// (0 outside the image or for padded channels).  A stride-s k x k conv of X
+// is then a stride-1 ceil(k/s)^2 conv of Y with s*s*c (-> cp) channels, which
+// tiles the 32-channel TMA im2col boxes of the implicit GEMM.
+__global__ void __launch_bounds__(kThreads) space_to_depth_kernel(
+    const float* __restrict__ X, int b, int n, int c, int cs, int s, float* __restrict__ Y, int n2,
+    int cp) {
+  const int cv = cp / 4;
+  const long long total = (long long)b * n2 * n2 * cv;
+  const int sc = s * c;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long pix = idx / cv;
+    const int j0 = (int)(idx - pix * cv) * 4;
+    const int img = (int)(pix / ((long long)n2 * n2));
+    const int r = (int)(pix - (long long)img * n2 * n2);
+    const int X2 = r / n2, Y2 = r - (r / n2) * n2;
+    float v[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int j = j0 + t;
+      float val = 0.f;
+      if (j < s * sc) {
+        const int dx = j / sc, rem = j - (j / sc) * sc;
+        const int dy = rem / c, ch = rem - (rem / c) * c;
+        const int ix = s * X2 + dx, iy = s * Y2 + dy;
+        if (ix < n && iy < n) val = __ldg(X + (((long long)img * n + ix) * n + iy) * cs + ch);
+      }
+      v[t] = val;
+    }
+    *reinterpret_cast<float4*>(Y + pix * cp + j0) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+// Weights of the space-to-depth conv: Wt[o*ld + (kx2*k2 + ky2)*cp + (dx*s + dy)*c + ch]
+// = W[o, ch, s*kx2+dx, s*ky2+dy] (0 past the original kernel / padded channels).
+// inverse: read dWt, write the OIHW gradient (padded entries dropped).
+__global__ void __launch_bounds__(kThreads) weight_s2d_kernel(
+    float* __restrict__ W, int o, int c, int k, int s, int cp, float* __restrict__ Wt, long long ld,
+    int inverse) {
+  const int k2 = (k + s - 1) / s;
+  const int sc = s * c;
+  if (!inverse) {
+    const long long total = (long long)o * ld;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+      const int oo = (int)(idx / ld);
+      const int col = (int)(idx - (long long)oo * ld);
+      float v = 0.f;
+      if (col < k2 * k2 * cp) {
+        const int tap = col / cp, j = col - (col / cp) * cp;
+        if (j < s * sc) {
+          const int kx2 = tap / k2, ky2 = tap - (tap / k2) * k2;
+          const int dx = j / sc, rem = j - (j / sc) * sc;
+          const int dy = rem / c, ch = rem - (rem / c) * c;
+          const int kx = s * kx2 + dx, ky = s * ky2 + dy;
+          if (kx < k && ky < k) v = W[(((long long)oo * c + ch) * k + kx) * k + ky];
+        }
+      }
+      Wt[idx] = v;
+    }
+  } else {
+    const long long total = (long long)o * c * k * k;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+      long long r = idx;
+      const int ky = (int)(r % k); r /= k;
+      const int kx = (int)(r % k); r /= k;
+      const int ch = (int)(r % c); r /= c;
+      const int oo = (int)r;
+      const int tap = (kx / s) * k2 + (ky / s);
+      const int j = ((kx % s) * s + (ky % s)) * c + ch;
+      W[idx] = Wt[(long long)oo * ld + (long long)tap * cp + j];
+    }
+  }
+}
+
 // Batched tiled transpose through shared memory (32x33 tile: no bank conflicts).
 template <typename T>
 __global__ void __launch_bounds__(256) transpose_kernel(
@@ -465,6 +543,30 @@ int omni_conv_weight_flip_f32(const float* W, int o, int c, int k, float* Wf, lo
   weight_flip_kernel<<<omni::grid_for((long long)c * ld, kThreads), kThreads, 0,
                        omni::as_stream(stream)>>>(W, o, c, k, Wf, ld);
   return omni::check_launch("conv_weight_flip");
+}
+
+int omni_space_to_depth_f32(const float* X, int b, int n, int c, int cs, int s, float* Y, int n2,
+                            int cp, void* stream) {
+  OMNI_REQUIRE(b >= 0 && n >= 1 && c >= 1 && cs >= c && s >= 1 && n2 * s >= n && cp >= s * s * c &&
+                   cp % 4 == 0 && ((uintptr_t)Y % 16) == 0,
+               "space_to_depth: bad shape");
+  if (b == 0) return OMNI_OK;
+  const long long work = (long long)b * n2 * n2 * (cp / 4);
+  space_to_depth_kernel<<<omni::grid_for(work, kThreads), kThreads, 0, omni::as_stream(stream)>>>(
+      X, b, n, c, cs, s, Y, n2, cp);
+  return omni::check_launch("space_to_depth");
+}
+
+int omni_conv_weight_s2d_f32(float* W, int o, int c, int k, int s, int cp, float* Wt, long long ld,
+                             int inverse, void* stream) {
+  const int k2 = (k + s - 1) / s;
+  OMNI_REQUIRE(o >= 1 && c >= 1 && k >= 1 && s >= 1 && cp >= s * s * c &&
+                   ld >= (long long)k2 * k2 * cp,
+               "weight s2d: bad shape");
+  const long long work = inverse ? (long long)o * c * k * k : (long long)o * ld;
+  weight_s2d_kernel<<<omni::grid_for(work, kThreads), kThreads, 0, omni::as_stream(stream)>>>(
+      W, o, c, k, s, cp, Wt, ld, inverse);
+  return omni::check_launch("conv_weight_s2d");
 }
 
 int omni_transpose_f32(const float* src, long long lds, long long src_bstride, int rows, int cols,

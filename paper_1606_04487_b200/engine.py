@@ -74,6 +74,8 @@ class Op:
     ldK: int = 0
     w_inplace: bool = False
     implicit: bool = False
+    s2d: tuple | None = None          # (stride, k2, pad2, n2, cp) of the space-to-depth form
+    s2d_buf: torch.Tensor | None = None
     ldF: int = 0
     wflip: torch.Tensor | None = None
     dhat: torch.Tensor | None = None
@@ -129,7 +131,25 @@ class GpuNet:
                 # kernel, which needs stride 1 and d_out % 32 == 0.
                 op.implicit = (c % 32 == 0 and cur.cs % 4 == 0 and not explicit_only and
                                (first_param or (L.stride == 1 and d % 32 == 0)))
-                if op.implicit:
+                # Strided first layer with few channels (CaffeNet conv1: 3 ch, k=11, s=4):
+                # space-to-depth turns it into a stride-1 ceil(k/s)^2 conv over s*s*c
+                # channels (padded to 32), i.e. another implicit GEMM.
+                if (first_param and not op.implicit and not explicit_only and L.stride > 1
+                        and L.pad % L.stride == 0):
+                    st = L.stride
+                    k2 = -(-L.k // st)
+                    n2 = -(-n // st)
+                    p2 = L.pad // st
+                    cp = K.round_up(st * st * c, 32)
+                    if n2 + 2 * p2 - k2 + 1 == m and cp <= 2 * st * st * c:
+                        op.s2d = (st, k2, p2, n2, cp)
+                        op.implicit = True
+                        op.s2d_buf = z(self.b, n2, n2, cp)
+                if op.s2d is not None:
+                    st, k2, p2, n2, cp = op.s2d
+                    op.Kc = op.Kf = k2 * k2 * cp
+                    op.ldK = K.round_up(op.Kf, 32)
+                elif op.implicit:
                     op.Kf = op.Kc
                     op.ldK = K.round_up(op.Kf, 32)
                     if not first_param:
@@ -246,6 +266,16 @@ class GpuNet:
             M, N, Kd, A, lda, a_mn, B, ldb, b_mn, C, ldc, precision=self.prec, epilogue=epi,
             bias=bias, aux=aux, ld_aux=ld_aux, workspace=self._ws_active))
 
+    def _conv_input(self, op, b, transform=True):
+        """Activation + geometry the implicit GEMM of a conv layer reads: the layer
+        input itself, or its space-to-depth form (built here in forward)."""
+        if op.s2d is None:
+            return op.inp.value[:b], op.c_in, op.k, op.s, op.p
+        st, k2, p2, n2, cp = op.s2d
+        if transform:
+            K.space_to_depth(op.inp.value[:b], op.c_in, st, op.s2d_buf[:b])
+        return op.s2d_buf[:b], cp, k2, 1, p2
+
     def _conv(self, op_code, X, c, k, s, p, d, G, ldg, Y, ldy, epi=_abi.EPI_STORE, bias=None,
               aux=None, ld_aux=0):
         b, n = X.shape[0], X.shape[1]
@@ -266,7 +296,11 @@ class GpuNet:
             raise ValueError("the flat parameter vector must be 16-byte aligned")
         self._W = W
         for op in self.ops:
-            if op.kind == "conv":
+            if op.kind == "conv" and op.s2d is not None:
+                st, k2, p2, n2, cp = op.s2d
+                K.conv_weight_s2d(W[op.woff:op.woff + op.wsz], op.layer.d_out, op.c_in, op.k, st,
+                                  cp, op.wstage, op.ldK)
+            elif op.kind == "conv":
                 d = op.layer.d_out
                 bias = W[op.boff:op.boff + d] if op.boff >= 0 and not op.implicit else None
                 K.conv_weight_to_tap(W[op.woff:op.woff + op.wsz], d, op.c_in, op.k, op.wstage,
@@ -297,8 +331,9 @@ class GpuNet:
                     else:
                         epi = _abi.EPI_RELU if op.relu else _abi.EPI_STORE
                         bias = None
-                    self._conv(_abi.CONV_FPROP, op.inp.value[:b], op.c_in, op.k, op.s, op.p, d,
-                               op.wstage, op.ldK, op.out.value, op.out.cs, epi, bias)
+                    X, c_, k_, s_, p_ = self._conv_input(op, b)
+                    self._conv(_abi.CONV_FPROP, X, c_, k_, s_, p_, d, op.wstage, op.ldK,
+                               op.out.value, op.out.cs, epi, bias)
                     continue
                 K.lower_nhwc(op.inp.value[:b], op.c_in, op.k, op.s, op.p, op.ldK, out=op.dhat,
                              ones_col=op.boff >= 0)
@@ -413,10 +448,15 @@ class GpuNet:
                 dZ = op.out.grad
                 if op.implicit:
                     with wgrad_stream():
-                        self._conv(_abi.CONV_WGRAD, op.inp.value[:b], op.c_in, op.k, op.s, op.p, d,
-                                   dZ, op.out.cs, op.dwstage, op.ldK)
-                        K.conv_weight_to_tap(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k,
-                                             op.dwstage, op.ldK, inverse=True)
+                        X, c_, k_, s_, p_ = self._conv_input(op, b, transform=False)
+                        self._conv(_abi.CONV_WGRAD, X, c_, k_, s_, p_, d, dZ, op.out.cs,
+                                   op.dwstage, op.ldK)
+                        if op.s2d is not None:
+                            K.conv_weight_s2d(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k,
+                                              op.s2d[0], op.s2d[4], op.dwstage, op.ldK, inverse=True)
+                        else:
+                            K.conv_weight_to_tap(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k,
+                                                 op.dwstage, op.ldK, inverse=True)
                         if op.boff >= 0:
                             K.bias_grad(dZ, op.out.cs, Mr, d, G[op.boff:op.boff + d], self.bias_ws)
                         done(op)
@@ -484,6 +524,7 @@ class GpuNet:
         for op in self.ops:
             if op.kind == "conv" and op.implicit:
                 n += 1 + 1 + 1   # stage, implicit fprop, implicit wgrad
+                n += 1 if op.s2d is not None else 0   # space-to-depth of the input
                 n += 1 + (2 if op.boff >= 0 else 0)   # inverse stage, bias gradient
                 if not op.first_param_layer:
                     n += 2       # flipped-weight stage, implicit dgrad (+ fused ReLU mask)

@@ -244,6 +244,18 @@ def conv_weight_to_tap(W: torch.Tensor, o: int, c: int, k: int, Wt: torch.Tensor
          _stream())
 
 
+def space_to_depth(X: torch.Tensor, c: int, s: int, Y: torch.Tensor) -> None:
+    """NHWC X (b, n, n, cs) -> Y (b, n2, n2, cp) (see include/omni.h)."""
+    b, n, _, cs = X.shape
+    call("omni_space_to_depth_f32", _ptr(X), b, n, c, cs, s, _ptr(Y), Y.shape[1], Y.shape[3],
+         _stream())
+
+
+def conv_weight_s2d(W: torch.Tensor, o: int, c: int, k: int, s: int, cp: int, Wt: torch.Tensor,
+                    ld: int, inverse: bool = False) -> None:
+    call("omni_conv_weight_s2d_f32", _ptr(W), o, c, k, s, cp, _ptr(Wt), ld, int(inverse), _stream())
+
+
 def transpose(src: torch.Tensor, lds: int, src_bstride: int, rows: int, cols: int,
               dst: torch.Tensor, ldd: int, dst_bstride: int, batch: int = 1) -> None:
     call("omni_transpose_f32", _ptr(src), lds, src_bstride, rows, cols, _ptr(dst), ldd,

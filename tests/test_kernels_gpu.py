@@ -369,3 +369,37 @@ def test_conv_implicit_dgrad_via_flipped_weights(geom):
     out.backward(dY.permute(0, 3, 1, 2).double().cpu())
     torch.cuda.synchronize()
     assert rel_err(dX.cpu(), Xd.grad.permute(0, 2, 3, 1)) < 2e-6 * max(1.0, (d * k * k / 1000) ** 0.5)
+
+
+@pytest.mark.parametrize("geom", [(2, 27, 3, 11, 4, 0, 96), (2, 227, 3, 11, 4, 0, 96), (3, 16, 5, 4, 2, 0, 32)])
+def test_space_to_depth_conv_equals_strided_conv(geom):
+    """A stride-s k x k conv == the stride-1 ceil(k/s)^2 implicit conv of the
+    space-to-depth input with the mapped weights; and the weight-gradient maps back."""
+    b, n, c, k, s, p, d = geom
+    m = (n + 2 * p - k) // s + 1
+    gen = torch.Generator().manual_seed(21)
+    X = torch.randn(b, n, n, c, generator=gen).to(DEV)
+    W = (torch.randn(d, c, k, k, generator=gen) / (c * k * k) ** 0.5).to(DEV)
+    k2, n2 = -(-k // s), -(-n // s)
+    cp = K.round_up(s * s * c, 32)
+    assert n2 - k2 + 1 == m
+    Y = torch.empty(b, n2, n2, cp, device=DEV)
+    K.space_to_depth(X, c, s, Y)
+    ld = K.round_up(k2 * k2 * cp, 32)
+    Wt = torch.empty(d, ld, device=DEV)
+    K.conv_weight_s2d(W, d, c, k, s, cp, Wt, ld)
+    out = torch.empty(b * m * m, d, device=DEV)
+    K.conv_implicit(_abi.CONV_FPROP, Y, cp, k2, 1, 0, d, Wt, ld, out, d, precision=_abi.PREC_3XTF32)
+    Xd = X.permute(0, 3, 1, 2).double().cpu().requires_grad_(False)
+    Wd = W.double().cpu().requires_grad_(True)
+    ref = torch.nn.functional.conv2d(Xd, Wd, stride=s)
+    torch.cuda.synchronize()
+    assert rel_err(out.cpu(), ref.permute(0, 2, 3, 1).reshape(-1, d)) < 2e-6 * max(1.0, (k2 * k2 * cp / 1000) ** 0.5)
+    dY = torch.randn(b * m * m, d, generator=gen)
+    ref.backward(dY.reshape(b, m, m, d).permute(0, 3, 1, 2).double())
+    dWt = torch.empty(d, ld, device=DEV)
+    K.conv_implicit(_abi.CONV_WGRAD, Y, cp, k2, 1, 0, d, dY.to(DEV), d, dWt, ld, precision=_abi.PREC_3XTF32)
+    dW = torch.empty(d, c, k, k, device=DEV)
+    K.conv_weight_s2d(dW, d, c, k, s, cp, dWt, ld, inverse=True)
+    torch.cuda.synchronize()
+    assert rel_err(dW.cpu(), Wd.grad) < 2e-6 * max(1.0, (b * m * m / 1000) ** 0.5)
