@@ -293,30 +293,34 @@ __global__ void __launch_bounds__(kThreads) weight_flip_kernel(
 __global__ void __launch_bounds__(kThreads) space_to_depth_kernel(
     const float* __restrict__ X, int b, int n, int c, int cs, int s, float* __restrict__ Y, int n2,
     int cp) {
-  const int cv = cp / 4;
-  const long long total = (long long)b * n2 * n2 * cv;
+  // one block per output row (img, X2); shared decode table j -> (dx, dy, ch)
+  extern __shared__ int s2d_tab[];
   const int sc = s * c;
-  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long pix = idx / cv;
-    const int j0 = (int)(idx - pix * cv) * 4;
-    const int img = (int)(pix / ((long long)n2 * n2));
-    const int r = (int)(pix - (long long)img * n2 * n2);
-    const int X2 = r / n2, Y2 = r - (r / n2) * n2;
-    float v[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int j = j0 + t;
-      float val = 0.f;
-      if (j < s * sc) {
-        const int dx = j / sc, rem = j - (j / sc) * sc;
-        const int dy = rem / c, ch = rem - (rem / c) * c;
-        const int ix = s * X2 + dx, iy = s * Y2 + dy;
-        if (ix < n && iy < n) val = __ldg(X + (((long long)img * n + ix) * n + iy) * cs + ch);
-      }
-      v[t] = val;
+  for (int j = threadIdx.x; j < cp; j += blockDim.x) {
+    int e = -1;
+    if (j < s * sc) {
+      const int dx = j / sc, rem = j - (j / sc) * sc;
+      const int dy = rem / c, ch = rem - (rem / c) * c;
+      e = (dx << 24) | (dy << 16) | ch;
     }
-    *reinterpret_cast<float4*>(Y + pix * cp + j0) = make_float4(v[0], v[1], v[2], v[3]);
+    s2d_tab[j] = e;
+  }
+  __syncthreads();
+  for (int row = blockIdx.x; row < b * n2; row += gridDim.x) {
+    const int img = row / n2, X2 = row - (row / n2) * n2;
+    const float* Xi = X + (long long)img * n * n * cs;
+    float* out = Y + (long long)row * n2 * cp;
+    const int total = n2 * cp;
+    for (int q = threadIdx.x; q < total; q += blockDim.x) {
+      const int Y2 = q / cp, j = q - (q / cp) * cp;
+      const int e = s2d_tab[j];
+      float val = 0.f;
+      if (e >= 0) {
+        const int ix = s * X2 + (e >> 24), iy = s * Y2 + ((e >> 16) & 0xff);
+        if (ix < n && iy < n) val = __ldg(Xi + ((long long)ix * n + iy) * cs + (e & 0xffff));
+      }
+      out[q] = val;   // lane-consecutive q: coalesced 128-byte stores
+    }
   }
 }
 
@@ -551,8 +555,12 @@ int omni_space_to_depth_f32(const float* X, int b, int n, int c, int cs, int s, 
                    cp % 4 == 0 && ((uintptr_t)Y % 16) == 0,
                "space_to_depth: bad shape");
   if (b == 0) return OMNI_OK;
-  const long long work = (long long)b * n2 * n2 * (cp / 4);
-  space_to_depth_kernel<<<omni::grid_for(work, kThreads), kThreads, 0, omni::as_stream(stream)>>>(
+  OMNI_REQUIRE(cp <= 12288, "space_to_depth: too many channels");
+  const int rows = b * n2;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int grid = rows < omni::sm_count_cached(dev) * 16 ? rows : omni::sm_count_cached(dev) * 16;
+  space_to_depth_kernel<<<grid, kThreads, cp * sizeof(int), omni::as_stream(stream)>>>(
       X, b, n, c, cs, s, Y, n2, cp);
   return omni::check_launch("space_to_depth");
 }
