@@ -144,10 +144,21 @@ __global__ void __launch_bounds__(kThreads) lower_nhwc_table_kernel(
     float* out = Dhat + (long long)row * ld;
     if (ix0 >= 0 && iy0 >= 0 && ix0 + k <= n && iy0 + k <= n) {
       const float* org = X + (((long long)img * n + ix0) * n + iy0) * cs;
-#pragma unroll 4
-      for (int j = lane; j < ld; j += 32) {
-        const int e = kxy[j];
-        out[j] = e >= 0 ? __ldg(org + off[j]) : (e == -2 ? 1.f : 0.f);
+      for (int j0 = lane; j0 < ld; j0 += 128) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + 32 * u;
+          float val = 0.f;
+          if (j < ld) {
+            const int e = kxy[j];
+            val = e >= 0 ? __ldg(org + off[j]) : (e == -2 ? 1.f : 0.f);
+          }
+          v[u] = val;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (j0 + 32 * u < ld) out[j0 + 32 * u] = v[u];
       }
     } else {
       const float* Ximg = X + (long long)img * n * n * cs;
@@ -311,15 +322,28 @@ __global__ void __launch_bounds__(kThreads) space_to_depth_kernel(
     const float* Xi = X + (long long)img * n * n * cs;
     float* out = Y + (long long)row * n2 * cp;
     const int total = n2 * cp;
-    for (int q = threadIdx.x; q < total; q += blockDim.x) {
-      const int Y2 = q / cp, j = q - (q / cp) * cp;
-      const int e = s2d_tab[j];
-      float val = 0.f;
-      if (e >= 0) {
-        const int ix = s * X2 + (e >> 24), iy = s * Y2 + ((e >> 16) & 0xff);
-        if (ix < n && iy < n) val = __ldg(Xi + ((long long)ix * n + iy) * cs + (e & 0xffff));
+    // 4 independent loads in flight per thread before the (coalesced) stores
+    for (int q0 = threadIdx.x; q0 < total; q0 += 4 * blockDim.x) {
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * blockDim.x;
+        float val = 0.f;
+        if (q < total) {
+          const int Y2 = q / cp, j = q - (q / cp) * cp;
+          const int e = s2d_tab[j];
+          if (e >= 0) {
+            const int ix = s * X2 + (e >> 24), iy = s * Y2 + ((e >> 16) & 0xff);
+            if (ix < n && iy < n) val = __ldg(Xi + ((long long)ix * n + iy) * cs + (e & 0xffff));
+          }
+        }
+        v[u] = val;
       }
-      out[q] = val;   // lane-consecutive q: coalesced 128-byte stores
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * blockDim.x;
+        if (q < total) out[q] = v[u];
+      }
     }
   }
 }
