@@ -348,6 +348,57 @@ __global__ void __launch_bounds__(kThreads) space_to_depth_kernel(
   }
 }
 
+// Fast path (cs == c, (s*c) % 4 == 0): every output float4 (4 consecutive j) is
+// 4 contiguous input floats of one input row; table per group: (dx, dy of the
+// group's first element, offset within the s-pixel run).
+__global__ void __launch_bounds__(kThreads) space_to_depth_v4_kernel(
+    const float* __restrict__ X, int b, int n, int c, int s, float* __restrict__ Y, int n2,
+    int cp) {
+  extern __shared__ int s2d_tab[];
+  const int sc = s * c, g4 = cp / 4;
+  for (int t = threadIdx.x; t < g4; t += blockDim.x) {
+    const int j = 4 * t;
+    int e = -1;
+    if (j < s * sc) {
+      const int dx = j / sc, off = j - (j / sc) * sc;   // off = dy*c + ch, 4 contiguous floats
+      e = (dx << 16) | off;
+    }
+    s2d_tab[t] = e;
+  }
+  __syncthreads();
+  for (int row = blockIdx.x; row < b * n2; row += gridDim.x) {
+    const int img = row / n2, X2 = row - (row / n2) * n2;
+    float4* out = reinterpret_cast<float4*>(Y + (long long)row * n2 * cp);
+    const int total = n2 * g4;
+    for (int q0 = threadIdx.x; q0 < total; q0 += 2 * blockDim.x) {
+      float4 v[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int q = q0 + u * blockDim.x;
+        float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (q < total) {
+          const int Y2 = q / g4, t = q - (q / g4) * g4;
+          const int e = s2d_tab[t];
+          const int ix = s * X2 + (e >> 16);
+          if (e >= 0 && ix < n) {
+            const int off = e & 0xffff;
+            const float* src = X + (((long long)img * n + ix) * n + (long long)s * Y2) * c + off;
+            const int iy0 = s * Y2 + off / c;   // pixel of the first element; others may spill past n
+            float a[4];
+#pragma unroll
+            for (int w = 0; w < 4; ++w) a[w] = (iy0 + (off % c + w) / c < n) ? __ldg(src + w) : 0.f;
+            r = make_float4(a[0], a[1], a[2], a[3]);
+          }
+        }
+        v[u] = r;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (q0 + u * blockDim.x < total) out[q0 + u * blockDim.x] = v[u];
+    }
+  }
+}
+
 // Weights of the space-to-depth conv: Wt[o*ld + (kx2*k2 + ky2)*cp + (dx*s + dy)*c + ch]
 // = W[o, ch, s*kx2+dx, s*ky2+dy] (0 past the original kernel / padded channels).
 // inverse: read dWt, write the OIHW gradient (padded entries dropped).
@@ -584,8 +635,12 @@ int omni_space_to_depth_f32(const float* X, int b, int n, int c, int cs, int s, 
   int dev = 0;
   cudaGetDevice(&dev);
   const int grid = rows < omni::sm_count_cached(dev) * 16 ? rows : omni::sm_count_cached(dev) * 16;
-  space_to_depth_kernel<<<grid, kThreads, cp * sizeof(int), omni::as_stream(stream)>>>(
-      X, b, n, c, cs, s, Y, n2, cp);
+  if (cs == c && (s * c) % 4 == 0)
+    space_to_depth_v4_kernel<<<grid, kThreads, (cp / 4) * sizeof(int), omni::as_stream(stream)>>>(
+        X, b, n, c, s, Y, n2, cp);
+  else
+    space_to_depth_kernel<<<grid, kThreads, cp * sizeof(int), omni::as_stream(stream)>>>(
+        X, b, n, c, cs, s, Y, n2, cp);
   return omni::check_launch("space_to_depth");
 }
 
