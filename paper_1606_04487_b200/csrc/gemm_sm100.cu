@@ -736,10 +736,21 @@ Plan make_plan(int M, int N, int K, int sms, int bkt = BK) {
   const long long tiles = (long long)pl.m_tiles * pl.n_tiles;
   int splits = 1;
   if (tiles < sms && pl.k_tiles >= 8) {
-    splits = (int)(sms / tiles);
-    const int max_splits = pl.k_tiles / 4;  // keep >= 4 k-tiles per split
-    if (splits > max_splits) splits = max_splits;
-    if (splits < 1) splits = 1;
+    // Split-K cost model: the persistent grid finishes after ceil(tiles*s/sms)
+    // rounds of (k_tiles/s) k-steps each; every extra split adds one M x N
+    // fp32 partial written and re-read by the fixed-order reduction.
+    const double t_kstep = 2.0 * BM * pl.bn * bkt / (650e12 / sms);  // s per k-step per SM
+    const int max_splits = pl.k_tiles / 4 < 64 ? pl.k_tiles / 4 : 64;  // >= 4 k-steps per split
+    double best = 1e30;
+    for (int s = 1; s <= max_splits; ++s) {
+      const long long rounds = omni::ceil_div(tiles * s, sms);
+      const double t = rounds * omni::ceil_div(pl.k_tiles, s) * t_kstep +
+                       (s > 1 ? s * (double)M * N * 8.0 / 6.0e12 : 0.0);
+      if (t < best * 0.98) {   // prefer fewer splits unless clearly faster
+        best = t;
+        splits = s;
+      }
+    }
   }
   pl.kps = (int)omni::ceil_div(pl.k_tiles, splits);
   pl.splits = (int)omni::ceil_div(pl.k_tiles, pl.kps);
