@@ -1,7 +1,9 @@
 """GPU unit tests of the individual sm_100a kernels through the C-ABI.
 
-Floating-point kernels are compared against a plain PyTorch fp64/fp32
-reference of the same op; data-movement kernels must be bit-exact.
+Floating-point kernels are compared against a plain PyTorch fp64 reference of
+the same op (normwise relative error; 3xTF32 bound 5e-6 * max(1, sqrt(K/1000)):
+tf32 hi/lo products lose ~2^-21 and the tensor-core fp32 accumulation is not
+IEEE-exact); data-movement kernels must be bit-exact.
 """
 
 import numpy as np
@@ -61,7 +63,7 @@ def test_gemm_vs_torch(a_mn, b_mn, shape, prec):
     ref = Al @ Bl.t()
     err = rel_err(C.cpu(), ref)
     # fp32 accumulation error grows like sqrt(K)
-    tol = 3e-3 if prec == "tf32" else 2e-6 * max(1.0, (Kd / 1000.0) ** 0.5)
+    tol = 3e-3 if prec == "tf32" else 5e-6 * max(1.0, (Kd / 1000.0) ** 0.5)
     assert err < tol, (shape, a_mn, b_mn, prec, err)
 
 
@@ -328,10 +330,10 @@ def test_conv_implicit_fprop(geom, prec):
     Yr = torch.empty(b * m * m, d, device=DEV)
     K.gemm(b * m * m, d, Kc, D, ld, False, Wt, ld, False, Yr, d, precision=pr)
     torch.cuda.synchronize()
-    assert rel_err(Y.cpu(), Yr.cpu()) < 1e-6, rel_err(Y.cpu(), Yr.cpu())
+    assert rel_err(Y.cpu(), Yr.cpu()) < 2e-6, rel_err(Y.cpu(), Yr.cpu())
     ref = torch.nn.functional.conv2d(X.permute(0, 3, 1, 2).double().cpu(), W.double().cpu(),
                                      stride=s, padding=p).permute(0, 2, 3, 1).reshape(b * m * m, d)
-    assert rel_err(Y.cpu(), ref) < (3e-3 if prec == "tf32" else 2e-6 * max(1.0, (Kc / 1000) ** 0.5))
+    assert rel_err(Y.cpu(), ref) < (3e-3 if prec == "tf32" else 5e-6 * max(1.0, (Kc / 1000) ** 0.5))
 
 
 @pytest.mark.parametrize("geom", IMPLICIT_GEOMS)
@@ -347,7 +349,7 @@ def test_conv_implicit_wgrad(geom):
     D = K.lower_nhwc(X, c, k, s, p, ld)
     ref = (dY.double().t() @ D[:, :Kc].double()).cpu()
     torch.cuda.synchronize()
-    assert rel_err(dW[:, :Kc].cpu(), ref) < 2e-6 * max(1.0, (b * m * m / 1000) ** 0.5)
+    assert rel_err(dW[:, :Kc].cpu(), ref) < 5e-6 * max(1.0, (b * m * m / 1000) ** 0.5)
 
 
 @pytest.mark.parametrize("geom", [g for g in IMPLICIT_GEOMS if g[4] == 1 and g[6] % 32 == 0])
@@ -368,7 +370,7 @@ def test_conv_implicit_dgrad_via_flipped_weights(geom):
     out = torch.nn.functional.conv2d(Xd, W.double().cpu(), padding=p)
     out.backward(dY.permute(0, 3, 1, 2).double().cpu())
     torch.cuda.synchronize()
-    assert rel_err(dX.cpu(), Xd.grad.permute(0, 2, 3, 1)) < 2e-6 * max(1.0, (d * k * k / 1000) ** 0.5)
+    assert rel_err(dX.cpu(), Xd.grad.permute(0, 2, 3, 1)) < 5e-6 * max(1.0, (d * k * k / 1000) ** 0.5)
 
 
 @pytest.mark.parametrize("geom", [(2, 27, 3, 11, 4, 0, 96), (2, 227, 3, 11, 4, 0, 96), (3, 16, 5, 4, 2, 0, 32)])
@@ -394,7 +396,7 @@ def test_space_to_depth_conv_equals_strided_conv(geom):
     Wd = W.double().cpu().requires_grad_(True)
     ref = torch.nn.functional.conv2d(Xd, Wd, stride=s)
     torch.cuda.synchronize()
-    assert rel_err(out.cpu(), ref.permute(0, 2, 3, 1).reshape(-1, d)) < 2e-6 * max(1.0, (k2 * k2 * cp / 1000) ** 0.5)
+    assert rel_err(out.cpu(), ref.permute(0, 2, 3, 1).reshape(-1, d)) < 5e-6 * max(1.0, (k2 * k2 * cp / 1000) ** 0.5)
     dY = torch.randn(b * m * m, d, generator=gen)
     ref.backward(dY.reshape(b, m, m, d).permute(0, 3, 1, 2).double())
     dWt = torch.empty(d, ld, device=DEV)
@@ -402,4 +404,4 @@ def test_space_to_depth_conv_equals_strided_conv(geom):
     dW = torch.empty(d, c, k, k, device=DEV)
     K.conv_weight_s2d(dW, d, c, k, s, cp, dWt, ld, inverse=True)
     torch.cuda.synchronize()
-    assert rel_err(dW.cpu(), Wd.grad) < 2e-6 * max(1.0, (b * m * m / 1000) ** 0.5)
+    assert rel_err(dW.cpu(), Wd.grad) < 5e-6 * max(1.0, (b * m * m / 1000) ** 0.5)
