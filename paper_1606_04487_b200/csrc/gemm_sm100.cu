@@ -823,7 +823,15 @@ int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, lon
     if (rc) return rc;
   }
   auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT3, IM2COL, BKT>;
-  OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
+  // once per instantiation and device (so a launch inside CUDA-graph capture
+  // makes no attribute calls)
+  static unsigned long long configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured & (1ull << (dev & 63)))) {
+    OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
+    configured |= 1ull << (dev & 63);
+  }
   kern<<<pl.grid, L::THREADS, L::BYTES, st>>>(ta, tb, tc, p);
   return omni::check_launch("gemm_tf32");
 }

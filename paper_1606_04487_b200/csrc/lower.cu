@@ -548,9 +548,12 @@ int omni_lower_nhwc_f32(const float* X, int b, int n, int c, int cs, int k, int 
         X, n, c, cs, k, stride, pad, m, (int)rows, K, (int)ld, ones_col, Dhat);
   } else if (ld <= 8192) {
     const int smem = 2 * (int)ld * (int)sizeof(int);
-    if (smem > 48 * 1024)
+    static int configured_max = 48 * 1024;
+    if (smem > configured_max) {
       OMNI_CUDA_TRY(cudaFuncSetAttribute(lower_nhwc_table_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+      configured_max = 64 * 1024;
+    }
     lower_nhwc_table_kernel<<<grid, kThreads, smem, st>>>(
         X, n, c, cs, k, stride, pad, m, (int)rows, K, (int)ld, ones_col, Dhat);
   } else if (cs == c) {

@@ -98,7 +98,7 @@ class DeviceSession:
     and the mean over ranks is folded into the fused update."""
 
     def __init__(self, problem: "CNNProblem", state: SGDState, hp: Hyperparams,
-                 process_group=None):
+                 process_group=None, use_graph: bool = True):
         self.problem = problem
         self.hp = hp
         dev = problem.device
@@ -112,6 +112,14 @@ class DeviceSession:
         self._slot_free = [None, None]
         self._next_slot = 0
         self._copy_stream = None
+        # CUDA graph of a whole single-GPU step on device-resident batches:
+        # captured on the second such step (the first eager one does all lazy
+        # setup), replayed with the batch indices copied into a static buffer.
+        self.use_graph = use_graph
+        self._graph = None
+        self._graph_key = None
+        self._graph_seen = 0
+        self._gidx = None
         self.world = 1
         if process_group is not None:
             import torch.distributed as dist
@@ -166,9 +174,36 @@ class DeviceSession:
         self._pending_free = (slot, free)
         return batch.size
 
+    def _graphable(self, batch, w_read) -> bool:
+        return (self.use_graph and self.world == 1 and w_read is None and
+                isinstance(batch, DeviceBatch) and batch.size == self.engine.b and
+                self.engine.timer is None and self.engine.overlap)
+
     def step(self, batch: Any, w_read: torch.Tensor | None = None) -> None:
         """V = mu V - eta (grad(w_read) + lam w_read); W += V, with w_read = W when
         synchronous (sgd.py:104-112)."""
+        if self._graphable(batch, w_read):
+            key = (self.W.data_ptr(), self.V.data_ptr(), self.problem.data.data_ptr())
+            if self._graph is not None and self._graph_key == key:
+                self._gidx.copy_(batch.idx, non_blocking=True)
+                self._graph.replay()
+                self.t += 1
+                return
+            self._graph_seen += 1
+            if self._graph_seen >= 2:       # capture (the eager first step did the lazy setup)
+                self._gidx = torch.empty_like(batch.idx)
+                self._gidx.copy_(batch.idx)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._step(DeviceBatch(self._gidx), None)
+                self._graph, self._graph_key = g, key
+                g.replay()                   # capture does not execute: run this step now
+                self.t += 1
+                return
+        self._step(batch, w_read)
+        self.t += 1
+
+    def _step(self, batch: Any, w_read: torch.Tensor | None) -> None:
         wr = self.W if w_read is None else w_read
         self._pending_free = None
         b = self._load(batch)
@@ -189,7 +224,6 @@ class DeviceSession:
             free.record(torch.cuda.current_stream())
             self._slot_free[slot] = free
             self.engine.input.value, self.engine.labels = self._own   # launches already hold the pointers
-        self.t += 1
 
     def full_loss(self) -> float:
         return self.problem.full_loss_device(self.W)

@@ -1,0 +1,55 @@
+"""DeviceSession execution modes must not change the math: eager steps, CUDA
+graph replay, and host batches prefetched on a copy stream give bit-identical
+weights for the same batches."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_1606_04487_b200 as P  # noqa: E402
+from paper_1606_04487_b200.problems import CNNProblem, DeviceBatch, HostBatch  # noqa: E402
+
+
+@pytest.mark.parametrize("net,b", [("lenet", 16), ("cifar10_quick", 8)])
+def test_graph_replay_equals_eager(net, b):
+    prob = CNNProblem(net, n_examples=64, seed=2, precision="tf32")
+    hp = P.Hyperparams(eta=0.01, mu=0.9, lam=5e-4, b=b)
+    rng = np.random.default_rng(0)
+    batches = [torch.from_numpy(rng.integers(0, 64, size=b)).cuda() for _ in range(6)]
+    state = prob.initial_state()
+    out = []
+    for use_graph in (False, True):
+        sess = prob.device_session(state, hp)
+        sess.use_graph = use_graph
+        losses = []
+        for idx in batches:
+            sess.step(DeviceBatch(idx))
+            losses.append(sess.last_loss())
+        assert (sess._graph is not None) == use_graph
+        out.append((sess.W.clone(), sess.V.clone(), losses, sess.t))
+    (W0, V0, l0, t0), (W1, V1, l1, t1) = out
+    assert t0 == t1 == 6
+    assert torch.equal(W0, W1) and torch.equal(V0, V1) and l0 == l1
+
+
+def test_prefetched_host_batches_equal_device_batches():
+    prob = CNNProblem("cifar10_quick", n_examples=32, seed=5, precision="tf32")
+    hp = P.Hyperparams(eta=0.01, mu=0.9, b=8)
+    state = prob.initial_state()
+    rng = np.random.default_rng(1)
+    idxs = [rng.integers(0, 32, size=8) for _ in range(4)]
+    a = prob.device_session(state, hp, use_graph=False)
+    for idx in idxs:
+        a.step(DeviceBatch(torch.from_numpy(idx).cuda()))
+    b = prob.device_session(state, hp)
+    hbs = [HostBatch(prob.data[torch.from_numpy(i).cuda()].cpu().pin_memory(),
+                     prob.data_labels[torch.from_numpy(i).cuda()].cpu().pin_memory()) for i in idxs]
+    b.prefetch(hbs[0])
+    for i, hb in enumerate(hbs):
+        b.step(hb)
+        if i + 1 < len(hbs):
+            b.prefetch(hbs[i + 1])
+    torch.cuda.synchronize()
+    assert torch.equal(a.W, b.W) and torch.equal(a.V, b.V)
