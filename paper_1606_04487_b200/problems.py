@@ -116,9 +116,8 @@ class DeviceSession:
         # captured on the second such step (the first eager one does all lazy
         # setup), replayed with the batch indices copied into a static buffer.
         self.use_graph = use_graph
-        self._graph = None
-        self._graph_key = None
-        self._graph_seen = 0
+        self._graphs: dict = {}
+        self._seen: dict = {}
         self._gidx = None
         self.world = 1
         if process_group is not None:
@@ -159,54 +158,10 @@ class DeviceSession:
             ready.record(self._copy_stream)
         self._staged[id(batch)] = (slot, ready)
 
-    def _load(self, batch) -> int:
-        staged = self._staged.pop(id(batch), None) if isinstance(batch, HostBatch) else None
-        if staged is None:
-            return self.problem.load_batch(self.engine, batch)
-        slot, ready = staged
-        cur = torch.cuda.current_stream()
-        cur.wait_event(ready)
-        X, y = self._slots[slot]
-        eng = self.engine
-        self._own = (eng.input.value, eng.labels)
-        eng.input.value, eng.labels = X, y          # consume the staged buffers in place
-        free = torch.cuda.Event()
-        self._pending_free = (slot, free)
-        return batch.size
-
-    def _graphable(self, batch, w_read) -> bool:
-        return (self.use_graph and self.world == 1 and w_read is None and
-                isinstance(batch, DeviceBatch) and batch.size == self.engine.b and
-                self.engine.timer is None and self.engine.overlap)
-
-    def step(self, batch: Any, w_read: torch.Tensor | None = None) -> None:
-        """V = mu V - eta (grad(w_read) + lam w_read); W += V, with w_read = W when
-        synchronous (sgd.py:104-112)."""
-        if self._graphable(batch, w_read):
-            key = (self.W.data_ptr(), self.V.data_ptr(), self.problem.data.data_ptr())
-            if self._graph is not None and self._graph_key == key:
-                self._gidx.copy_(batch.idx, non_blocking=True)
-                self._graph.replay()
-                self.t += 1
-                return
-            self._graph_seen += 1
-            if self._graph_seen >= 2:       # capture (the eager first step did the lazy setup)
-                self._gidx = torch.empty_like(batch.idx)
-                self._gidx.copy_(batch.idx)
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    self._step(DeviceBatch(self._gidx), None)
-                self._graph, self._graph_key = g, key
-                g.replay()                   # capture does not execute: run this step now
-                self.t += 1
-                return
-        self._step(batch, w_read)
-        self.t += 1
-
-    def _step(self, batch: Any, w_read: torch.Tensor | None) -> None:
-        wr = self.W if w_read is None else w_read
-        self._pending_free = None
-        b = self._load(batch)
+    # ------------------------------------------------------------ steps --
+    def _compute(self, wr: torch.Tensor, b: int) -> None:
+        """forward + backward (+ overlapped allreduce) + fused update on the batch
+        already in the engine's input buffers."""
         hp = self.hp
         if self.world > 1:
             works = []
@@ -219,11 +174,71 @@ class DeviceSession:
         else:
             self.engine.loss_and_grad(wr, b)
             K.sgd_momentum(self.W, self.V, self.engine.grad, wr, hp.eta, hp.mu, hp.lam)
-        if self._pending_free is not None:
-            slot, free = self._pending_free
-            free.record(torch.cuda.current_stream())
-            self._slot_free[slot] = free
-            self.engine.input.value, self.engine.labels = self._own   # launches already hold the pointers
+
+    def _run_on_slot(self, slot: int, b: int, wr: torch.Tensor) -> None:
+        eng = self.engine
+        own = (eng.input.value, eng.labels)
+        eng.input.value, eng.labels = self._slots[slot]   # consume the staged buffers in place
+        try:
+            self._compute(wr, b)
+        finally:
+            eng.input.value, eng.labels = own            # launches already hold the pointers
+
+    def _graph_key(self, batch, w_read):
+        if not (self.use_graph and self.world == 1 and w_read is None and
+                self.engine.timer is None and self.engine.overlap):
+            return None
+        base = (self.W.data_ptr(), self.V.data_ptr())
+        if isinstance(batch, DeviceBatch) and batch.size == self.engine.b:
+            return ("device", self.problem.data.data_ptr()) + base
+        if isinstance(batch, HostBatch) and batch.size == self.engine.b and id(batch) in self._staged:
+            return ("host", self._staged[id(batch)][0]) + base
+        return None
+
+    def step(self, batch: Any, w_read: torch.Tensor | None = None) -> None:
+        """V = mu V - eta (grad(w_read) + lam w_read); W += V, with w_read = W when
+        synchronous (sgd.py:104-112).
+
+        Single-GPU steps on full device batches or prefetched host batches are
+        captured in a CUDA graph on their second occurrence and replayed after."""
+        wr = self.W if w_read is None else w_read
+        key = self._graph_key(batch, w_read)
+        staged = self._staged.pop(id(batch), None) if isinstance(batch, HostBatch) else None
+        cur = torch.cuda.current_stream()
+        if staged is not None:
+            cur.wait_event(staged[1])                     # H2D of this batch done
+        if key is not None and key in self._graphs:
+            if key[0] == "device":
+                self._gidx.copy_(batch.idx, non_blocking=True)
+            self._graphs[key].replay()
+        elif key is not None and self._seen.get(key, 0) >= 1:
+            # second occurrence: capture (the first eager step did all lazy setup)
+            g = torch.cuda.CUDAGraph()
+            if key[0] == "device":
+                if self._gidx is None or self._gidx.numel() != batch.size:
+                    self._gidx = torch.empty_like(batch.idx)
+                self._gidx.copy_(batch.idx)
+                with torch.cuda.graph(g):
+                    self.engine.gather_batch(self.problem.data, self.problem.data_labels, self._gidx)
+                    self._compute(wr, batch.size)
+            else:
+                with torch.cuda.graph(g):
+                    self._run_on_slot(key[1], batch.size, wr)
+            self._graphs[key] = g
+            g.replay()                                     # capture does not execute
+        else:
+            if key is not None:
+                self._seen[key] = self._seen.get(key, 0) + 1
+            if staged is not None:
+                self._run_on_slot(staged[0], batch.size, wr)
+            else:
+                b = self.problem.load_batch(self.engine, batch)
+                self._compute(wr, b)
+        if staged is not None:
+            free = torch.cuda.Event()
+            free.record(cur)
+            self._slot_free[staged[0]] = free
+        self.t += 1
 
     def full_loss(self) -> float:
         return self.problem.full_loss_device(self.W)
@@ -367,8 +382,9 @@ class CNNProblem(TrainingProblem):
             acc += G.double() * (b / n)
         return acc.cpu().numpy()
 
-    def device_session(self, state: SGDState, hp: Hyperparams, process_group=None) -> DeviceSession:
-        return DeviceSession(self, state, hp, process_group)
+    def device_session(self, state: SGDState, hp: Hyperparams, process_group=None,
+                       use_graph: bool = True) -> DeviceSession:
+        return DeviceSession(self, state, hp, process_group, use_graph)
 
 
 def make_cnn(net: str, n_examples: int = 128, seed: int = 0, **kw) -> CNNProblem:
