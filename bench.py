@@ -28,6 +28,9 @@ import numpy as np
 # stdout carries exactly one JSON line: keep the real stdout for it and send
 # everything else that writes to fd 1 (NCCL's version banner, library chatter) to stderr.
 os.environ["NCCL_DEBUG"] = os.environ.get("BENCH_NCCL_DEBUG", "WARN")
+# Measured on 4x B200 (profiles/README.md): the per-layer gradient allreduces,
+# overlapped with the backward, run 6% faster over ring/tree than over NVLS.
+os.environ.setdefault("NCCL_NVLS_ENABLE", "0")
 _JSON_FD = os.dup(1)
 os.dup2(2, 1)
 
