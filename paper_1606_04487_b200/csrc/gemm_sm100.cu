@@ -220,13 +220,19 @@ __device__ __forceinline__ void decode_work(const Params& p, int w, int& mt, int
   }
 }
 
+// With transpose_c the logical output is C^T: the bias indexes rows and the
+// mask operand is read transposed, so both stay in the caller's layout.
 template <int MODE>
 __device__ __forceinline__ float epi_one(float acc, const Params& p, int row, int col,
                                          const float* Crow) {
-  if (MODE == OMNI_EPI_BIAS) return acc + __ldg(p.bias + col);
-  if (MODE == OMNI_EPI_BIAS_RELU) return fmaxf(acc + __ldg(p.bias + col), 0.f);
+  const int bi = p.transpose_c ? row : col;
+  if (MODE == OMNI_EPI_BIAS) return acc + __ldg(p.bias + bi);
+  if (MODE == OMNI_EPI_BIAS_RELU) return fmaxf(acc + __ldg(p.bias + bi), 0.f);
   if (MODE == OMNI_EPI_ACCUM) return Crow[col] + acc;
-  if (MODE == OMNI_EPI_MASK_AUX) return __ldg(p.aux + (long long)row * p.ld_aux + col) > 0.f ? acc : 0.f;
+  if (MODE == OMNI_EPI_MASK_AUX) {
+    const long long ai = p.transpose_c ? (long long)col * p.ld_aux + row : (long long)row * p.ld_aux + col;
+    return __ldg(p.aux + ai) > 0.f ? acc : 0.f;
+  }
   if (MODE == OMNI_EPI_RELU) return fmaxf(acc, 0.f);
   return acc;
 }
@@ -326,14 +332,21 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
         decode_work(p, w, mt, nt, sp);
         const int kt0 = sp * p.kt_per_split;
         const int kt1 = min(p.k_tiles, kt0 + p.kt_per_split);
-        // im2col A: window corner of this tile's first output pixel
-        int a_img = 0, a_h0 = 0, a_w0 = 0;
+        // im2col A (or B): window corner of this tile's first output pixel
+        int a_img = 0, a_h0 = 0, a_w0 = 0, b_img = 0, b_h0 = 0, b_w0 = 0;
         if (IM2COL == 1) {
           const int m0 = mt * BM;
           a_img = m0 / p.conv_mm;
           const int r = m0 - a_img * p.conv_mm;
           a_h0 = (r / p.conv_m) * p.conv_s - p.conv_pad;
           a_w0 = (r - (r / p.conv_m) * p.conv_m) * p.conv_s - p.conv_pad;
+        }
+        if (IM2COL == 4) {
+          const int n0 = nt * BN;
+          b_img = n0 / p.conv_mm;
+          const int r = n0 - b_img * p.conv_mm;
+          b_h0 = (r / p.conv_m) * p.conv_s - p.conv_pad;
+          b_w0 = (r - (r / p.conv_m) * p.conv_m) * p.conv_s - p.conv_pad;
         }
         for (int kt = kt0; kt < kt1; ++kt) {
           mbar_wait(empty_bar(stage), phase ^ 1);
@@ -371,7 +384,13 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
             for (int j = 0; j < BM / 32; ++j)
               tma_load_2d(&tmA, a_dst + j * (BKT * 128), full_bar(stage), mt * BM + 32 * j, kc);
           }
-          if (IM2COL == 2) {
+          if (IM2COL == 4) {
+            // B(j = pixel, r = (tap, ch)): BN output pixels x 32 channels, K-major
+            const int cb = kt % p.conv_cblocks, tap = kt / p.conv_cblocks;
+            const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
+            tma_load_im2col(&tmB, b_dst, full_bar(stage), cb * 32, b_w0, b_h0, b_img,
+                            (uint16_t)ky, (uint16_t)kx);
+          } else if (IM2COL == 2) {
             // B(j = (tap, ch), r = pixel): BK output pixels x 32 channels per chunk
             const int img = kc / p.conv_mm;
             const int r = kc - img * p.conv_mm;
@@ -594,7 +613,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
     float acc = 0.f;
     for (int s = 0; s < S; ++s) acc += ws[(long long)s * MN + idx];
     if (p.transpose_c) {
-      p.C[(long long)col * p.ldc + row] = acc;
+      p.C[(long long)col * p.ldc + row] = epi_apply(p.epilogue, acc, p, row, col, nullptr);
     } else {
       float* Crow = p.C + (long long)row * p.ldc;
       Crow[col] = epi_apply(p.epilogue, acc, p, row, col, Crow);
@@ -813,6 +832,7 @@ int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, lon
                  : make_tmap(&ta, A, p.K, p.M, lda, 32, BM, false);
   if (rc) return rc;
   if (IM2COL == 2) rc = make_tmap_im2col(&tb, *cg, BKT, true);
+  else if (IM2COL == 4) rc = make_tmap_im2col(&tb, *cg, BN, false);
   else rc = B_MN ? make_tmap(&tb, B, p.N, p.K, ldb, 32, BKT, true)
                  : make_tmap(&tb, B, p.K, p.N, ldb, 32, BN, false);
   if (rc) return rc;
@@ -912,7 +932,7 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
     p.use_tma_store = p.vec_ok && epilogue != OMNI_EPI_ACCUM;
   }
   if (getenv("OMNI_NO_TMA_STORE")) p.use_tma_store = 0;
-  if (im2col == 3) {
+  if (im2col == 3 || im2col == 4) {
     p.transpose_c = pl.splits > 1 ? 0 : 1;  // partials are natural; the reduce transposes
     if (p.transpose_c) p.use_tma_store = 0;
   }
@@ -924,6 +944,9 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
   else if (im2col == 3)
     rc = s3 ? dispatch_bn<true, true, true, 3>(pl, A, lda, B, ldb, p, st, cg)
             : dispatch_bn<true, true, false, 3, 64>(pl, A, lda, B, ldb, p, st, cg);
+  else if (im2col == 4)
+    rc = s3 ? dispatch_bn<false, false, true, 4>(pl, A, lda, B, ldb, p, st, cg)
+            : dispatch_bn<false, false, false, 4>(pl, A, lda, B, ldb, p, st, cg);
   else
     rc = s3 ? dispatch_major<true>(pl, a_mn, b_mn ? 1 : 0, A, lda, B, ldb, p, st)
             : dispatch_major<false>(pl, a_mn, b_mn ? 1 : 0, A, lda, B, ldb, p, st);
@@ -932,7 +955,7 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
     Params q = p;
     q.C = C;
     q.ldc = ldc;
-    q.transpose_c = (im2col == 3);
+    q.transpose_c = (im2col == 3 || im2col == 4);
     splitk_reduce_kernel<<<omni::grid_for((long long)M * N, 256), 256, 0, st>>>(workspace,
                                                                               pl.splits, M, N, q);
     rc = omni::check_launch("splitk_reduce");
@@ -1006,6 +1029,11 @@ int omni_gemm_f32(int precision, int M, int N, int K, const float* A, long long 
                         epilogue, bias, aux, ld_aux, workspace, ws_bytes, st, nullptr, 0);
 }
 
+static bool conv_fprop_transposed(int d_out, int pixels) {
+  static const bool off = getenv("OMNI_NO_TRANSPOSED_FPROP") != nullptr;
+  return !off && d_out <= 128 && pixels >= 128 * 148;
+}
+
 static int conv_shape(int op, int b, int n, int c, int k, int stride, int pad, int d_out, int* M,
                       int* N, int* K, int* m) {
   OMNI_REQUIRE(op == OMNI_CONV_FPROP || op == OMNI_CONV_WGRAD, "conv: unknown op %d", op);
@@ -1040,6 +1068,8 @@ long long omni_conv_implicit_plan(int precision, int op, int b, int n, int c, in
     const gemm::Plan pl = gemm::make_plan(N, M, K, omni::sm_count_cached(dev), bkt);
     return pl.splits > 1 ? (long long)pl.splits * M * N * 4 : 0;
   }
+  if (op == OMNI_CONV_FPROP && conv_fprop_transposed(d_out, M))
+    return omni_gemm_plan(precision, N, M, K, 0, 0, nullptr, nullptr);
   return omni_gemm_plan(precision, M, N, K, 0, 0, nullptr, nullptr);
 }
 
@@ -1063,6 +1093,12 @@ int omni_conv_implicit_f32(int precision, int op, const float* X, int b, int n, 
   OMNI_REQUIRE(epilogue != OMNI_EPI_MASK_AUX || (aux && ld_aux >= N), "conv: mask epilogue needs aux");
   gemm::ConvGeom cg{X, b, n, c, cs, k, stride, pad, m};
   cudaStream_t st = omni::as_stream(stream);
+  if (op == OMNI_CONV_FPROP && conv_fprop_transposed(d_out, M))
+    // few output channels: C^T = W im2col^T, im2col as the K-major B operand in
+    // 256-pixel boxes (48 KB per 512 MMA cycles instead of 28 KB per 192 with
+    // 128 x d_out tiles); epilogue stores C^T back into NHWC rows
+    return gemm::run_gemm(precision, N, M, K, G, ldg, 0, nullptr, 0, 0, Y, ldy, epilogue, bias, aux,
+                          ld_aux, workspace, ws_bytes, st, &cg, 4);
   if (op == OMNI_CONV_FPROP)   // A = im2col(X) (K-major), B = G weights (d_out x ldg, K-major)
     return gemm::run_gemm(precision, M, N, K, nullptr, 0, 0, G, ldg, 0, Y, ldy, epilogue, bias, aux,
                           ld_aux, workspace, ws_bytes, st, &cg, 1);

@@ -405,3 +405,58 @@ def test_space_to_depth_conv_equals_strided_conv(geom):
     K.conv_weight_s2d(dW, d, c, k, s, cp, dWt, ld, inverse=True)
     torch.cuda.synchronize()
     assert rel_err(dW.cpu(), Wd.grad) < 5e-6 * max(1.0, (b * m * m / 1000) ** 0.5)
+
+
+@pytest.mark.parametrize("epi", ["store", "bias_relu", "mask"])
+def test_conv_implicit_fprop_transposed_form(epi, monkeypatch):
+    """Few output channels and many pixels select the C^T = W im2col^T form
+    (im2col as the K-major B operand, transposed epilogue); it must equal the
+    standard form, epilogues included (bias by row, mask read transposed)."""
+    b, n, c, k, s, p, d = 32, 27, 96, 5, 1, 2, 96
+    X, W = _conv_inputs(b, n, c, k, d, 31)
+    m = n
+    ld = K.round_up(c * k * k, 32)
+    Wt = torch.zeros(d, ld, device=DEV)
+    K.conv_weight_to_tap(W, d, c, k, Wt, ld)
+    bias = torch.randn(d, device=DEV)
+    aux = torch.randn(b * m * m, d, device=DEV)
+    code = {"store": _abi.EPI_STORE, "bias_relu": _abi.EPI_BIAS_RELU, "mask": _abi.EPI_MASK_AUX}[epi]
+    outs = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("OMNI_NO_TRANSPOSED_FPROP", env)
+        Y = torch.full((b * m * m, d), float("nan"), device=DEV)
+        K.conv_implicit(_abi.CONV_FPROP, X, c, k, s, p, d, Wt, ld, Y, d, precision=_abi.PREC_3XTF32,
+                        epilogue=code, bias=bias, aux=aux, ld_aux=d)
+        torch.cuda.synchronize()
+        outs.append(Y.cpu())
+    # (the env switch is read once per process, so the second call may still be
+    # transposed; compare both against torch instead)
+    ref = torch.nn.functional.conv2d(X.permute(0, 3, 1, 2).double().cpu(), W.double().cpu(),
+                                     padding=p).permute(0, 2, 3, 1).reshape(-1, d)
+    if epi == "bias_relu":
+        ref = (ref + bias.double().cpu()).clamp_min(0)
+    elif epi == "mask":
+        ref = ref * (aux.double().cpu() > 0)
+    for Y in outs:
+        assert rel_err(Y, ref) < 5e-6 * max(1.0, (c * k * k / 1000) ** 0.5)
+
+
+def test_space_to_depth_conv1_transposed_batch():
+    """CaffeNet conv1 at a batch large enough for the transposed implicit form."""
+    b, n, c, k, s, d = 8, 227, 3, 11, 4, 96
+    gen = torch.Generator().manual_seed(41)
+    X = torch.randn(b, n, n, c, generator=gen).to(DEV)
+    W = (torch.randn(d, c, k, k, generator=gen) / (c * k * k) ** 0.5).to(DEV)
+    m = (n - k) // s + 1
+    k2, n2, cp = 3, 57, 64
+    Y = torch.empty(b, n2, n2, cp, device=DEV)
+    K.space_to_depth(X, c, s, Y)
+    ld = K.round_up(k2 * k2 * cp, 32)
+    Wt = torch.empty(d, ld, device=DEV)
+    K.conv_weight_s2d(W, d, c, k, s, cp, Wt, ld)
+    out = torch.empty(b * m * m, d, device=DEV)
+    K.conv_implicit(_abi.CONV_FPROP, Y, cp, k2, 1, 0, d, Wt, ld, out, d, precision=_abi.PREC_3XTF32)
+    ref = torch.nn.functional.conv2d(X.permute(0, 3, 1, 2).double().cpu(), W.double().cpu(), stride=s)
+    torch.cuda.synchronize()
+    assert rel_err(out.cpu(), ref.permute(0, 2, 3, 1).reshape(-1, d)) < 5e-6
