@@ -1029,9 +1029,13 @@ int omni_gemm_f32(int precision, int M, int N, int K, const float* A, long long 
                         epilogue, bias, aux, ld_aux, workspace, ws_bytes, st, nullptr, 0);
 }
 
-static bool conv_fprop_transposed(int d_out, int pixels) {
+// The transposed form trades 128 x d_out tiles for 128-row weight tiles against
+// 256-pixel im2col boxes; its C^T epilogue store only pays off over a long
+// reduction (conv2's data gradient: K = 6400 -> 615 TFLOP/s; CaffeNet conv1,
+// K = 576, is faster untransposed).
+static bool conv_fprop_transposed(int d_out, int pixels, int K) {
   static const bool off = getenv("OMNI_NO_TRANSPOSED_FPROP") != nullptr;
-  return !off && d_out <= 128 && pixels >= 128 * 148;
+  return !off && d_out <= 128 && pixels >= 128 * 148 && K >= 2048;
 }
 
 static int conv_shape(int op, int b, int n, int c, int k, int stride, int pad, int d_out, int* M,
@@ -1068,7 +1072,7 @@ long long omni_conv_implicit_plan(int precision, int op, int b, int n, int c, in
     const gemm::Plan pl = gemm::make_plan(N, M, K, omni::sm_count_cached(dev), bkt);
     return pl.splits > 1 ? (long long)pl.splits * M * N * 4 : 0;
   }
-  if (op == OMNI_CONV_FPROP && conv_fprop_transposed(d_out, M))
+  if (op == OMNI_CONV_FPROP && conv_fprop_transposed(d_out, M, K))
     return omni_gemm_plan(precision, N, M, K, 0, 0, nullptr, nullptr);
   return omni_gemm_plan(precision, M, N, K, 0, 0, nullptr, nullptr);
 }
@@ -1093,7 +1097,7 @@ int omni_conv_implicit_f32(int precision, int op, const float* X, int b, int n, 
   OMNI_REQUIRE(epilogue != OMNI_EPI_MASK_AUX || (aux && ld_aux >= N), "conv: mask epilogue needs aux");
   gemm::ConvGeom cg{X, b, n, c, cs, k, stride, pad, m};
   cudaStream_t st = omni::as_stream(stream);
-  if (op == OMNI_CONV_FPROP && conv_fprop_transposed(d_out, M))
+  if (op == OMNI_CONV_FPROP && conv_fprop_transposed(d_out, M, K))
     // few output channels: C^T = W im2col^T, im2col as the K-major B operand in
     // 256-pixel boxes (48 KB per 512 MMA cycles instead of 28 KB per 192 with
     // 128 x d_out tiles); epilogue stores C^T back into NHWC rows

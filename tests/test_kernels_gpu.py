@@ -442,8 +442,8 @@ def test_conv_implicit_fprop_transposed_form(epi, monkeypatch):
         assert rel_err(Y, ref) < 5e-6 * max(1.0, (c * k * k / 1000) ** 0.5)
 
 
-def test_space_to_depth_conv1_transposed_batch():
-    """CaffeNet conv1 at a batch large enough for the transposed implicit form."""
+def test_space_to_depth_conv1_large_batch():
+    """CaffeNet conv1 geometry at a batch where the implicit GEMM spans all SMs."""
     b, n, c, k, s, d = 8, 227, 3, 11, 4, 96
     gen = torch.Generator().manual_seed(41)
     X = torch.randn(b, n, n, c, generator=gen).to(DEV)
