@@ -24,10 +24,11 @@ __host__ __device__ inline int pool_out(int n, int k, int s, int p, int ceil_mod
 // One thread per (img, oy, ox, channel group of V).  Max: first maximum in
 // (dy, dx) order, argmax = iy*w + ix (problems.py:213-216).  Avg: Caffe
 // divisor.  V = 4 uses float4/int4 accesses (c, cs_in, cs_out multiples of 4).
-template <int MODE, int V>
+template <int MODE, int V, int KS = 0>
 __global__ void __launch_bounds__(kThreads) pool_fwd_kernel(
-    const float* __restrict__ X, int b, int h, int w, int c, int cs_in, int k, int s, int p,
+    const float* __restrict__ X, int b, int h, int w, int c, int cs_in, int k_rt, int s, int p,
     int oh, int ow, float* __restrict__ Y, int cs_out, int32_t* __restrict__ argmax) {
+  const int k = KS ? KS : k_rt;   // KS > 0: fully unrolled window, all loads in flight
   const int cv = c / V;
   const int total = b * oh * ow * cv;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
@@ -53,29 +54,35 @@ __global__ void __launch_bounds__(kThreads) pool_fwd_kernel(
       arg[v] = hs * w + ws;
     }
     bool first = true;
-    for (int iy = hs; iy < he; ++iy)
-      for (int ix = ws; ix < we; ++ix) {
-        const float* src = Xi + (iy * w + ix) * cs_in;
-        float val[V];
-        if (V == 4) {
-          const float4 t = __ldg(reinterpret_cast<const float4*>(src));
-          val[0] = t.x; val[1] = t.y; val[2 % V] = t.z; val[3 % V] = t.w;
-        } else {
-          val[0] = __ldg(src);
-        }
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          if (MODE == 0) {
-            if (first || val[v] > best[v]) {
-              best[v] = val[v];
-              arg[v] = iy * w + ix;
+    for (int dy = 0; dy < (KS ? KS : 1); ++dy) {
+      for (int iy = (KS ? hs + dy : hs); iy < (KS ? min(hs + dy + 1, he) : he); ++iy)
+#pragma unroll
+        for (int dx = 0; dx < (KS ? KS : 1); ++dx) {
+          for (int ix = (KS ? ws + dx : ws); ix < (KS ? min(ws + dx + 1, we) : we); ++ix) {
+            const float* src = Xi + (iy * w + ix) * cs_in;
+            float val[V];
+            if (V == 4) {
+              const float4 t = __ldg(reinterpret_cast<const float4*>(src));
+              val[0] = t.x; val[1 % V] = t.y; val[2 % V] = t.z; val[3 % V] = t.w;
+            } else {
+              val[0] = __ldg(src);
             }
-          } else {
-            acc[v] += val[v];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              if (MODE == 0) {
+                if (first || val[v] > best[v]) {
+                  best[v] = val[v];
+                  arg[v] = iy * w + ix;
+                }
+              } else {
+                acc[v] += val[v];
+              }
+            }
+            first = false;
           }
         }
-        first = false;
-      }
+    }
     float* dst = Y + (long long)opix * cs_out + ch;
     if (MODE == 0) {
       if (V == 4) {
@@ -202,8 +209,14 @@ __global__ void __launch_bounds__(kThreads) pool_bwd_s2_kernel(
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[a][e][v] = 0.f;
     const int obase = img * oh * ow;
-    for (int oy = oy0; oy < oy1; ++oy)
-      for (int ox = ox0; ox < ox1; ++ox) {
+    // k <= 4 at stride 2: at most 2 x 2 windows cover an aligned 2x2 block, so
+    // iterate a fixed, unrolled candidate set (loads of all windows in flight)
+#pragma unroll
+    for (int ty = 0; ty < 2; ++ty)
+#pragma unroll
+      for (int tx = 0; tx < 2; ++tx) {
+        const int oy = oy0 + ty, ox = ox0 + tx;
+        if (oy >= oy1 || ox >= ox1) continue;
         const int o = obase + oy * ow + ox;
         const float4 g = __ldg(reinterpret_cast<const float4*>(dY + (long long)o * cs_out + ch));
         const float gv[4] = {g.x, g.y, g.z, g.w};
@@ -488,12 +501,16 @@ int omni_pool_fwd_nhwc_f32(int mode, const float* X, int b, int h, int w, int c,
   const bool v4 = c % 4 == 0 && cs_in % 4 == 0 && cs_out % 4 == 0 && aligned16(X) && aligned16(Y) &&
                   (mode == 1 || aligned16(argmax));
   const int grid = omni::grid_for(v4 ? work / 4 : work, kThreads);
-#define OMNI_POOL_FWD(M, V) \
-  pool_fwd_kernel<M, V><<<grid, kThreads, 0, st>>>(X, b, h, w, c, cs_in, k, stride, pad, oh, ow, Y, cs_out, argmax)
+#define OMNI_POOL_FWD(M, V, KS) \
+  pool_fwd_kernel<M, V, KS><<<grid, kThreads, 0, st>>>(X, b, h, w, c, cs_in, k, stride, pad, oh, ow, Y, cs_out, argmax)
   if (mode == 0) {
-    if (v4) OMNI_POOL_FWD(0, 4); else OMNI_POOL_FWD(0, 1);
+    if (v4 && k == 3) OMNI_POOL_FWD(0, 4, 3);
+    else if (v4) OMNI_POOL_FWD(0, 4, 0);
+    else OMNI_POOL_FWD(0, 1, 0);
   } else {
-    if (v4) OMNI_POOL_FWD(1, 4); else OMNI_POOL_FWD(1, 1);
+    if (v4 && k == 3) OMNI_POOL_FWD(1, 4, 3);
+    else if (v4) OMNI_POOL_FWD(1, 4, 0);
+    else OMNI_POOL_FWD(1, 1, 0);
   }
 #undef OMNI_POOL_FWD
   return omni::check_launch("pool_fwd");
@@ -515,7 +532,7 @@ int omni_pool_bwd_nhwc_f32(int mode, const float* dY, int b, int h, int w, int c
   cudaStream_t st = omni::as_stream(stream);
   const bool v4 = c % 4 == 0 && cs_in % 4 == 0 && cs_out % 4 == 0 && aligned16(dY) && aligned16(dX) &&
                   (mode == 1 || aligned16(argmax)) && (!relu_mask_x || aligned16(X));
-  if (v4 && stride == 2 && !getenv("OMNI_POOL_BWD_PIXEL")) {
+  if (v4 && stride == 2 && k <= 4 && !getenv("OMNI_POOL_BWD_PIXEL")) {
     const long long blocks = (long long)b * ((h + 1) / 2) * ((w + 1) / 2) * (c / 4);
     const int g2 = omni::grid_for(blocks, kThreads);
     if (mode == 0)
