@@ -211,8 +211,7 @@ class GpuNet:
         # workspaces sized for the largest GEMM / bias reduction
         ws, bws, dd = 0, 0, 0
         for op in self.ops:
-            for M, N, Kd in self._gemm_shapes(op, self.b):
-                ws = max(ws, K.gemm_workspace_bytes(self.prec, M, N, Kd, False, False))
+            ws = max(ws, self._workspace_need(op, self.b))
             if op.kind == "fc" and op.boff >= 0:
                 bws = max(bws, K.bias_grad_ws_elems(self.b, op.layer.d_out))
             if op.kind == "conv" and op.implicit and op.boff >= 0:
@@ -230,6 +229,26 @@ class GpuNet:
         self.overlap = True  # False: weight gradients on the main stream (isolated kernel timing)
 
     # ------------------------------------------------------------ shapes --
+    def _workspace_need(self, op: Op, b: int) -> int:
+        """Largest split-K workspace any GEMM of this layer asks for, from the
+        same plan functions the launches use (implicit convs plan differently
+        from plain GEMMs: 64-deep wgrad stages, transposed fprop)."""
+        if op.kind == "conv" and op.implicit:
+            d = op.layer.d_out
+            if op.s2d is not None:
+                st, k2, p2, n2, cp = op.s2d
+                geo = (b, n2, cp, k2, 1, p2, d)
+            else:
+                geo = (b, op.inp.n, op.c_in, op.k, op.s, op.p, d)
+            need = max(K.conv_implicit_workspace_bytes(self.prec, _abi.CONV_FPROP, *geo),
+                       K.conv_implicit_workspace_bytes(self.prec, _abi.CONV_WGRAD, *geo))
+            if not op.first_param_layer:
+                need = max(need, K.conv_implicit_workspace_bytes(
+                    self.prec, _abi.CONV_FPROP, b, op.m, d, op.k, 1, op.k - 1 - op.p, op.c_in))
+            return need
+        return max([K.gemm_workspace_bytes(self.prec, M, N, Kd, False, False)
+                    for M, N, Kd in self._gemm_shapes(op, b)] or [0])
+
     @staticmethod
     def _gemm_shapes(op: Op, b: int):
         if op.kind == "conv":

@@ -109,6 +109,22 @@ def _workspace(nbytes: int, device: torch.device) -> torch.Tensor | None:
     return ws
 
 
+def _check_workspace(need: int, workspace: torch.Tensor | None, device) -> torch.Tensor | None:
+    """A caller-owned workspace must be big enough (engines size theirs per
+    launch; sharing a fallback buffer across streams or CUDA graphs would
+    race).  Without one, standalone calls use a per-device cache."""
+    if need <= 0:
+        return workspace
+    if workspace is not None:
+        if workspace.numel() * 4 < need:
+            raise RuntimeError(f"split-K workspace of {need} bytes needed, "
+                               f"{workspace.numel() * 4} given")
+        return workspace
+    if torch.cuda.is_current_stream_capturing():
+        raise RuntimeError("split-K GEMM inside CUDA graph capture needs an explicit workspace")
+    return _workspace(need, device)
+
+
 def gemm(M: int, N: int, K: int, A: torch.Tensor, lda: int, a_mn: bool, B: torch.Tensor,
          ldb: int, b_mn: bool, C: torch.Tensor, ldc: int, *, precision: int = _abi.PREC_TF32,
          epilogue: int = _abi.EPI_STORE, bias: torch.Tensor | None = None,
@@ -117,8 +133,7 @@ def gemm(M: int, N: int, K: int, A: torch.Tensor, lda: int, a_mn: bool, B: torch
     """C[i,j] (op)= sum_r A(i,r) B(j,r) on tcgen05 (see include/omni.h for the operand maps)."""
     _require_cuda(A, B, C)
     need = gemm_workspace_bytes(precision, M, N, K, a_mn, b_mn)
-    if need > 0 and (workspace is None or workspace.numel() * 4 < need):
-        workspace = _workspace(need, C.device)
+    workspace = _check_workspace(need, workspace, C.device)
     call("omni_gemm_f32", precision, M, N, K, _ptr(A), lda, int(a_mn), _ptr(B), ldb, int(b_mn),
          _ptr(C), ldc, epilogue, _ptr(bias), _ptr(aux), ld_aux, _ptr(workspace),
          0 if workspace is None else workspace.numel() * 4, _stream())
@@ -163,8 +178,7 @@ def conv_implicit(op: int, X: torch.Tensor, c: int, k: int, stride: int, pad: in
     _require_cuda(X, G, Y)
     b, n, _, cs = X.shape
     need = conv_implicit_workspace_bytes(precision, op, b, n, c, k, stride, pad, d_out)
-    if need > 0 and (workspace is None or workspace.numel() * 4 < need):
-        workspace = _workspace(need, Y.device)
+    workspace = _check_workspace(need, workspace, Y.device)
     call("omni_conv_implicit_f32", precision, op, _ptr(X), b, n, c, cs, k, stride, pad, d_out,
          _ptr(G), ldg, _ptr(Y), ldy, epilogue, _ptr(bias), _ptr(aux), ld_aux, _ptr(workspace),
          0 if workspace is None else workspace.numel() * 4, _stream())
