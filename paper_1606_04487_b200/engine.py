@@ -27,6 +27,7 @@ CUDA graph (``capture``).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -226,7 +227,8 @@ class GpuNet:
         self.ddhat = z(max(dd, 4))
         self.graph = None
         self.timer = None   # list -> (M, N, K, kind, ev0, ev1) per GEMM launch
-        self.overlap = True  # False: weight gradients on the main stream (isolated kernel timing)
+        # False: weight gradients on the main stream (isolated kernel timing / debugging)
+        self.overlap = not os.environ.get("OMNI_NO_SIDE_STREAM")
 
     # ------------------------------------------------------------ shapes --
     def _workspace_need(self, op: Op, b: int) -> int:

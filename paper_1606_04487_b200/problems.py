@@ -15,6 +15,7 @@ losses and gradients can be compared with the reference on identical inputs.
 
 from __future__ import annotations
 
+import os
 from typing import Any
 
 import numpy as np
@@ -115,7 +116,7 @@ class DeviceSession:
         # CUDA graph of a whole single-GPU step on device-resident batches:
         # captured on the second such step (the first eager one does all lazy
         # setup), replayed with the batch indices copied into a static buffer.
-        self.use_graph = use_graph
+        self.use_graph = use_graph and not os.environ.get("OMNI_NO_GRAPH")
         self._graphs: dict = {}
         self._seen: dict = {}
         self._gidx = None
