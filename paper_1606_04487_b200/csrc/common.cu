@@ -1,5 +1,7 @@
 // Status plumbing shared by every entry point of libomni.so.
 #include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include <mutex>
 
@@ -23,6 +25,17 @@ int check_launch(const char* what) {
   if (e != cudaSuccess) {
     set_error("%s: launch failed: %s", what, cudaGetErrorString(e));
     return OMNI_ECUDA;
+  }
+  // OMNI_DEBUG_SYNC=1: wait for every launch and name the kernel that faulted
+  // (debugging aid; never set in production or inside graph capture)
+  static const bool debug_sync = getenv("OMNI_DEBUG_SYNC") != nullptr;
+  if (debug_sync) {
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      fprintf(stderr, "[omni] %s: kernel failed: %s\n", what, cudaGetErrorString(e));
+      set_error("%s: kernel failed: %s", what, cudaGetErrorString(e));
+      return OMNI_ECUDA;
+    }
   }
   return OMNI_OK;
 }

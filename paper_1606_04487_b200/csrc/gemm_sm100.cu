@@ -225,13 +225,17 @@ __device__ __forceinline__ void decode_work(const Params& p, int w, int& mt, int
 template <int MODE>
 __device__ __forceinline__ float epi_one(float acc, const Params& p, int row, int col,
                                          const float* Crow) {
+  // The TMA-store epilogue evaluates whole 32 x 32 sub-tiles and lets the
+  // tensor map clip the store at the M/N edges, so operand reads of
+  // out-of-range elements must be masked here (the value is discarded).
+  const bool in = row < p.M && col < p.N;
   const int bi = p.transpose_c ? row : col;
-  if (MODE == OMNI_EPI_BIAS) return acc + __ldg(p.bias + bi);
-  if (MODE == OMNI_EPI_BIAS_RELU) return fmaxf(acc + __ldg(p.bias + bi), 0.f);
+  if (MODE == OMNI_EPI_BIAS) return acc + (in ? __ldg(p.bias + bi) : 0.f);
+  if (MODE == OMNI_EPI_BIAS_RELU) return fmaxf(acc + (in ? __ldg(p.bias + bi) : 0.f), 0.f);
   if (MODE == OMNI_EPI_ACCUM) return Crow[col] + acc;
   if (MODE == OMNI_EPI_MASK_AUX) {
     const long long ai = p.transpose_c ? (long long)col * p.ld_aux + row : (long long)row * p.ld_aux + col;
-    return __ldg(p.aux + ai) > 0.f ? acc : 0.f;
+    return (in && __ldg(p.aux + ai) > 0.f) ? acc : 0.f;
   }
   if (MODE == OMNI_EPI_RELU) return fmaxf(acc, 0.f);
   return acc;

@@ -14,7 +14,11 @@ from ._abi import call, query
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
-    return None if t is None else t.data_ptr()
+    if t is None:
+        return None
+    if not t.is_cuda:   # a host pointer would be dereferenced by the kernel (HMM/UVA)
+        raise ValueError(f"libomni kernels take CUDA tensors (got {t.device}, shape {tuple(t.shape)})")
+    return t.data_ptr()
 
 
 def _stream() -> int:
@@ -25,6 +29,15 @@ def _require_cuda(*ts: torch.Tensor) -> None:
     for t in ts:
         if t is not None and not t.is_cuda:
             raise ValueError("libomni kernels take CUDA tensors")
+
+
+def _fits(t: torch.Tensor, need: int, name: str) -> None:
+    """The kernels address operands as (pointer, ld): the storage behind the
+    pointer must hold the whole strided extent, or a launch reads/writes past
+    the allocation."""
+    have = t.untyped_storage().nbytes() // t.element_size() - t.storage_offset()
+    if need > have:
+        raise ValueError(f"operand {name}: extent of {need} elements, only {have} behind the pointer")
 
 
 def round_up(x: int, m: int) -> int:
@@ -132,6 +145,14 @@ def gemm(M: int, N: int, K: int, A: torch.Tensor, lda: int, a_mn: bool, B: torch
          workspace: torch.Tensor | None = None) -> torch.Tensor:
     """C[i,j] (op)= sum_r A(i,r) B(j,r) on tcgen05 (see include/omni.h for the operand maps)."""
     _require_cuda(A, B, C)
+    if M > 0 and N > 0 and K > 0:
+        _fits(A, (K - 1) * lda + M if a_mn else (M - 1) * lda + K, "A")
+        _fits(B, (K - 1) * ldb + N if b_mn else (N - 1) * ldb + K, "B")
+        _fits(C, (M - 1) * ldc + N, "C")
+        if aux is not None:
+            _fits(aux, (M - 1) * ld_aux + N, "aux")
+        if bias is not None:
+            _fits(bias, N, "bias")
     need = gemm_workspace_bytes(precision, M, N, K, a_mn, b_mn)
     workspace = _check_workspace(need, workspace, C.device)
     call("omni_gemm_f32", precision, M, N, K, _ptr(A), lda, int(a_mn), _ptr(B), ldb, int(b_mn),
