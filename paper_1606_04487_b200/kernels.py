@@ -198,6 +198,19 @@ def conv_implicit(op: int, X: torch.Tensor, c: int, k: int, stride: int, pad: in
     (b, n, n, cs); op = _abi.CONV_FPROP or _abi.CONV_WGRAD."""
     _require_cuda(X, G, Y)
     b, n, _, cs = X.shape
+    m = (n + 2 * pad - k) // stride + 1
+    pixels, taps = b * m * m, k * k * c
+    _fits(X, (b * n * n - 1) * cs + c, "X")
+    if op == _abi.CONV_FPROP:   # G: d_out x ldg (tap-major weights), Y: pixels x ldy
+        _fits(G, (d_out - 1) * ldg + taps, "G")
+        _fits(Y, (pixels - 1) * ldy + d_out, "Y")
+        if aux is not None:
+            _fits(aux, (pixels - 1) * ld_aux + d_out, "aux")
+    else:                       # G: dY, pixels x ldg; Y: dW, d_out x ldy
+        _fits(G, (pixels - 1) * ldg + d_out, "G")
+        _fits(Y, (d_out - 1) * ldy + taps, "Y")
+    if bias is not None:
+        _fits(bias, d_out, "bias")
     need = conv_implicit_workspace_bytes(precision, op, b, n, c, k, stride, pad, d_out)
     workspace = _check_workspace(need, workspace, Y.device)
     call("omni_conv_implicit_f32", precision, op, _ptr(X), b, n, c, cs, k, stride, pad, d_out,

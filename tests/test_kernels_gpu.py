@@ -89,6 +89,41 @@ def test_gemm_epilogues(epi):
     assert rel_err(C.cpu(), ref) < 2e-6
 
 
+@pytest.mark.parametrize("epi", ["bias_relu", "mask"])
+def test_gemm_epilogue_operands_read_in_bounds(epi):
+    """Small-M GEMM whose bias/aux operands end exactly at the end of a
+    segment-sized allocation: the TMA-store epilogue computes whole 32x32
+    sub-tiles (128 rows per tile), so any read of rows >= M or columns >= N
+    would land past the segment (regression: LeNet FC dgrad, M = 16)."""
+    M, N, Kd = 16, 40, 64
+    gen = torch.Generator().manual_seed(9)
+    A, lda, Al = make_operand(M, Kd, False, gen)
+    B, ldb, Bl = make_operand(N, Kd, False, gen)
+    seg = 8 << 20   # 32 MiB of fp32: a dedicated, 2 MiB-rounded cudaMalloc segment
+    big = torch.empty(seg, device=DEV)
+    aux = big[seg - M * N:].view(M, N)
+    aux.copy_(torch.randn(M, N, generator=gen).to(DEV))
+    big2 = torch.empty(seg, device=DEV)
+    bias = big2[seg - N:]
+    bias.copy_(torch.randn(N, generator=gen).to(DEV))
+    C = torch.empty(M, N, device=DEV)
+    code = _abi.EPI_BIAS_RELU if epi == "bias_relu" else _abi.EPI_MASK_AUX
+    K.gemm(M, N, Kd, A, lda, False, B, ldb, False, C, N, precision=_abi.PREC_3XTF32,
+           epilogue=code, bias=bias, aux=aux, ld_aux=N)
+    torch.cuda.synchronize()
+    acc = Al @ Bl.t()
+    ref = (acc + bias.cpu().double()).clamp_min(0) if epi == "bias_relu" else \
+        acc * (aux.cpu().double() > 0)
+    assert rel_err(C.cpu(), ref) < 2e-6
+
+
+def test_gemm_operand_extent_checked():
+    A = torch.zeros(8, 8, device=DEV)
+    C = torch.zeros(8, 8, device=DEV)
+    with pytest.raises(ValueError, match="extent"):
+        K.gemm(16, 8, 8, A, 8, False, A, 8, False, C, 8)   # A holds 8 rows, not 16
+
+
 def test_gemm_simt_reference():
     M, N, Kd = 70, 50, 40
     gen = torch.Generator().manual_seed(1)
