@@ -209,8 +209,8 @@ __global__ void __launch_bounds__(kThreads) pool_bwd_s2_kernel(
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[a][e][v] = 0.f;
     const int obase = img * oh * ow;
-    // k <= 4 at stride 2: at most 2 x 2 windows cover an aligned 2x2 block, so
-    // iterate a fixed, unrolled candidate set (loads of all windows in flight)
+    // at stride 2 with k <= 3 (or k = 4, even pad) at most 2 x 2 windows cover an
+    // aligned 2x2 block: iterate a fixed, unrolled candidate set (all loads in flight)
 #pragma unroll
     for (int ty = 0; ty < 2; ++ty)
 #pragma unroll
@@ -532,7 +532,10 @@ int omni_pool_bwd_nhwc_f32(int mode, const float* dY, int b, int h, int w, int c
   cudaStream_t st = omni::as_stream(stream);
   const bool v4 = c % 4 == 0 && cs_in % 4 == 0 && cs_out % 4 == 0 && aligned16(dY) && aligned16(dX) &&
                   (mode == 1 || aligned16(argmax)) && (!relu_mask_x || aligned16(X));
-  if (v4 && stride == 2 && k <= 4 && !getenv("OMNI_POOL_BWD_PIXEL")) {
+  // the blocked kernel visits 2 x 2 candidate windows per aligned 2x2 input
+  // block: enough for k <= 3, and for k = 4 only with even padding (odd
+  // padding puts a third window over the block)
+  if (v4 && stride == 2 && (k <= 3 || (k == 4 && pad % 2 == 0)) && !getenv("OMNI_POOL_BWD_PIXEL")) {
     const long long blocks = (long long)b * ((h + 1) / 2) * ((w + 1) / 2) * (c / 4);
     const int g2 = omni::grid_for(blocks, kThreads);
     if (mode == 0)

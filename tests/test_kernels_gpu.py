@@ -210,7 +210,11 @@ def test_lift_bit_exact():
 
 @pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("geom", [(2, 8, 8, 3, 2, 2, 0, True), (2, 55, 55, 5, 3, 2, 0, True),
-                                  (3, 32, 32, 4, 3, 2, 0, True), (1, 7, 7, 4, 3, 2, 1, True)])
+                                  (3, 32, 32, 4, 3, 2, 0, True), (1, 7, 7, 4, 3, 2, 1, True),
+                                  # stride-2 blocked backward: k=4 with odd pad has 3 covering
+                                  # windows per axis (must take the per-pixel kernel)
+                                  (2, 9, 9, 8, 4, 2, 1, True), (2, 8, 8, 8, 4, 2, 0, False),
+                                  (2, 9, 9, 8, 3, 2, 1, False), (2, 8, 8, 8, 2, 2, 0, False)])
 def test_pool_fwd_bwd(mode, geom):
     b, h, w, c, k, s, p, ceil_mode = geom
     gen = torch.Generator().manual_seed(3)
