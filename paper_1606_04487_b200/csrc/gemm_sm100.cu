@@ -55,10 +55,13 @@ struct Params {
   int transpose_c;  // store C^T: C[j*ldc + i] (weight gradient with im2col as the A operand)
 };
 
-template <int BN, bool SPLIT3, int BKT = BK>
+// CTA2: the tile is computed by a CTA pair (cluster of 2, tcgen05 cta_group::2,
+// M = 256): each CTA stages its own 128 rows of A and half (BN/2) of B.
+template <int BN, bool SPLIT3, int BKT = BK, bool CTA2 = false>
 struct Layout {
+  static constexpr int BNL = CTA2 ? BN / 2 : BN;  // B rows staged by this CTA
   static constexpr int A_BYTES = BM * BKT * 4;
-  static constexpr int B_BYTES = BN * BKT * 4;
+  static constexpr int B_BYTES = BNL * BKT * 4;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGE_ALL = SPLIT3 ? 2 * STAGE : STAGE;
   static constexpr int STG_BYTES = 4 * 2 * 32 * 32 * 4;  // 4 epilogue warps x 2 x (32x32 fp32)
@@ -169,6 +172,75 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t adesc, uin
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// ---- CTA-pair (cta_group::2) variants ----
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
+}
+// shared::cluster address of the same shared-memory offset in CTA 0 of the pair
+__device__ __forceinline__ uint32_t mapa_rank0(uint32_t addr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(addr));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAITC:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONEC;\n\t"
+      "bra LAB_WAITC;\n\t"
+      "DONEC:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// TMA loads whose completion is signalled on CTA 0's barrier (bar is a
+// shared::cluster address); data lands in the issuing CTA's shared memory.
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t dst, uint32_t bar,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_im2col_pair(const CUtensorMap* map, uint32_t dst,
+                                                     uint32_t bar, int c, int w, int h, int n,
+                                                     uint16_t ow, uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.im2col.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow),
+      "h"(oh)
+      : "memory");
+}
+// commit to the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                                 uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -200,11 +272,11 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
          (layout << 61);
 }
 
-// Instruction descriptor: D=f32, A=B=tf32, majors, N>>3, M>>4.
-template <int BN, bool A_MN, bool B_MN>
+// Instruction descriptor: D=f32, A=B=tf32, majors, N>>3, M>>4 (M = 256 for a CTA pair).
+template <int BN, bool A_MN, bool B_MN, int MM = BM>
 __host__ __device__ constexpr uint32_t instr_desc() {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
-         ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+         ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(MM >> 4) << 24);
 }
 
 __device__ __forceinline__ void decode_work(const Params& p, int w, int& mt, int& nt, int& sp) {
@@ -274,15 +346,18 @@ __device__ __forceinline__ void epi_chunk(int mode, float (&v)[N], const uint32_
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, bool SPLIT3, int IM2COL, int BKT>
-__global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
+template <int BN, bool A_MN, bool B_MN, bool SPLIT3, int IM2COL, int BKT, bool CTA2>
+__global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const Params p) {
   // K-major operands hold exactly one 128-byte swizzle row (32 fp32) per stage;
   // deeper stages are for MN-major operands only.
   static_assert(BKT == BK || (A_MN && B_MN), "BKT > 32 needs MN-major operands");
-  using L = Layout<BN, SPLIT3, BKT>;
+  static_assert(!(CTA2 && SPLIT3), "the CTA-pair kernel is TF32 only");
+  using L = Layout<BN, SPLIT3, BKT, CTA2>;
+  constexpr int BM_T = CTA2 ? 2 * BM : BM;  // output rows per work tile
+  constexpr int BNL = L::BNL;               // B rows this CTA stages
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
@@ -296,6 +371,10 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::BAR_OFF + 8 * 28);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // CTA pair: rank 0 issues the MMAs for both; work units go to pairs
+  const int rank = CTA2 ? (int)cluster_ctarank() : 0;
+  const int unit0 = CTA2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int units = CTA2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -308,19 +387,28 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), 128);
+      mbar_init(tempty_bar(a), CTA2 ? 8 : 128);  // pair: one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_holder)),
-                 "n"(L::TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (CTA2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_holder)),
+                   "n"(L::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_holder)),
+                   "n"(L::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (CTA2) cluster_sync();  // peer barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -331,22 +419,24 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
       // ---------------------------------------------------- TMA producer --
       int stage = 0;
       uint32_t phase = 0;
-      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      for (int w = unit0; w < total; w += units) {
         int mt, nt, sp;
         decode_work(p, w, mt, nt, sp);
         const int kt0 = sp * p.kt_per_split;
         const int kt1 = min(p.k_tiles, kt0 + p.kt_per_split);
+        const int arow = mt * BM_T + rank * BM;  // first A row / B column this CTA stages
+        const int bcol = nt * BN + rank * BNL;
         // im2col A (or B): window corner of this tile's first output pixel
         int a_img = 0, a_h0 = 0, a_w0 = 0, b_img = 0, b_h0 = 0, b_w0 = 0;
         if (IM2COL == 1) {
-          const int m0 = mt * BM;
+          const int m0 = arow;
           a_img = m0 / p.conv_mm;
           const int r = m0 - a_img * p.conv_mm;
           a_h0 = (r / p.conv_m) * p.conv_s - p.conv_pad;
           a_w0 = (r - (r / p.conv_m) * p.conv_m) * p.conv_s - p.conv_pad;
         }
         if (IM2COL == 4) {
-          const int n0 = nt * BN;
+          const int n0 = bcol;
           b_img = n0 / p.conv_mm;
           const int r = n0 - b_img * p.conv_mm;
           b_h0 = (r / p.conv_m) * p.conv_s - p.conv_pad;
@@ -354,7 +444,17 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
         }
         for (int kt = kt0; kt < kt1; ++kt) {
           mbar_wait(empty_bar(stage), phase ^ 1);
-          mbar_expect_tx(full_bar(stage), (uint32_t)L::STAGE);
+          if (rank == 0) mbar_expect_tx(full_bar(stage), (uint32_t)(CTA2 ? 2 * L::STAGE : L::STAGE));
+          const uint32_t fb = CTA2 ? mapa_rank0(full_bar(stage)) : full_bar(stage);
+          auto load2d = [&](const CUtensorMap* map, uint32_t dst, int c0, int c1) {
+            if (CTA2) tma_load_2d_pair(map, dst, fb, c0, c1);
+            else tma_load_2d(map, dst, fb, c0, c1);
+          };
+          auto load_im2col = [&](const CUtensorMap* map, uint32_t dst, int c, int w_, int h_, int n_,
+                                 uint16_t ow, uint16_t oh) {
+            if (CTA2) tma_load_im2col_pair(map, dst, fb, c, w_, h_, n_, ow, oh);
+            else tma_load_im2col(map, dst, fb, c, w_, h_, n_, ow, oh);
+          };
           const uint32_t a_dst = sbase + stage * L::STAGE_ALL;
           const uint32_t b_dst = a_dst + L::A_BYTES;
           const int kc = kt * BKT;
@@ -362,8 +462,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
             // K index = (tap, channel): tap-major, 32-channel blocks
             const int cb = kt % p.conv_cblocks, tap = kt / p.conv_cblocks;
             const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
-            tma_load_im2col(&tmA, a_dst, full_bar(stage), cb * 32, a_w0, a_h0, a_img,
-                            (uint16_t)ky, (uint16_t)kx);
+            load_im2col(&tmA, a_dst, cb * 32, a_w0, a_h0, a_img, (uint16_t)ky, (uint16_t)kx);
           } else if (IM2COL == 3) {
             // A(i = (tap, ch), r = pixel): BK output pixels x 32 channels per 32-row chunk
             const int img = kc / p.conv_mm;
@@ -373,27 +472,26 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
             const int taps = p.conv_k * p.conv_k;
 #pragma unroll
             for (int j = 0; j < BM / 32; ++j) {
-              const int blk = mt * (BM / 32) + j;
+              const int blk = arow / 32 + j;
               int tap = blk / p.conv_cblocks;
               const int cb = blk - tap * p.conv_cblocks;
               if (tap >= taps) tap = taps - 1;  // rows past M: any valid load, discarded
               const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
-              tma_load_im2col(&tmA, a_dst + j * (BKT * 128), full_bar(stage), cb * 32, w0, h0, img,
-                              (uint16_t)ky, (uint16_t)kx);
+              load_im2col(&tmA, a_dst + j * (BKT * 128), cb * 32, w0, h0, img, (uint16_t)ky,
+                          (uint16_t)kx);
             }
           } else if (!A_MN) {
-            tma_load_2d(&tmA, a_dst, full_bar(stage), kc, mt * BM);
+            load2d(&tmA, a_dst, kc, arow);
           } else {
 #pragma unroll
             for (int j = 0; j < BM / 32; ++j)
-              tma_load_2d(&tmA, a_dst + j * (BKT * 128), full_bar(stage), mt * BM + 32 * j, kc);
+              load2d(&tmA, a_dst + j * (BKT * 128), arow + 32 * j, kc);
           }
           if (IM2COL == 4) {
             // B(j = pixel, r = (tap, ch)): BN output pixels x 32 channels, K-major
             const int cb = kt % p.conv_cblocks, tap = kt / p.conv_cblocks;
             const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
-            tma_load_im2col(&tmB, b_dst, full_bar(stage), cb * 32, b_w0, b_h0, b_img,
-                            (uint16_t)ky, (uint16_t)kx);
+            load_im2col(&tmB, b_dst, cb * 32, b_w0, b_h0, b_img, (uint16_t)ky, (uint16_t)kx);
           } else if (IM2COL == 2) {
             // B(j = (tap, ch), r = pixel): BK output pixels x 32 channels per chunk
             const int img = kc / p.conv_mm;
@@ -402,21 +500,21 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
             const int w0 = (r - (r / p.conv_m) * p.conv_m) * p.conv_s - p.conv_pad;
             const int taps = p.conv_k * p.conv_k;
 #pragma unroll
-            for (int j = 0; j < BN / 32; ++j) {
-              const int blk = nt * (BN / 32) + j;
+            for (int j = 0; j < BNL / 32; ++j) {
+              const int blk = bcol / 32 + j;
               int tap = blk / p.conv_cblocks;
               const int cb = blk - tap * p.conv_cblocks;
               if (tap >= taps) tap = taps - 1;  // columns past N: any valid load, discarded
               const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
-              tma_load_im2col(&tmB, b_dst + j * (BKT * 128), full_bar(stage), cb * 32, w0, h0, img,
-                              (uint16_t)ky, (uint16_t)kx);
+              load_im2col(&tmB, b_dst + j * (BKT * 128), cb * 32, w0, h0, img, (uint16_t)ky,
+                          (uint16_t)kx);
             }
           } else if (!B_MN) {
-            tma_load_2d(&tmB, b_dst, full_bar(stage), kc, nt * BN);
+            load2d(&tmB, b_dst, kc, bcol);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 32; ++j)
-              tma_load_2d(&tmB, b_dst + j * (BKT * 128), full_bar(stage), nt * BN + 32 * j, kc);
+            for (int j = 0; j < BNL / 32; ++j)
+              load2d(&tmB, b_dst + j * (BKT * 128), bcol + 32 * j, kc);
           }
           if (++stage == L::STAGES) {
             stage = 0;
@@ -426,19 +524,20 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {
       // ------------------------------------------------------ MMA issuer --
-      constexpr uint32_t idesc = instr_desc<BN, A_MN, B_MN>();
+      constexpr uint32_t idesc = instr_desc<BN, A_MN, B_MN, BM_T>();
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      for (int w = unit0; w < total; w += units) {
         int mt, nt, sp;
         decode_work(p, w, mt, nt, sp);
         const int kt0 = sp * p.kt_per_split;
         const int kt1 = min(p.k_tiles, kt0 + p.kt_per_split);
-        mbar_wait(tempty_bar(acc), acc_phase ^ 1);
+        if (CTA2) mbar_wait_acq_cluster(tempty_bar(acc), acc_phase ^ 1);  // both CTAs drained it
+        else mbar_wait(tempty_bar(acc), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * L::ACC_STRIDE);
         for (int kt = kt0; kt < kt1; ++kt) {
@@ -452,7 +551,8 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
             const uint32_t b_off = B_MN ? kk * 1024u : kk * 32u;
             const uint64_t ad = smem_desc<A_MN, BKT>(a_addr + a_off);
             const uint64_t bd = smem_desc<B_MN, BKT>(b_addr + b_off);
-            tc_mma_tf32(d_tmem, ad, bd, idesc, (kt > kt0 || kk > 0) ? 1u : 0u);
+            if (CTA2) tc_mma_tf32_pair(d_tmem, ad, bd, idesc, (kt > kt0 || kk > 0) ? 1u : 0u);
+            else tc_mma_tf32(d_tmem, ad, bd, idesc, (kt > kt0 || kk > 0) ? 1u : 0u);
             if (SPLIT3) {
               const uint64_t ad_lo = smem_desc<A_MN, BKT>(a_addr + L::STAGE + a_off);
               const uint64_t bd_lo = smem_desc<B_MN, BKT>(b_addr + L::STAGE + b_off);
@@ -460,13 +560,16 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
               tc_mma_tf32(d_tmem, ad, bd_lo, idesc, 1u);
             }
           }
-          tc_commit(empty_bar(stage));  // frees the stage once these MMAs have read it
+          // frees the stage (in both CTAs of a pair) once these MMAs have read it
+          if (CTA2) tc_commit_pair(empty_bar(stage));
+          else tc_commit(empty_bar(stage));
           if (++stage == L::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(tfull_bar(acc));  // accumulator complete -> epilogue
+        if (CTA2) tc_commit_pair(tfull_bar(acc));  // accumulator complete -> epilogues
+        else tc_commit(tfull_bar(acc));
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -478,12 +581,23 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
     uint32_t acc_phase = 0;
     const int mode = p.splits > 1 ? OMNI_EPI_STORE : p.epilogue;
     int st_chunk = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    // hand a drained accumulator back to the MMA issuer (CTA 0 of a pair)
+    auto release_acc = [&](int a) {
+      tc_fence_before();
+      if (CTA2) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_rank0(tempty_bar(a)));
+      } else {
+        mbar_arrive(tempty_bar(a));
+      }
+    };
+    for (int w = unit0; w < total; w += units) {
       int mt, nt, sp;
       decode_work(p, w, mt, nt, sp);
       mbar_wait(tfull_bar(acc), acc_phase);
       tc_fence_after();
-      const int row = mt * BM + ew * 32 + lane;
+      const int row0 = mt * BM_T + rank * BM + ew * 32;  // this warp's 32 output rows
+      const int row = row0 + lane;
       const uint32_t t_row =
           tmem_base + (uint32_t)(acc * L::ACC_STRIDE) + ((uint32_t)(ew * 32) << 16);
       if (p.use_tma_store) {
@@ -500,8 +614,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
           tmem_wait_ld();
           if (c0 + 32 >= BN || col0 + 32 >= p.N) {
             // last TMEM read of this accumulator: hand it back to the MMA warp early
-            tc_fence_before();
-            mbar_arrive(tempty_bar(acc));
+            release_acc(acc);
           }
           const uint32_t buf = stg + (uint32_t)(st_chunk & 1) * 4096u;
           if (lane == 0) bulk_wait_read<1>();  // the store that last used `buf` has read it
@@ -515,7 +628,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            tma_store_3d(&tmC, buf, col0, mt * BM + ew * 32, sp);
+            tma_store_3d(&tmC, buf, col0, row0, sp);
             bulk_commit();
           }
           ++st_chunk;
@@ -556,8 +669,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(tempty_bar(acc));
+      release_acc(acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -567,7 +679,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
     const int t = threadIdx.x - 256;
     int stage = 0;
     uint32_t phase = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    for (int w = unit0; w < total; w += units) {
       int mt, nt, sp;
       decode_work(p, w, mt, nt, sp);
       const int kt0 = sp * p.kt_per_split;
@@ -598,11 +710,17 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT>::THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (CTA2) cluster_sync();  // the peer's MMAs / commits into this CTA are complete
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "n"(L::TMEM_COLS)
-                 : "memory");
+    if (CTA2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(L::TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(L::TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -718,12 +836,23 @@ int make_tmap(CUtensorMap* map, const float* ptr, long long inner, long long out
 
 struct Plan {
   int bn, splits, kps, m_tiles, n_tiles, k_tiles, grid, raster_m_inner;
+  int cta2;  // tiles of 256 rows computed by CTA pairs
 };
 
 constexpr int kBNs[] = {32, 64, 96, 128, 192, 256};
 
-Plan make_plan(int M, int N, int K, int sms, int bkt = BK) {
+// Stage depth of the implicit weight gradient (im2col A, both operands
+// MN-major): 64-deep in TF32 mode (OMNI_WGRAD_BKT=32 for the 32-deep variant).
+int wgrad_bkt(int precision) {
+  static const int env = getenv("OMNI_WGRAD_BKT") ? atoi(getenv("OMNI_WGRAD_BKT")) : 64;
+  return (precision == OMNI_PREC_TF32 && env == 64) ? 64 : BK;
+}
+
+Plan make_plan(int M, int N, int K, int sms, int bkt = BK, bool cta2 = false, bool b_mn = false) {
   Plan pl{};
+  pl.cta2 = cta2;
+  const int bm = cta2 ? 2 * BM : BM;
+  const int units = cta2 ? sms / 2 : sms;  // concurrent work units (SMs or SM pairs)
   if (N <= 256) {
     for (int b : kBNs)
       if (b >= N) {
@@ -753,20 +882,22 @@ Plan make_plan(int M, int N, int K, int sms, int bkt = BK) {
       }
     }
   }
-  pl.m_tiles = (int)omni::ceil_div(M, BM);
+  // a pair stages BN/2 columns of B per CTA: MN-major B needs whole 32-column chunks
+  if (cta2 && b_mn && (pl.bn / 2) % 32 != 0) pl.bn = pl.bn < 64 ? 64 : pl.bn + 32;
+  pl.m_tiles = (int)omni::ceil_div(M, bm);
   pl.n_tiles = (int)omni::ceil_div(N, pl.bn);
   pl.k_tiles = (int)omni::ceil_div(K, bkt);
   const long long tiles = (long long)pl.m_tiles * pl.n_tiles;
   int splits = 1;
-  if (tiles < sms && pl.k_tiles >= 8) {
+  if (tiles < units && pl.k_tiles >= 8) {
     // Split-K cost model: the persistent grid finishes after ceil(tiles*s/sms)
     // rounds of (k_tiles/s) k-steps each; every extra split adds one M x N
     // fp32 partial written and re-read by the fixed-order reduction.
-    const double t_kstep = 2.0 * BM * pl.bn * bkt / (650e12 / sms);  // s per k-step per SM
+    const double t_kstep = 2.0 * bm * pl.bn * bkt / (650e12 / units);  // s per k-step per unit
     const int max_splits = pl.k_tiles / 4 < 64 ? pl.k_tiles / 4 : 64;  // >= 4 k-steps per split
     double best = 1e30;
     for (int s = 1; s <= max_splits; ++s) {
-      const long long rounds = omni::ceil_div(tiles * s, sms);
+      const long long rounds = omni::ceil_div(tiles * s, units);
       const double t = rounds * omni::ceil_div(pl.k_tiles, s) * t_kstep +
                        (s > 1 ? s * (double)M * N * 8.0 / 6.0e12 : 0.0);
       if (t < best * 0.98) {   // prefer fewer splits unless clearly faster
@@ -775,12 +906,45 @@ Plan make_plan(int M, int N, int K, int sms, int bkt = BK) {
       }
     }
   }
+  // tuning probes (tools/conv_probe.py sweeps): force a tile width / split count
+  static const int force_bn = getenv("OMNI_FORCE_BN") ? atoi(getenv("OMNI_FORCE_BN")) : 0;
+  static const int force_splits = getenv("OMNI_FORCE_SPLITS") ? atoi(getenv("OMNI_FORCE_SPLITS")) : 0;
+  if (force_bn) {
+    pl.bn = force_bn;
+    pl.n_tiles = (int)omni::ceil_div(N, pl.bn);
+  }
+  if (force_splits) splits = force_splits < pl.k_tiles ? force_splits : pl.k_tiles;
   pl.kps = (int)omni::ceil_div(pl.k_tiles, splits);
   pl.splits = (int)omni::ceil_div(pl.k_tiles, pl.kps);
   const long long work = tiles * pl.splits;
-  pl.grid = (int)(work < sms ? work : sms);
+  pl.grid = (int)(work < units ? work : units) * (cta2 ? 2 : 1);
   pl.raster_m_inner = pl.m_tiles < pl.n_tiles;
   return pl;
+}
+
+// CTA pairs (M = 256 tiles, half of B per CTA) for TF32 GEMMs with more than
+// one 128-row tile; the transposed conv form (im2col B, M = d_out <= 128) and
+// 3xTF32 stay on single CTAs.  OMNI_NO_2CTA=1 disables pairs.
+bool pair_ok(int precision, int M, int im2col) {
+  static const bool off = getenv("OMNI_NO_2CTA") != nullptr;
+  return !off && precision == OMNI_PREC_TF32 && M > BM && im2col != 4;
+}
+
+// The one planning entry point: launches and workspace queries agree on it.
+Plan plan_for(int precision, int M, int N, int K, bool b_mn, int im2col) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int bkt = im2col == 3 ? wgrad_bkt(precision) : BK;
+  const bool b_mn_eff = b_mn || im2col == 2 || im2col == 3;
+  const int sms = omni::sm_count_cached(dev);
+  bool pair = pair_ok(precision, M, im2col);
+  if (pair && b_mn_eff) {
+    // MN-major B is split into 32-column halves: a tile width that does not
+    // split (N = 96 -> BN 96) would have to grow and waste MMA work; stay single
+    const Plan single = make_plan(M, N, K, sms, bkt, false, b_mn_eff);
+    if ((single.bn / 2) % 32 != 0) return single;
+  }
+  return make_plan(M, N, K, sms, bkt, pair, b_mn_eff);
 }
 
 // Activation tensor behind an im2col operand (NHWC, pixel stride cs).
@@ -824,55 +988,89 @@ int make_tmap_im2col(CUtensorMap* map, const ConvGeom& g, int pixels, bool mn_ma
   return OMNI_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool SPLIT3, int IM2COL, int BKT = BK>
+template <int BN, bool A_MN, bool B_MN, bool SPLIT3, int IM2COL, int BKT, bool CTA2>
 int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, long long ldb,
               const Params& p, cudaStream_t st, const ConvGeom* cg) {
-  using L = Layout<BN, SPLIT3, BKT>;
-  CUtensorMap ta, tb;
-  int rc;
-  if (IM2COL == 1) rc = make_tmap_im2col(&ta, *cg, BM, false);
-  else if (IM2COL == 3) rc = make_tmap_im2col(&ta, *cg, BKT, true);
-  else rc = A_MN ? make_tmap(&ta, A, p.M, p.K, lda, 32, BKT, true)
-                 : make_tmap(&ta, A, p.K, p.M, lda, 32, BM, false);
-  if (rc) return rc;
-  if (IM2COL == 2) rc = make_tmap_im2col(&tb, *cg, BKT, true);
-  else if (IM2COL == 4) rc = make_tmap_im2col(&tb, *cg, BN, false);
-  else rc = B_MN ? make_tmap(&tb, B, p.N, p.K, ldb, 32, BKT, true)
-                 : make_tmap(&tb, B, p.K, p.N, ldb, 32, BN, false);
-  if (rc) return rc;
-  CUtensorMap tc;
-  memset(&tc, 0, sizeof(tc));
-  if (p.use_tma_store) {
-    rc = make_tmap_c(&tc, p.C, p.N, p.M, p.ldc, p.splits, p.split_stride);
+  constexpr bool B_CHUNKED = B_MN || IM2COL == 2;  // B staged as 32-column MN-major chunks
+  if constexpr (CTA2 && B_CHUNKED && (BN / 2) % 32 != 0) {
+    omni::set_error("gemm: BN=%d cannot be split across a CTA pair with MN-major B", BN);
+    return OMNI_EUNSUPPORTED;
+  } else {
+    using L = Layout<BN, SPLIT3, BKT, CTA2>;
+    CUtensorMap ta, tb;
+    int rc;
+    if (IM2COL == 1) rc = make_tmap_im2col(&ta, *cg, BM, false);
+    else if (IM2COL == 3) rc = make_tmap_im2col(&ta, *cg, BKT, true);
+    else rc = A_MN ? make_tmap(&ta, A, p.M, p.K, lda, 32, BKT, true)
+                   : make_tmap(&ta, A, p.K, p.M, lda, 32, BM, false);
     if (rc) return rc;
+    if (IM2COL == 2) rc = make_tmap_im2col(&tb, *cg, BKT, true);
+    else if (IM2COL == 4) rc = make_tmap_im2col(&tb, *cg, L::BNL, false);
+    else rc = B_MN ? make_tmap(&tb, B, p.N, p.K, ldb, 32, BKT, true)
+                   : make_tmap(&tb, B, p.K, p.N, ldb, 32, L::BNL, false);
+    if (rc) return rc;
+    CUtensorMap tc;
+    memset(&tc, 0, sizeof(tc));
+    if (p.use_tma_store) {
+      rc = make_tmap_c(&tc, p.C, p.N, p.M, p.ldc, p.splits, p.split_stride);
+      if (rc) return rc;
+    }
+    auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT3, IM2COL, BKT, CTA2>;
+    // once per instantiation and device (so a launch inside CUDA-graph capture
+    // makes no attribute calls)
+    static unsigned long long configured = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(configured & (1ull << (dev & 63)))) {
+      OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
+      configured |= 1ull << (dev & 63);
+    }
+    if (CTA2) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3((unsigned)pl.grid);
+      cfg.blockDim = dim3(L::THREADS);
+      cfg.dynamicSmemBytes = L::BYTES;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      OMNI_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p));
+    } else {
+      kern<<<pl.grid, L::THREADS, L::BYTES, st>>>(ta, tb, tc, p);
+    }
+    return omni::check_launch("gemm_tf32");
   }
-  auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT3, IM2COL, BKT>;
-  // once per instantiation and device (so a launch inside CUDA-graph capture
-  // makes no attribute calls)
-  static unsigned long long configured = 0;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!(configured & (1ull << (dev & 63)))) {
-    OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
-    configured |= 1ull << (dev & 63);
+}
+
+template <bool A_MN, bool B_MN, bool SPLIT3, int IM2COL, int BKT, bool CTA2>
+int dispatch_bn_t(const Plan& pl, const float* A, long long lda, const float* B, long long ldb,
+                  const Params& p, cudaStream_t st, const ConvGeom* cg) {
+#define OMNI_BN_CASE(X) \
+  case X: return launch_tc<X, A_MN, B_MN, SPLIT3, IM2COL, BKT, CTA2>(pl, A, lda, B, ldb, p, st, cg);
+  switch (pl.bn) {
+    OMNI_BN_CASE(32)
+    OMNI_BN_CASE(64)
+    OMNI_BN_CASE(96)
+    OMNI_BN_CASE(128)
+    OMNI_BN_CASE(192)
+    OMNI_BN_CASE(256)
   }
-  kern<<<pl.grid, L::THREADS, L::BYTES, st>>>(ta, tb, tc, p);
-  return omni::check_launch("gemm_tf32");
+#undef OMNI_BN_CASE
+  omni::set_error("gemm: no kernel for BN=%d", pl.bn);
+  return OMNI_EUNSUPPORTED;
 }
 
 template <bool A_MN, bool B_MN, bool SPLIT3, int IM2COL, int BKT = BK>
 int dispatch_bn(const Plan& pl, const float* A, long long lda, const float* B, long long ldb,
                 const Params& p, cudaStream_t st, const ConvGeom* cg = nullptr) {
-  switch (pl.bn) {
-    case 32: return launch_tc<32, A_MN, B_MN, SPLIT3, IM2COL, BKT>(pl, A, lda, B, ldb, p, st, cg);
-    case 64: return launch_tc<64, A_MN, B_MN, SPLIT3, IM2COL, BKT>(pl, A, lda, B, ldb, p, st, cg);
-    case 96: return launch_tc<96, A_MN, B_MN, SPLIT3, IM2COL, BKT>(pl, A, lda, B, ldb, p, st, cg);
-    case 128: return launch_tc<128, A_MN, B_MN, SPLIT3, IM2COL, BKT>(pl, A, lda, B, ldb, p, st, cg);
-    case 192: return launch_tc<192, A_MN, B_MN, SPLIT3, IM2COL, BKT>(pl, A, lda, B, ldb, p, st, cg);
-    case 256: return launch_tc<256, A_MN, B_MN, SPLIT3, IM2COL, BKT>(pl, A, lda, B, ldb, p, st, cg);
+  if constexpr (!SPLIT3 && IM2COL != 4) {
+    if (pl.cta2) return dispatch_bn_t<A_MN, B_MN, false, IM2COL, BKT, true>(pl, A, lda, B, ldb, p, st, cg);
   }
-  omni::set_error("gemm: no kernel for BN=%d", pl.bn);
-  return OMNI_EUNSUPPORTED;
+  return dispatch_bn_t<A_MN, B_MN, SPLIT3, IM2COL, BKT, false>(pl, A, lda, B, ldb, p, st, cg);
 }
 
 template <bool SPLIT3>
@@ -898,12 +1096,10 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
   p.bias = bias;
   p.aux = aux;
   p.ld_aux = ld_aux;
-  int dev = 0;
-  cudaGetDevice(&dev);
   // The implicit weight gradient (im2col A, both operands MN-major) runs 64-deep
   // K stages in TF32 mode: half the TMA ops per byte, 64-pixel im2col boxes.
-  const int bkt = (im2col == 3 && precision == OMNI_PREC_TF32) ? 64 : BK;
-  const Plan pl = make_plan(M, N, K, omni::sm_count_cached(dev), bkt);
+  const int bkt = im2col == 3 ? wgrad_bkt(precision) : BK;
+  const Plan pl = plan_for(precision, M, N, K, b_mn != 0, im2col);
   p.m_tiles = pl.m_tiles;
   p.n_tiles = pl.n_tiles;
   p.k_tiles = pl.k_tiles;
@@ -947,7 +1143,8 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
             : dispatch_bn<false, false, false, 1>(pl, A, lda, B, ldb, p, st, cg);
   else if (im2col == 3)
     rc = s3 ? dispatch_bn<true, true, true, 3>(pl, A, lda, B, ldb, p, st, cg)
-            : dispatch_bn<true, true, false, 3, 64>(pl, A, lda, B, ldb, p, st, cg);
+       : bkt == 64 ? dispatch_bn<true, true, false, 3, 64>(pl, A, lda, B, ldb, p, st, cg)
+                   : dispatch_bn<true, true, false, 3>(pl, A, lda, B, ldb, p, st, cg);
   else if (im2col == 4)
     rc = s3 ? dispatch_bn<false, false, true, 4>(pl, A, lda, B, ldb, p, st, cg)
             : dispatch_bn<false, false, false, 4>(pl, A, lda, B, ldb, p, st, cg);
@@ -974,16 +1171,13 @@ extern "C" {
 long long omni_gemm_plan(int precision, int M, int N, int K, int a_mn_major, int b_mn_major,
                          int* splits, int* bn) {
   (void)a_mn_major;
-  (void)b_mn_major;
   if (M < 1 || N < 1 || K < 1) return -1;
   if (precision == OMNI_PREC_FP32_SIMT) {
     if (splits) *splits = 1;
     if (bn) *bn = 16;
     return 0;
   }
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const gemm::Plan pl = gemm::make_plan(M, N, K, omni::sm_count_cached(dev));
+  const gemm::Plan pl = gemm::plan_for(precision, M, N, K, b_mn_major != 0, 0);
   if (splits) *splits = pl.splits;
   if (bn) *bn = pl.bn;
   return pl.splits > 1 ? (long long)pl.splits * M * N * 4 : 0;
@@ -1069,16 +1263,12 @@ long long omni_conv_implicit_plan(int precision, int op, int b, int n, int c, in
                                   int pad, int d_out) {
   int M, N, K, m;
   if (conv_shape(op, b, n, c, k, stride, pad, d_out, &M, &N, &K, &m)) return -1;
-  if (op == OMNI_CONV_WGRAD) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const int bkt = precision == OMNI_PREC_TF32 ? 64 : gemm::BK;
-    const gemm::Plan pl = gemm::make_plan(N, M, K, omni::sm_count_cached(dev), bkt);
-    return pl.splits > 1 ? (long long)pl.splits * M * N * 4 : 0;
-  }
-  if (op == OMNI_CONV_FPROP && conv_fprop_transposed(d_out, M, K))
-    return omni_gemm_plan(precision, N, M, K, 0, 0, nullptr, nullptr);
-  return omni_gemm_plan(precision, M, N, K, 0, 0, nullptr, nullptr);
+  // exactly the plans omni_conv_implicit_f32 launches
+  gemm::Plan pl;
+  if (op == OMNI_CONV_WGRAD) pl = gemm::plan_for(precision, N, M, K, true, 3);
+  else if (conv_fprop_transposed(d_out, M, K)) pl = gemm::plan_for(precision, N, M, K, false, 4);
+  else pl = gemm::plan_for(precision, M, N, K, false, 1);
+  return pl.splits > 1 ? (long long)pl.splits * M * N * 4 : 0;
 }
 
 int omni_conv_implicit_f32(int precision, int op, const float* X, int b, int n, int c, int cs,

@@ -375,8 +375,11 @@ def test_conv_implicit_fprop(geom, prec):
     assert rel_err(Y.cpu(), ref) < (3e-3 if prec == "tf32" else 5e-6 * max(1.0, (Kc / 1000) ** 0.5))
 
 
-@pytest.mark.parametrize("geom", IMPLICIT_GEOMS)
-def test_conv_implicit_wgrad(geom):
+@pytest.mark.parametrize("geom", IMPLICIT_GEOMS + [(8, 13, 384, 3, 1, 1, 384)])
+@pytest.mark.parametrize("prec", ["tf32", "3xtf32"])
+def test_conv_implicit_wgrad(geom, prec):
+    """TF32 runs on CTA pairs (M = taps*c > 128: 256-row tiles, half of dY per
+    CTA); 3xTF32 on single CTAs."""
     b, n, c, k, s, p, d = geom
     X, _ = _conv_inputs(b, n, c, k, d, 12)
     m = (n + 2 * p - k) // s + 1
@@ -384,11 +387,13 @@ def test_conv_implicit_wgrad(geom):
     ld = K.round_up(Kc, 32)
     dY = torch.randn(b * m * m, d, device=DEV)
     dW = torch.full((d, ld), float("nan"), device=DEV)
-    K.conv_implicit(_abi.CONV_WGRAD, X, c, k, s, p, d, dY, d, dW, ld, precision=_abi.PREC_3XTF32)
+    K.conv_implicit(_abi.CONV_WGRAD, X, c, k, s, p, d, dY, d, dW, ld,
+                    precision=_abi.PRECISIONS[prec])
     D = K.lower_nhwc(X, c, k, s, p, ld)
     ref = (dY.double().t() @ D[:, :Kc].double()).cpu()
     torch.cuda.synchronize()
-    assert rel_err(dW[:, :Kc].cpu(), ref) < 5e-6 * max(1.0, (b * m * m / 1000) ** 0.5)
+    tol = 3e-3 if prec == "tf32" else 5e-6 * max(1.0, (b * m * m / 1000) ** 0.5)
+    assert rel_err(dW[:, :Kc].cpu(), ref) < tol
 
 
 @pytest.mark.parametrize("geom", [g for g in IMPLICIT_GEOMS if g[4] == 1 and g[6] % 32 == 0])
