@@ -34,6 +34,8 @@ extern "C" {
 const char* omni_last_error(void);
 int omni_version(void);
 int omni_device_sm_count(int device);
+/* Kernels launched by this library so far (process-wide; for launch accounting). */
+long long omni_launch_count(void);
 
 /* ---------------------------------------------------------------- K1 --
  * Batched lowering (type-1 im2col over b_p images starting at `start`).
@@ -108,8 +110,13 @@ int omni_gemm_f32(int precision, int M, int N, int K, const float* A, long long 
  *                    (G = output gradient dY, b*m*m rows, ld ldg)
  * The data gradient of a stride-1 conv is OMNI_CONV_FPROP on dY with pad
  * k-1-pad and the spatially flipped, transposed weights.                     */
+/*   OMNI_CONV_WGRAD_BIAS: as OMNI_CONV_WGRAD, plus the bias gradient
+ *                    Y[o*ldy + k*k*c] = sum_pix G[pix*ldg + o] as one more GEMM row
+ *                    (a ones operand chunk; needs ldy > k*k*c).  The workspace
+ *                    (size from omni_conv_implicit_plan) holds that ones tile.  */
 #define OMNI_CONV_FPROP 0
 #define OMNI_CONV_WGRAD 1
+#define OMNI_CONV_WGRAD_BIAS 2
 long long omni_conv_implicit_plan(int precision, int op, int b, int n, int c, int k, int stride,
                                   int pad, int d_out);
 int omni_conv_implicit_f32(int precision, int op, const float* X, int b, int n, int c, int cs,
@@ -180,9 +187,11 @@ int omni_space_to_depth_f32(const float* X, int b, int n, int c, int cs, int s, 
                             int cp, void* stream);
 /* Weights of that conv, tap-major rows Wt (o x ld, ld >= ceil(k/s)^2 * cp):
  * Wt[o*ld + (kx2*k2 + ky2)*cp + (dx*s + dy)*c + ch] = W[o, ch, s*kx2+dx, s*ky2+dy]
- * (0 past the kernel).  inverse=1 maps a gradient in that layout back to OIHW. */
+ * (0 past the kernel).  inverse=1 maps a gradient in that layout back to OIHW
+ * and, when bias != NULL, copies column ceil(k/s)^2 * cp (the
+ * OMNI_CONV_WGRAD_BIAS row) to bias[o].                                        */
 int omni_conv_weight_s2d_f32(float* W, int o, int c, int k, int s, int cp, float* Wt, long long ld,
-                             int inverse, void* stream);
+                             int inverse, float* bias, void* stream);
 /* Batched 2-D transpose: dst[bi][j*ldd + i] = src[bi][i*lds + j], i < rows,
  * j < cols; batch strides in elements.  Used for NHWC <-> flattened CHW and
  * for FC weight staging.                                                     */

@@ -34,6 +34,7 @@ EPI_RELU = 5
 
 CONV_FPROP = 0
 CONV_WGRAD = 1
+CONV_WGRAD_BIAS = 2
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -45,6 +46,7 @@ SIGNATURES: dict[str, tuple] = {
     "omni_last_error": (ctypes.c_char_p, []),
     "omni_version": (_I, []),
     "omni_device_sm_count": (_I, [_I]),
+    "omni_launch_count": (_L, []),
     "omni_lower_nchw_f32": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P]),
     "omni_lower_nchw_f64": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P]),
     "omni_lower_nhwc_f32": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P]),
@@ -78,7 +80,7 @@ SIGNATURES: dict[str, tuple] = {
     "omni_gather_i32": (_I, [_P, _P, _I, _P, _P]),
     "omni_conv_weight_to_tap_f32": (_I, [_P, _I, _I, _I, _P, _L, _I, _P, _P]),
     "omni_space_to_depth_f32": (_I, [_P, _I, _I, _I, _I, _I, _P, _I, _I, _P]),
-    "omni_conv_weight_s2d_f32": (_I, [_P, _I, _I, _I, _I, _I, _P, _L, _I, _P]),
+    "omni_conv_weight_s2d_f32": (_I, [_P, _I, _I, _I, _I, _I, _P, _L, _I, _P, _P]),
     "omni_transpose_f32": (_I, [_P, _L, _L, _I, _I, _P, _L, _L, _I, _P]),
     "omni_fill_f32": (_I, [_P, _F, _L, _P]),
 }

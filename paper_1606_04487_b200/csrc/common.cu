@@ -3,6 +3,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <atomic>
 #include <mutex>
 
 #include "common.cuh"
@@ -20,7 +21,10 @@ void set_error(const char* fmt, ...) {
   g_last_error = buf;
 }
 
+static std::atomic<long long> g_launches{0};
+
 int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("%s: launch failed: %s", what, cudaGetErrorString(e));
@@ -74,5 +78,7 @@ const char* omni_last_error(void) { return omni::g_last_error.c_str(); }
 int omni_version(void) { return 1; }
 
 int omni_device_sm_count(int device) { return omni::sm_count_cached(device); }
+
+long long omni_launch_count(void) { return omni::g_launches.load(std::memory_order_relaxed); }
 
 }  // extern "C"

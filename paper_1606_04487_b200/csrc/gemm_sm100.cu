@@ -53,6 +53,8 @@ struct Params {
   // kernel size, 32-channel blocks per filter tap
   int conv_m, conv_mm, conv_s, conv_pad, conv_k, conv_cblocks;
   int transpose_c;  // store C^T: C[j*ldc + i] (weight gradient with im2col as the A operand)
+  int ones_chunk;   // IM2COL 3: 32-row A chunk loaded from the ones tile (bias gradient), or -1
+  int px_dh, px_dw; // IM2COL 2/3: one k-tile of BKT pixels = px_dh output rows + px_dw columns
 };
 
 // CTA2: the tile is computed by a CTA pair (cluster of 2, tcgen05 cta_group::2,
@@ -350,7 +352,8 @@ template <int BN, bool A_MN, bool B_MN, bool SPLIT3, int IM2COL, int BKT, bool C
 __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmC, const Params p) {
+                     const __grid_constant__ CUtensorMap tmC,
+                     const __grid_constant__ CUtensorMap tmO, const Params p) {
   // K-major operands hold exactly one 128-byte swizzle row (32 fp32) per stage;
   // deeper stages are for MN-major operands only.
   static_assert(BKT == BK || (A_MN && B_MN), "BKT > 32 needs MN-major operands");
@@ -380,6 +383,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     if (p.use_tma_store) tma_prefetch_desc(&tmC);
+    if (IM2COL == 3 && p.ones_chunk >= 0) tma_prefetch_desc(&tmO);
     for (int s = 0; s < L::STAGES; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
@@ -442,6 +446,41 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
           b_h0 = (r / p.conv_m) * p.conv_s - p.conv_pad;
           b_w0 = (r - (r / p.conv_m) * p.conv_m) * p.conv_s - p.conv_pad;
         }
+        // This single thread paces the pipeline, so everything that does not
+        // change along K is computed once per work unit and the K walk uses
+        // division-free cursors.
+        // IM2COL 2/3: (filter tap, channel block) of each 32-row im2col chunk
+        constexpr int NCH = IM2COL == 3 ? BM / 32 : (IM2COL == 2 ? BNL / 32 : 1);
+        int ch_c[NCH], ch_kx[NCH], ch_ky[NCH];  // ch_c < 0: the ones chunk
+        // IM2COL 2/3: pixel cursor (image, output row, output column) of k-tile kt
+        int px_img = 0, px_oh = 0, px_ow = 0;
+        if (IM2COL == 2 || IM2COL == 3) {
+          const int taps = p.conv_k * p.conv_k;
+          const int first = (IM2COL == 3 ? arow : bcol) / 32;
+#pragma unroll
+          for (int j = 0; j < NCH; ++j) {
+            const int blk = first + j;
+            int tap = blk / p.conv_cblocks;
+            const int cb = blk - tap * p.conv_cblocks;
+            if (tap >= taps) tap = taps - 1;  // rows past M: any valid load, discarded
+            ch_kx[j] = tap / p.conv_k;
+            ch_ky[j] = tap - ch_kx[j] * p.conv_k;
+            ch_c[j] = (IM2COL == 3 && blk == p.ones_chunk) ? -1 : cb * 32;
+          }
+          const int kc0 = kt0 * BKT;
+          px_img = kc0 / p.conv_mm;
+          const int r = kc0 - px_img * p.conv_mm;
+          px_oh = r / p.conv_m;
+          px_ow = r - px_oh * p.conv_m;
+        }
+        // IM2COL 1/4: (channel block, tap) cursor of k-tile kt, tap-major K
+        int t_cb = 0, t_kx = 0, t_ky = 0;
+        if (IM2COL == 1 || IM2COL == 4) {
+          const int tap = kt0 / p.conv_cblocks;
+          t_cb = kt0 - tap * p.conv_cblocks;
+          t_kx = tap / p.conv_k;
+          t_ky = tap - t_kx * p.conv_k;
+        }
         for (int kt = kt0; kt < kt1; ++kt) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           if (rank == 0) mbar_expect_tx(full_bar(stage), (uint32_t)(CTA2 ? 2 * L::STAGE : L::STAGE));
@@ -458,27 +497,19 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
           const uint32_t a_dst = sbase + stage * L::STAGE_ALL;
           const uint32_t b_dst = a_dst + L::A_BYTES;
           const int kc = kt * BKT;
+          const int px_h0 = px_oh * p.conv_s - p.conv_pad, px_w0 = px_ow * p.conv_s - p.conv_pad;
           if (IM2COL == 1) {
             // K index = (tap, channel): tap-major, 32-channel blocks
-            const int cb = kt % p.conv_cblocks, tap = kt / p.conv_cblocks;
-            const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
-            load_im2col(&tmA, a_dst, cb * 32, a_w0, a_h0, a_img, (uint16_t)ky, (uint16_t)kx);
+            load_im2col(&tmA, a_dst, t_cb * 32, a_w0, a_h0, a_img, (uint16_t)t_ky, (uint16_t)t_kx);
           } else if (IM2COL == 3) {
-            // A(i = (tap, ch), r = pixel): BK output pixels x 32 channels per 32-row chunk
-            const int img = kc / p.conv_mm;
-            const int r = kc - img * p.conv_mm;
-            const int h0 = (r / p.conv_m) * p.conv_s - p.conv_pad;
-            const int w0 = (r - (r / p.conv_m) * p.conv_m) * p.conv_s - p.conv_pad;
-            const int taps = p.conv_k * p.conv_k;
+            // A(i = (tap, ch), r = pixel): BKT output pixels x 32 channels per 32-row chunk
 #pragma unroll
-            for (int j = 0; j < BM / 32; ++j) {
-              const int blk = arow / 32 + j;
-              int tap = blk / p.conv_cblocks;
-              const int cb = blk - tap * p.conv_cblocks;
-              if (tap >= taps) tap = taps - 1;  // rows past M: any valid load, discarded
-              const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
-              load_im2col(&tmA, a_dst + j * (BKT * 128), cb * 32, w0, h0, img, (uint16_t)ky,
-                          (uint16_t)kx);
+            for (int j = 0; j < NCH; ++j) {
+              if (ch_c[j] < 0)  // bias-gradient row: sum over pixels of dY
+                load2d(&tmO, a_dst + j * (BKT * 128), 0, 0);
+              else
+                load_im2col(&tmA, a_dst + j * (BKT * 128), ch_c[j], px_w0, px_h0, px_img,
+                            (uint16_t)ch_ky[j], (uint16_t)ch_kx[j]);
             }
           } else if (!A_MN) {
             load2d(&tmA, a_dst, kc, arow);
@@ -489,32 +520,41 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
           }
           if (IM2COL == 4) {
             // B(j = pixel, r = (tap, ch)): BN output pixels x 32 channels, K-major
-            const int cb = kt % p.conv_cblocks, tap = kt / p.conv_cblocks;
-            const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
-            load_im2col(&tmB, b_dst, cb * 32, b_w0, b_h0, b_img, (uint16_t)ky, (uint16_t)kx);
+            load_im2col(&tmB, b_dst, t_cb * 32, b_w0, b_h0, b_img, (uint16_t)t_ky, (uint16_t)t_kx);
           } else if (IM2COL == 2) {
-            // B(j = (tap, ch), r = pixel): BK output pixels x 32 channels per chunk
-            const int img = kc / p.conv_mm;
-            const int r = kc - img * p.conv_mm;
-            const int h0 = (r / p.conv_m) * p.conv_s - p.conv_pad;
-            const int w0 = (r - (r / p.conv_m) * p.conv_m) * p.conv_s - p.conv_pad;
-            const int taps = p.conv_k * p.conv_k;
+            // B(j = (tap, ch), r = pixel): BKT output pixels x 32 channels per chunk
 #pragma unroll
-            for (int j = 0; j < BNL / 32; ++j) {
-              const int blk = bcol / 32 + j;
-              int tap = blk / p.conv_cblocks;
-              const int cb = blk - tap * p.conv_cblocks;
-              if (tap >= taps) tap = taps - 1;  // columns past N: any valid load, discarded
-              const int kx = tap / p.conv_k, ky = tap - (tap / p.conv_k) * p.conv_k;
-              load_im2col(&tmB, b_dst + j * (BKT * 128), cb * 32, w0, h0, img, (uint16_t)ky,
-                          (uint16_t)kx);
-            }
+            for (int j = 0; j < NCH; ++j)
+              load_im2col(&tmB, b_dst + j * (BKT * 128), ch_c[j], px_w0, px_h0, px_img,
+                          (uint16_t)ch_ky[j], (uint16_t)ch_kx[j]);
           } else if (!B_MN) {
             load2d(&tmB, b_dst, kc, bcol);
           } else {
 #pragma unroll
             for (int j = 0; j < BNL / 32; ++j)
               load2d(&tmB, b_dst + j * (BKT * 128), bcol + 32 * j, kc);
+          }
+          // advance the K cursors by one k-tile
+          if (IM2COL == 1 || IM2COL == 4) {
+            if (++t_cb == p.conv_cblocks) {
+              t_cb = 0;
+              if (++t_ky == p.conv_k) {
+                t_ky = 0;
+                ++t_kx;
+              }
+            }
+          }
+          if (IM2COL == 2 || IM2COL == 3) {
+            px_ow += p.px_dw;  // BKT = px_dh * m + px_dw pixels
+            px_oh += p.px_dh;
+            if (px_ow >= p.conv_m) {
+              px_ow -= p.conv_m;
+              ++px_oh;
+            }
+            if (px_oh >= p.conv_m) {
+              px_img += px_oh / p.conv_m;
+              px_oh -= (px_oh / p.conv_m) * p.conv_m;
+            }
           }
           if (++stage == L::STAGES) {
             stage = 0;
@@ -722,6 +762,13 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
                    "n"(L::TMEM_COLS)
                    : "memory");
   }
+}
+
+// The ones tile behind OMNI_CONV_WGRAD_BIAS's bias-gradient row (head of the
+// caller's workspace; rewritten per call since split-K partials share it).
+constexpr int kOnesBytes = 64 * 32 * 4;  // BKT (<= 64) K-rows x 32 fp32
+__global__ void fill_ones_kernel(float* __restrict__ p, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = 1.f;
 }
 
 // Split-K reduction: C[i,j] = epi(sum_s ws[s][i][j]) in ascending s.
@@ -990,7 +1037,7 @@ int make_tmap_im2col(CUtensorMap* map, const ConvGeom& g, int pixels, bool mn_ma
 
 template <int BN, bool A_MN, bool B_MN, bool SPLIT3, int IM2COL, int BKT, bool CTA2>
 int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, long long ldb,
-              const Params& p, cudaStream_t st, const ConvGeom* cg) {
+              const Params& p, cudaStream_t st, const ConvGeom* cg, const float* ones) {
   constexpr bool B_CHUNKED = B_MN || IM2COL == 2;  // B staged as 32-column MN-major chunks
   if constexpr (CTA2 && B_CHUNKED && (BN / 2) % 32 != 0) {
     omni::set_error("gemm: BN=%d cannot be split across a CTA pair with MN-major B", BN);
@@ -1009,10 +1056,15 @@ int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, lon
     else rc = B_MN ? make_tmap(&tb, B, p.N, p.K, ldb, 32, BKT, true)
                    : make_tmap(&tb, B, p.K, p.N, ldb, 32, L::BNL, false);
     if (rc) return rc;
-    CUtensorMap tc;
+    CUtensorMap tc, to;
     memset(&tc, 0, sizeof(tc));
+    memset(&to, 0, sizeof(to));
     if (p.use_tma_store) {
       rc = make_tmap_c(&tc, p.C, p.N, p.M, p.ldc, p.splits, p.split_stride);
+      if (rc) return rc;
+    }
+    if (IM2COL == 3 && p.ones_chunk >= 0) {  // BKT x 32 ones, MN-major like an im2col chunk
+      rc = make_tmap(&to, ones, 32, BKT, 32, 32, BKT, true);
       if (rc) return rc;
     }
     auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT3, IM2COL, BKT, CTA2>;
@@ -1038,9 +1090,9 @@ int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, lon
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      OMNI_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p));
+      OMNI_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, to, p));
     } else {
-      kern<<<pl.grid, L::THREADS, L::BYTES, st>>>(ta, tb, tc, p);
+      kern<<<pl.grid, L::THREADS, L::BYTES, st>>>(ta, tb, tc, to, p);
     }
     return omni::check_launch("gemm_tf32");
   }
@@ -1048,9 +1100,10 @@ int launch_tc(const Plan& pl, const float* A, long long lda, const float* B, lon
 
 template <bool A_MN, bool B_MN, bool SPLIT3, int IM2COL, int BKT, bool CTA2>
 int dispatch_bn_t(const Plan& pl, const float* A, long long lda, const float* B, long long ldb,
-                  const Params& p, cudaStream_t st, const ConvGeom* cg) {
+                  const Params& p, cudaStream_t st, const ConvGeom* cg, const float* ones) {
 #define OMNI_BN_CASE(X) \
-  case X: return launch_tc<X, A_MN, B_MN, SPLIT3, IM2COL, BKT, CTA2>(pl, A, lda, B, ldb, p, st, cg);
+  case X:               \
+    return launch_tc<X, A_MN, B_MN, SPLIT3, IM2COL, BKT, CTA2>(pl, A, lda, B, ldb, p, st, cg, ones);
   switch (pl.bn) {
     OMNI_BN_CASE(32)
     OMNI_BN_CASE(64)
@@ -1066,11 +1119,13 @@ int dispatch_bn_t(const Plan& pl, const float* A, long long lda, const float* B,
 
 template <bool A_MN, bool B_MN, bool SPLIT3, int IM2COL, int BKT = BK>
 int dispatch_bn(const Plan& pl, const float* A, long long lda, const float* B, long long ldb,
-                const Params& p, cudaStream_t st, const ConvGeom* cg = nullptr) {
+                const Params& p, cudaStream_t st, const ConvGeom* cg = nullptr,
+                const float* ones = nullptr) {
   if constexpr (!SPLIT3 && IM2COL != 4) {
-    if (pl.cta2) return dispatch_bn_t<A_MN, B_MN, false, IM2COL, BKT, true>(pl, A, lda, B, ldb, p, st, cg);
+    if (pl.cta2)
+      return dispatch_bn_t<A_MN, B_MN, false, IM2COL, BKT, true>(pl, A, lda, B, ldb, p, st, cg, ones);
   }
-  return dispatch_bn_t<A_MN, B_MN, SPLIT3, IM2COL, BKT, false>(pl, A, lda, B, ldb, p, st, cg);
+  return dispatch_bn_t<A_MN, B_MN, SPLIT3, IM2COL, BKT, false>(pl, A, lda, B, ldb, p, st, cg, ones);
 }
 
 template <bool SPLIT3>
@@ -1087,8 +1142,10 @@ int dispatch_major(const Plan& pl, int a_mn, int b_mn, const float* A, long long
 int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, int a_mn,
              const float* B, long long ldb, int b_mn, float* C, long long ldc, int epilogue,
              const float* bias, const float* aux, long long ld_aux, float* workspace,
-             long long ws_bytes, cudaStream_t st, const ConvGeom* cg, int im2col) {
+             long long ws_bytes, cudaStream_t st, const ConvGeom* cg, int im2col,
+             const float* ones = nullptr) {
   Params p{};
+  p.ones_chunk = (im2col == 3 && ones) ? (M - 1) / 32 : -1;  // last row = bias gradient
   p.M = M;
   p.N = N;
   p.K = K;
@@ -1113,6 +1170,8 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
     p.conv_pad = cg->pad;
     p.conv_k = cg->k;
     p.conv_cblocks = cg->c / 32;
+    p.px_dh = bkt / cg->m;
+    p.px_dw = bkt - p.px_dh * cg->m;
   }
   if (pl.splits > 1) {
     const long long need = (long long)pl.splits * M * N * 4;
@@ -1142,9 +1201,9 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
     rc = s3 ? dispatch_bn<false, false, true, 1>(pl, A, lda, B, ldb, p, st, cg)
             : dispatch_bn<false, false, false, 1>(pl, A, lda, B, ldb, p, st, cg);
   else if (im2col == 3)
-    rc = s3 ? dispatch_bn<true, true, true, 3>(pl, A, lda, B, ldb, p, st, cg)
-       : bkt == 64 ? dispatch_bn<true, true, false, 3, 64>(pl, A, lda, B, ldb, p, st, cg)
-                   : dispatch_bn<true, true, false, 3>(pl, A, lda, B, ldb, p, st, cg);
+    rc = s3 ? dispatch_bn<true, true, true, 3>(pl, A, lda, B, ldb, p, st, cg, ones)
+       : bkt == 64 ? dispatch_bn<true, true, false, 3, 64>(pl, A, lda, B, ldb, p, st, cg, ones)
+                   : dispatch_bn<true, true, false, 3>(pl, A, lda, B, ldb, p, st, cg, ones);
   else if (im2col == 4)
     rc = s3 ? dispatch_bn<false, false, true, 4>(pl, A, lda, B, ldb, p, st, cg)
             : dispatch_bn<false, false, false, 4>(pl, A, lda, B, ldb, p, st, cg);
@@ -1238,7 +1297,8 @@ static bool conv_fprop_transposed(int d_out, int pixels, int K) {
 
 static int conv_shape(int op, int b, int n, int c, int k, int stride, int pad, int d_out, int* M,
                       int* N, int* K, int* m) {
-  OMNI_REQUIRE(op == OMNI_CONV_FPROP || op == OMNI_CONV_WGRAD, "conv: unknown op %d", op);
+  OMNI_REQUIRE(op == OMNI_CONV_FPROP || op == OMNI_CONV_WGRAD || op == OMNI_CONV_WGRAD_BIAS,
+               "conv: unknown op %d", op);
   OMNI_REQUIRE(b >= 1 && n >= 1 && k >= 1 && stride >= 1 && pad >= 0 && d_out >= 1,
                "n, k, d_in, d_out, stride must be positive");
   OMNI_REQUIRE(c % 32 == 0, "implicit conv needs d_in %% 32 == 0 (got %d)", c);
@@ -1264,10 +1324,14 @@ long long omni_conv_implicit_plan(int precision, int op, int b, int n, int c, in
   int M, N, K, m;
   if (conv_shape(op, b, n, c, k, stride, pad, d_out, &M, &N, &K, &m)) return -1;
   // exactly the plans omni_conv_implicit_f32 launches
-  gemm::Plan pl;
-  if (op == OMNI_CONV_WGRAD) pl = gemm::plan_for(precision, N, M, K, true, 3);
-  else if (conv_fprop_transposed(d_out, M, K)) pl = gemm::plan_for(precision, N, M, K, false, 4);
-  else pl = gemm::plan_for(precision, M, N, K, false, 1);
+  if (op != OMNI_CONV_FPROP) {
+    const int rows = op == OMNI_CONV_WGRAD_BIAS ? N + 1 : N;
+    const gemm::Plan pl = gemm::plan_for(precision, rows, M, K, true, 3);
+    return (op == OMNI_CONV_WGRAD_BIAS ? gemm::kOnesBytes : 0) +
+           (pl.splits > 1 ? (long long)pl.splits * rows * M * 4 : 0);
+  }
+  const gemm::Plan pl = conv_fprop_transposed(d_out, M, K) ? gemm::plan_for(precision, N, M, K, false, 4)
+                                                           : gemm::plan_for(precision, M, N, K, false, 1);
   return pl.splits > 1 ? (long long)pl.splits * M * N * 4 : 0;
 }
 
@@ -1284,7 +1348,9 @@ int omni_conv_implicit_f32(int precision, int op, const float* X, int b, int n, 
   OMNI_REQUIRE(cs >= c && cs % 4 == 0 && ((uintptr_t)X & 15) == 0,
                "conv: X must be 16-byte aligned NHWC with cs %% 4 == 0");
   OMNI_REQUIRE(ldg % 4 == 0 && ((uintptr_t)G & 15) == 0, "conv: G must be 16-byte aligned, ldg %% 4 == 0");
-  OMNI_REQUIRE(ldg >= (op == OMNI_CONV_FPROP ? K : d_out) && ldy >= N, "conv: leading dimension too small");
+  const bool with_bias = op == OMNI_CONV_WGRAD_BIAS;
+  OMNI_REQUIRE(ldg >= (op == OMNI_CONV_FPROP ? K : d_out) && ldy >= N + (with_bias ? 1 : 0),
+               "conv: leading dimension too small");
   OMNI_REQUIRE(epilogue >= 0 && epilogue <= 5, "conv: unknown epilogue %d", epilogue);
   OMNI_REQUIRE(!(epilogue == OMNI_EPI_BIAS || epilogue == OMNI_EPI_BIAS_RELU) || bias,
                "conv: bias epilogue needs a bias vector");
@@ -1305,8 +1371,20 @@ int omni_conv_implicit_f32(int precision, int op, const float* X, int b, int n, 
   // the B-side form needs) and dY (pixels x ldg) as the MN-major B operand;
   // the epilogue stores C^T, i.e. Y[o*ldy + (tap, ch)].
   OMNI_REQUIRE(epilogue == OMNI_EPI_STORE, "conv wgrad supports the plain store epilogue only");
-  return gemm::run_gemm(precision, N, M, K, nullptr, 0, 1, G, ldg, 1, Y, ldy, epilogue, bias, aux,
-                        ld_aux, workspace, ws_bytes, st, &cg, 3);
+  float* ones = nullptr;
+  if (with_bias) {
+    // one more GEMM row (tap*c index k*k*c) fed by a ones chunk: the bias gradient
+    OMNI_REQUIRE(workspace && ws_bytes >= gemm::kOnesBytes && ((uintptr_t)workspace & 15) == 0,
+                 "conv wgrad+bias: workspace of at least %d bytes required", gemm::kOnesBytes);
+    ones = workspace;
+    gemm::fill_ones_kernel<<<4, 512, 0, st>>>(ones, gemm::kOnesBytes / 4);
+    rc = omni::check_launch("fill_ones");
+    if (rc) return rc;
+    workspace += gemm::kOnesBytes / 4;
+    ws_bytes -= gemm::kOnesBytes;
+  }
+  return gemm::run_gemm(precision, N + (with_bias ? 1 : 0), M, K, nullptr, 0, 1, G, ldg, 1, Y, ldy,
+                        epilogue, bias, aux, ld_aux, workspace, ws_bytes, st, &cg, 3, ones);
 }
 
 }  // extern "C"

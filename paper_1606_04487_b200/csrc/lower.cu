@@ -404,9 +404,13 @@ __global__ void __launch_bounds__(kThreads) space_to_depth_v4_kernel(
 // inverse: read dWt, write the OIHW gradient (padded entries dropped).
 __global__ void __launch_bounds__(kThreads) weight_s2d_kernel(
     float* __restrict__ W, int o, int c, int k, int s, int cp, float* __restrict__ Wt, long long ld,
-    int inverse) {
+    int inverse, float* __restrict__ bias) {
   const int k2 = (k + s - 1) / s;
   const int sc = s * c;
+  if (inverse && bias) {   // bias-gradient row of OMNI_CONV_WGRAD_BIAS
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < o; i += gridDim.x * blockDim.x)
+      bias[i] = Wt[(long long)i * ld + (long long)k2 * k2 * cp];
+  }
   if (!inverse) {
     const long long total = (long long)o * ld;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -648,14 +652,16 @@ int omni_space_to_depth_f32(const float* X, int b, int n, int c, int cs, int s, 
 }
 
 int omni_conv_weight_s2d_f32(float* W, int o, int c, int k, int s, int cp, float* Wt, long long ld,
-                             int inverse, void* stream) {
+                             int inverse, float* bias, void* stream) {
   const int k2 = (k + s - 1) / s;
   OMNI_REQUIRE(o >= 1 && c >= 1 && k >= 1 && s >= 1 && cp >= s * s * c &&
                    ld >= (long long)k2 * k2 * cp,
                "weight s2d: bad shape");
+  OMNI_REQUIRE(!bias || (inverse && ld > (long long)k2 * k2 * cp),
+               "weight s2d: the bias column needs inverse=1 and ld > ceil(k/s)^2 * cp");
   const long long work = inverse ? (long long)o * c * k * k : (long long)o * ld;
   weight_s2d_kernel<<<omni::grid_for(work, kThreads), kThreads, 0, omni::as_stream(stream)>>>(
-      W, o, c, k, s, cp, Wt, ld, inverse);
+      W, o, c, k, s, cp, Wt, ld, inverse, bias);
   return omni::check_launch("conv_weight_s2d");
 }
 

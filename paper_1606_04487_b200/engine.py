@@ -73,6 +73,8 @@ class Op:
     Kc: int = 0
     Kf: int = 0
     ldK: int = 0
+    ldW: int = 0     # row pitch of the weight-gradient staging (room for the bias column)
+    wgrad_op: int = 1  # implicit layers: _abi.CONV_WGRAD, or CONV_WGRAD_BIAS (bias row folded in)
     w_inplace: bool = False
     implicit: bool = False
     s2d: tuple | None = None          # (stride, k2, pad2, n2, cp) of the space-to-depth form
@@ -163,7 +165,12 @@ class GpuNet:
                     op.ldK = K.round_up(op.Kf, 32)
                     op.dhat = z(self.b * m * m, op.ldK)
                 op.wstage = z(d, op.ldK)
-                op.dwstage = z(d, op.ldK)
+                op.ldW = op.ldK
+                if op.implicit and op.boff >= 0 and not os.environ.get("OMNI_NO_WGRAD_BIAS"):
+                    # bias gradient as one more row of the implicit wgrad GEMM (column Kf)
+                    op.wgrad_op = _abi.CONV_WGRAD_BIAS
+                    op.ldW = K.round_up(op.Kf + 1, 32)
+                op.dwstage = z(d, op.ldW)
                 first_param = False
                 i += 2 if nxt_relu else 1
             elif L.kind == "fc":
@@ -243,7 +250,7 @@ class GpuNet:
             else:
                 geo = (b, op.inp.n, op.c_in, op.k, op.s, op.p, d)
             need = max(K.conv_implicit_workspace_bytes(self.prec, _abi.CONV_FPROP, *geo),
-                       K.conv_implicit_workspace_bytes(self.prec, _abi.CONV_WGRAD, *geo))
+                       K.conv_implicit_workspace_bytes(self.prec, op.wgrad_op, *geo))
             if not op.first_param_layer:
                 need = max(need, K.conv_implicit_workspace_bytes(
                     self.prec, _abi.CONV_FPROP, b, op.m, d, op.k, 1, op.k - 1 - op.p, op.c_in))
@@ -303,7 +310,7 @@ class GpuNet:
         m = (n + 2 * p - k) // s + 1
         if op_code == _abi.CONV_FPROP:
             M, N, Kd = b * m * m, d, c * k * k
-        else:
+        else:   # (the bias row of CONV_WGRAD_BIAS is not counted as conv work)
             M, N, Kd = d, c * k * k, b * m * m
         self._timed(M, N, Kd, "conv", lambda: K.conv_implicit(
             op_code, X, c, k, s, p, d, G, ldg, Y, ldy, precision=self.prec, epilogue=epi,
@@ -470,15 +477,18 @@ class GpuNet:
                 if op.implicit:
                     with wgrad_stream():
                         X, c_, k_, s_, p_ = self._conv_input(op, b, transform=False)
-                        self._conv(_abi.CONV_WGRAD, X, c_, k_, s_, p_, d, dZ, op.out.cs,
-                                   op.dwstage, op.ldK)
+                        self._conv(op.wgrad_op, X, c_, k_, s_, p_, d, dZ, op.out.cs,
+                                   op.dwstage, op.ldW)
+                        fold = op.wgrad_op == _abi.CONV_WGRAD_BIAS
+                        gb = G[op.boff:op.boff + d] if fold else None
                         if op.s2d is not None:
                             K.conv_weight_s2d(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k,
-                                              op.s2d[0], op.s2d[4], op.dwstage, op.ldK, inverse=True)
+                                              op.s2d[0], op.s2d[4], op.dwstage, op.ldW, inverse=True,
+                                              bias=gb)
                         else:
                             K.conv_weight_to_tap(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k,
-                                                 op.dwstage, op.ldK, inverse=True)
-                        if op.boff >= 0:
+                                                 op.dwstage, op.ldW, inverse=True, bias=gb)
+                        if op.boff >= 0 and not fold:
                             K.bias_grad(dZ, op.out.cs, Mr, d, G[op.boff:op.boff + d], self.bias_ws)
                         done(op)
                     if op.first_param_layer:
@@ -539,33 +549,3 @@ class GpuNet:
         self.backward(b)
         return self.loss_buf, self.grad
 
-    def kernel_launches_per_step(self) -> int:
-        """Launches of libomni kernels in one gather + fwd + bwd + SGD step."""
-        n = 2 + 1 + 1  # gathers, softmax, sgd
-        for op in self.ops:
-            if op.kind == "conv" and op.implicit:
-                n += 1 + 1 + 1   # stage, implicit fprop, implicit wgrad
-                n += 1 if op.s2d is not None else 0   # space-to-depth of the input
-                n += 1 + (2 if op.boff >= 0 else 0)   # inverse stage, bias gradient
-                if not op.first_param_layer:
-                    n += 2       # flipped-weight stage, implicit dgrad (+ fused ReLU mask)
-            elif op.kind == "conv":
-                n += 1 + 1 + 1   # stage, lower, gemm
-                n += 1 + 1       # wgrad gemm (+ bias column), inverse stage
-                if not op.first_param_layer:
-                    n += 2       # dgrad gemm, col2im (+ fused ReLU mask)
-            elif op.kind == "fc":
-                n += (0 if op.w_inplace else 1) + 1 + (1 if op.flat is not op.inp else 0)
-                n += 1 + (2 if op.boff >= 0 else 0)
-                if not op.first_param_layer:
-                    n += 1 + (1 if op.flat is not op.inp else 0)
-            elif op.kind == "pool":
-                n += 1 + (1 if op.inp.grad is not None else 0)
-            elif op.kind == "relu":
-                n += 2
-        # split-K GEMMs add a reduction launch each
-        for op in self.ops:
-            for M, N, Kd in self._gemm_shapes(op, self.b):
-                s, _ = K.gemm_plan(self.prec, M, N, Kd)
-                n += 1 if s > 1 else 0
-        return n

@@ -195,7 +195,8 @@ def conv_implicit(op: int, X: torch.Tensor, c: int, k: int, stride: int, pad: in
                   bias: torch.Tensor | None = None, aux: torch.Tensor | None = None,
                   ld_aux: int = 0, workspace: torch.Tensor | None = None) -> torch.Tensor:
     """Implicit-GEMM conv (TMA im2col operands) -- see include/omni.h.  X is NHWC
-    (b, n, n, cs); op = _abi.CONV_FPROP or _abi.CONV_WGRAD."""
+    (b, n, n, cs); op = _abi.CONV_FPROP, _abi.CONV_WGRAD or _abi.CONV_WGRAD_BIAS (the
+    bias gradient lands in column k*k*c of Y)."""
     _require_cuda(X, G, Y)
     b, n, _, cs = X.shape
     m = (n + 2 * pad - k) // stride + 1
@@ -206,9 +207,9 @@ def conv_implicit(op: int, X: torch.Tensor, c: int, k: int, stride: int, pad: in
         _fits(Y, (pixels - 1) * ldy + d_out, "Y")
         if aux is not None:
             _fits(aux, (pixels - 1) * ld_aux + d_out, "aux")
-    else:                       # G: dY, pixels x ldg; Y: dW, d_out x ldy
+    else:                       # G: dY, pixels x ldg; Y: dW (+ bias column), d_out x ldy
         _fits(G, (pixels - 1) * ldg + d_out, "G")
-        _fits(Y, (d_out - 1) * ldy + taps, "Y")
+        _fits(Y, (d_out - 1) * ldy + taps + (op == _abi.CONV_WGRAD_BIAS), "Y")
     if bias is not None:
         _fits(bias, d_out, "bias")
     need = conv_implicit_workspace_bytes(precision, op, b, n, c, k, stride, pad, d_out)
@@ -300,8 +301,9 @@ def space_to_depth(X: torch.Tensor, c: int, s: int, Y: torch.Tensor) -> None:
 
 
 def conv_weight_s2d(W: torch.Tensor, o: int, c: int, k: int, s: int, cp: int, Wt: torch.Tensor,
-                    ld: int, inverse: bool = False) -> None:
-    call("omni_conv_weight_s2d_f32", _ptr(W), o, c, k, s, cp, _ptr(Wt), ld, int(inverse), _stream())
+                    ld: int, inverse: bool = False, bias: torch.Tensor | None = None) -> None:
+    call("omni_conv_weight_s2d_f32", _ptr(W), o, c, k, s, cp, _ptr(Wt), ld, int(inverse),
+         _ptr(bias), _stream())
 
 
 def transpose(src: torch.Tensor, lds: int, src_bstride: int, rows: int, cols: int,

@@ -396,6 +396,44 @@ def test_conv_implicit_wgrad(geom, prec):
     assert rel_err(dW[:, :Kc].cpu(), ref) < tol
 
 
+@pytest.mark.parametrize("geom", IMPLICIT_GEOMS + [(8, 13, 384, 3, 1, 1, 256)])
+@pytest.mark.parametrize("prec", ["tf32", "3xtf32"])
+def test_conv_implicit_wgrad_bias_row(geom, prec):
+    """OMNI_CONV_WGRAD_BIAS: the weight gradient plus the bias gradient (column
+    sums of dY) in column k*k*c, from one GEMM with a ones operand chunk."""
+    b, n, c, k, s, p, d = geom
+    X, _ = _conv_inputs(b, n, c, k, d, 14)
+    m = (n + 2 * p - k) // s + 1
+    Kc = c * k * k
+    ld = K.round_up(Kc + 1, 32)
+    dY = torch.randn(b * m * m, d, device=DEV)
+    dW = torch.full((d, ld), float("nan"), device=DEV)
+    pr = _abi.PRECISIONS[prec]
+    ws = torch.empty(max(1, K.conv_implicit_workspace_bytes(pr, _abi.CONV_WGRAD_BIAS, b, n, c, k,
+                                                            s, p, d)) // 4, device=DEV)
+    ws.fill_(float("nan"))   # the ones tile must be written by the call itself
+    K.conv_implicit(_abi.CONV_WGRAD_BIAS, X, c, k, s, p, d, dY, d, dW, ld, precision=pr,
+                    workspace=ws)
+    D = K.lower_nhwc(X, c, k, s, p, K.round_up(Kc, 32))
+    ref = (dY.double().t() @ D[:, :Kc].double()).cpu()
+    torch.cuda.synchronize()
+    tol = 3e-3 if prec == "tf32" else 5e-6 * max(1.0, (b * m * m / 1000) ** 0.5)
+    assert rel_err(dW[:, :Kc].cpu(), ref) < tol
+    assert rel_err(dW[:, Kc].cpu(), dY.double().sum(0).cpu()) < tol
+
+
+def test_conv_weight_s2d_inverse_bias_column():
+    o, c, k, s = 8, 3, 11, 4
+    k2, cp = -(-k // s), K.round_up(s * s * c, 32)
+    ld = K.round_up(k2 * k2 * cp + 1, 32)
+    Wt = torch.randn(o, ld, device=DEV)
+    W = torch.empty(o * c * k * k, device=DEV)
+    bias = torch.empty(o, device=DEV)
+    K.conv_weight_s2d(W, o, c, k, s, cp, Wt, ld, inverse=True, bias=bias)
+    torch.cuda.synchronize()
+    assert torch.equal(bias.cpu(), Wt[:, k2 * k2 * cp].cpu())
+
+
 @pytest.mark.parametrize("geom", [g for g in IMPLICIT_GEOMS if g[4] == 1 and g[6] % 32 == 0])
 def test_conv_implicit_dgrad_via_flipped_weights(geom):
     """Stride-1 data gradient as one implicit forward conv of dY with the flipped,
