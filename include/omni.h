@@ -130,8 +130,12 @@ int omni_conv_implicit_f32(int precision, int op, const float* X, int b, int n, 
  * (dy,dx) window order, argmax = input pixel index iy*w + ix, as
  * problems.py:213-216), mode 1 = average (Caffe semantics: divisor is the
  * window clipped to the padded extent).  ceil_mode selects Caffe's output size
- * rule.  Backward is a deterministic gather; if relu_mask_x != 0 the input
- * gradient is also multiplied by (X > 0) (fused ReLU mask, problems.py:261). */
+ * rule.  Backward is a deterministic gather; if relu_mask_x == 1 the input
+ * gradient is also multiplied by (X > 0) (fused ReLU mask, problems.py:261).
+ * relu_mask_x == 2 (max pool only): X is the pooled OUTPUT (b, oh, ow, cs_out)
+ * and each window's gradient is masked by (Y > 0) -- the same result, since
+ * gradient reaches only the argmax element and Y equals it, at 1/k^2-ish of
+ * the bytes.                                                                   */
 int omni_pool_out_size(int n, int k, int stride, int pad, int ceil_mode);
 int omni_pool_fwd_nhwc_f32(int mode, const float* X, int b, int h, int w, int c, int cs_in,
                            int k, int stride, int pad, int ceil_mode, float* Y, int cs_out,

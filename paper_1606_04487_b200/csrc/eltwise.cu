@@ -145,6 +145,17 @@ __global__ void __launch_bounds__(kThreads) pool_bwd_kernel(
           } else {
             a[0] = __ldg(argmax + (long long)o * c + ch);
           }
+          if (relu_mask_x == 2) {  // X holds the pooled output: mask by the window max
+            if (V == 4) {
+              const float4 t = __ldg(reinterpret_cast<const float4*>(X + (long long)o * cs_out + ch));
+              g[0] = t.x > 0.f ? g[0] : 0.f;
+              g[1 % V] = t.y > 0.f ? g[1 % V] : 0.f;
+              g[2 % V] = t.z > 0.f ? g[2 % V] : 0.f;
+              g[3 % V] = t.w > 0.f ? g[3 % V] : 0.f;
+            } else {
+              g[0] = __ldg(X + (long long)o * cs_out + ch) > 0.f ? g[0] : 0.f;
+            }
+          }
 #pragma unroll
           for (int v = 0; v < V; ++v)
             if (a[v] == me) acc[v] += g[v];
@@ -157,7 +168,7 @@ __global__ void __launch_bounds__(kThreads) pool_bwd_kernel(
         }
       }
     float* dst = dX + (long long)pix * cs_in + ch;
-    if (relu_mask_x) {
+    if (relu_mask_x == 1) {
       const float* xm = X + (long long)pix * cs_in + ch;
       if (V == 4) {
         const float4 t = __ldg(reinterpret_cast<const float4*>(xm));
@@ -223,6 +234,14 @@ __global__ void __launch_bounds__(kThreads) pool_bwd_s2_kernel(
         if (MODE == 0) {
           const int4 t = __ldg(reinterpret_cast<const int4*>(argmax + (long long)o * c + ch));
           const int av[4] = {t.x, t.y, t.z, t.w};
+          float gm[4] = {gv[0], gv[1], gv[2], gv[3]};
+          if (relu_mask_x == 2) {  // X holds the pooled output: mask by the window max
+            const float4 y = __ldg(reinterpret_cast<const float4*>(X + (long long)o * cs_out + ch));
+            gm[0] = y.x > 0.f ? gm[0] : 0.f;
+            gm[1] = y.y > 0.f ? gm[1] : 0.f;
+            gm[2] = y.z > 0.f ? gm[2] : 0.f;
+            gm[3] = y.w > 0.f ? gm[3] : 0.f;
+          }
 #pragma unroll
           for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -230,7 +249,7 @@ __global__ void __launch_bounds__(kThreads) pool_bwd_s2_kernel(
               const int me = (y0 + a) * w + (x0 + e);
 #pragma unroll
               for (int v = 0; v < 4; ++v)
-                if (av[v] == me) acc[a][e][v] += gv[v];
+                if (av[v] == me) acc[a][e][v] += gm[v];
             }
         } else {
           const int hs = oy * 2 - p, ws = ox * 2 - p;
@@ -255,7 +274,7 @@ __global__ void __launch_bounds__(kThreads) pool_bwd_s2_kernel(
         if (yy >= h || xx >= w) continue;
         const long long pix = (long long)img * h * w + (long long)yy * w + xx;
         float4 out = make_float4(acc[a][e][0], acc[a][e][1], acc[a][e][2], acc[a][e][3]);
-        if (relu_mask_x) {
+        if (relu_mask_x == 1) {
           const float4 m = __ldg(reinterpret_cast<const float4*>(X + pix * cs_in + ch));
           out.x = m.x > 0.f ? out.x : 0.f;
           out.y = m.y > 0.f ? out.y : 0.f;
@@ -524,14 +543,16 @@ int omni_pool_bwd_nhwc_f32(int mode, const float* dY, int b, int h, int w, int c
                    pad < k && cs_in >= c && cs_out >= c,
                "pool: bad geometry");
   OMNI_REQUIRE(mode == 1 || argmax != nullptr, "pool: max mode needs the forward argmax");
-  OMNI_REQUIRE(!relu_mask_x || X != nullptr, "pool: relu mask needs X");
+  OMNI_REQUIRE(relu_mask_x >= 0 && relu_mask_x <= 2 && (!relu_mask_x || X != nullptr),
+               "pool: relu mask needs X");
+  OMNI_REQUIRE(relu_mask_x != 2 || mode == 0, "pool: relu_mask_x = 2 (mask by the output) is max-pool only");
   const int oh = pool_out(h, k, stride, pad, ceil_mode), ow = pool_out(w, k, stride, pad, ceil_mode);
   const long long work = (long long)b * h * w * c;
   if (work == 0) return OMNI_OK;
   OMNI_REQUIRE((long long)b * h * w * cs_in < (1LL << 31), "pool: tensor too large for 32-bit indexing");
   cudaStream_t st = omni::as_stream(stream);
   const bool v4 = c % 4 == 0 && cs_in % 4 == 0 && cs_out % 4 == 0 && aligned16(dY) && aligned16(dX) &&
-                  (mode == 1 || aligned16(argmax)) && (!relu_mask_x || aligned16(X));
+                  (mode == 1 || aligned16(argmax)) && (!relu_mask_x || aligned16(X));  // X: cs_in or cs_out rows, both % 4
   // the blocked kernel visits 2 x 2 candidate windows per aligned 2x2 input
   // block: enough for k <= 3, and for k = 4 only with even padding (odd
   // padding puts a third window over the block)

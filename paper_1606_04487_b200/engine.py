@@ -520,9 +520,13 @@ class GpuNet:
                 if op.inp.grad is None:
                     continue
                 mode = 0 if L.mode == "max" else 1
+                if mode == 0 and op.inp.fused_relu:
+                    # max pool: the ReLU mask of the routed element is (pooled value > 0)
+                    xm, rm = op.out.value[:b], 2
+                else:
+                    xm, rm = op.inp.value, int(op.inp.fused_relu)
                 K.pool_bwd(mode, op.out.grad[:b], (b, op.inp.n, op.inp.n, op.inp.cs), op.inp.c,
-                           op.k, op.s, op.p, L.ceil, op.argmax, op.inp.value,
-                           op.inp.fused_relu, op.inp.grad)
+                           op.k, op.s, op.p, L.ceil, op.argmax, xm, rm, op.inp.grad)
             elif op.kind == "relu":
                 if op.inp.grad is None:
                     continue

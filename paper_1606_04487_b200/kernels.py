@@ -241,7 +241,9 @@ def pool_fwd(mode: int, X: torch.Tensor, c: int, k: int, stride: int, pad: int, 
 
 def pool_bwd(mode: int, dY: torch.Tensor, X_shape, c: int, k: int, stride: int, pad: int,
              ceil_mode: bool, argmax: torch.Tensor | None, X: torch.Tensor | None,
-             relu_mask: bool, dX: torch.Tensor) -> None:
+             relu_mask: int, dX: torch.Tensor) -> None:
+    """relu_mask: 0 none, 1 mask by (X > 0) with X the pool input, 2 (max pool)
+    mask by (Y > 0) with X the pooled output -- see include/omni.h."""
     b, h, w, cs_in = X_shape
     call("omni_pool_bwd_nhwc_f32", mode, _ptr(dY), b, h, w, c, cs_in, k, stride, pad,
          int(ceil_mode), dY.shape[3], _ptr(argmax), _ptr(X), int(relu_mask), _ptr(dX), _stream())

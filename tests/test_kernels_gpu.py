@@ -257,6 +257,26 @@ def test_pool_fwd_bwd(mode, geom):
     assert torch.allclose(dX.cpu().double(), Xa.grad, rtol=1e-5, atol=1e-5)
 
 
+@pytest.mark.parametrize("geom", [(2, 55, 55, 96, 3, 2, 0, True), (2, 13, 13, 20, 2, 2, 0, True),
+                                  (2, 9, 9, 8, 3, 2, 1, False), (1, 7, 7, 3, 3, 3, 1, True)])
+def test_maxpool_bwd_output_mask_equals_input_mask(geom):
+    """relu_mask_x = 2 (mask by the pooled output) is bit-identical to masking
+    the routed gradient by the ReLU'd input: the routed element is the max."""
+    b, h, w, c, k, s, p, ceil_mode = geom
+    gen = torch.Generator().manual_seed(21)
+    X = torch.randn(b, h, w, c, generator=gen).clamp_min(0).to(DEV)   # post-ReLU (many zeros)
+    oh, ow = K.pool_out_size(h, k, s, p, ceil_mode), K.pool_out_size(w, k, s, p, ceil_mode)
+    Y = torch.empty(b, oh, ow, c, device=DEV)
+    am = torch.empty(b * oh * ow * c, dtype=torch.int32, device=DEV)
+    K.pool_fwd(0, X, c, k, s, p, ceil_mode, Y, am)
+    dY = torch.randn(b, oh, ow, c, generator=gen).to(DEV)
+    d1, d2 = torch.empty_like(X), torch.empty_like(X)
+    K.pool_bwd(0, dY, X.shape, c, k, s, p, ceil_mode, am, X, 1, d1)
+    K.pool_bwd(0, dY, X.shape, c, k, s, p, ceil_mode, am, Y, 2, d2)
+    torch.cuda.synchronize()
+    assert torch.equal(d1.cpu(), d2.cpu())
+
+
 def test_softmax_xent():
     b, C = 37, 1000
     gen = torch.Generator().manual_seed(2)
