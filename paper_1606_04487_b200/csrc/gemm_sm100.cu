@@ -771,7 +771,7 @@ __global__ void fill_ones_kernel(float* __restrict__ p, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = 1.f;
 }
 
-// Split-K reduction: C[i,j] = epi(sum_s ws[s][i][j]) in ascending s.
+// Generic (scalar) split-K reduction.
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int S,
                                                             int M, int N, Params p) {
   const long long total = (long long)M * N;
@@ -789,6 +789,94 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
     }
   }
 }
+
+// Split-K reductions: C[i,j] = epi(sum_s ws[s][i][j]) in ascending s (the same
+// order in every variant, so results do not depend on which one runs).
+// Natural store, 4 columns per thread (N, ldc % 4 == 0, C 16-byte aligned).
+template <int MODE>
+__global__ void __launch_bounds__(256) splitk_reduce_v4_kernel(const float* __restrict__ ws, int S,
+                                                               int M, int N, Params p) {
+  const int n4 = N >> 2;
+  const int total = M * n4;
+  const long long MN = (long long)M * N;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int row = i / n4;
+    const int col = (i - row * n4) << 2;
+    const float* src = ws + (long long)row * N + col;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);  // 0 + sum, as the generic kernel
+    for (int sp = 0; sp < S; ++sp) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(src + sp * MN));
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    float* Crow = p.C + (long long)row * p.ldc;
+    float4 out;
+    out.x = epi_one<MODE>(acc.x, p, row, col, Crow);
+    out.y = epi_one<MODE>(acc.y, p, row, col + 1, Crow);
+    out.z = epi_one<MODE>(acc.z, p, row, col + 2, Crow);
+    out.w = epi_one<MODE>(acc.w, p, row, col + 3, Crow);
+    *reinterpret_cast<float4*>(Crow + col) = out;
+  }
+}
+
+// Transposed store C[j*ldc + i] (weight gradients with im2col as A) through a
+// 32 x 32 shared-memory tile: coalesced partial reads and C^T writes.
+template <int MODE>
+__global__ void __launch_bounds__(256) splitk_reduce_t_kernel(const float* __restrict__ ws, int S,
+                                                              int M, int N, Params p) {
+  __shared__ float tile[32][33];
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const long long MN = (long long)M * N;
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const int i = i0 + r, j = j0 + tx;
+    float acc = 0.f;
+    if (i < M && j < N) {
+      const float* src = ws + (long long)i * N + j;
+      for (int sp = 0; sp < S; ++sp) acc += src[sp * MN];
+    }
+    tile[r][tx] = acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const int j = j0 + r, i = i0 + tx;
+    if (i < M && j < N) p.C[(long long)j * p.ldc + i] = epi_one<MODE>(tile[tx][r], p, i, j, nullptr);
+  }
+}
+
+int launch_splitk_reduce(const float* ws, int S, int M, int N, const Params& q, cudaStream_t st) {
+  const bool v4 = !q.transpose_c && N % 4 == 0 && q.ldc % 4 == 0 && ((uintptr_t)q.C & 15) == 0 &&
+                  (long long)M * (N / 4) < (1LL << 31);
+#define OMNI_REDUCE_MODES(KERNEL, GRID, BLOCK)                                                   \
+  switch (q.epilogue) {                                                                        \
+    case OMNI_EPI_BIAS: KERNEL<OMNI_EPI_BIAS><<<GRID, BLOCK, 0, st>>>(ws, S, M, N, q); break;   \
+    case OMNI_EPI_BIAS_RELU:                                                                   \
+      KERNEL<OMNI_EPI_BIAS_RELU><<<GRID, BLOCK, 0, st>>>(ws, S, M, N, q);                      \
+      break;                                                                                   \
+    case OMNI_EPI_ACCUM: KERNEL<OMNI_EPI_ACCUM><<<GRID, BLOCK, 0, st>>>(ws, S, M, N, q); break; \
+    case OMNI_EPI_MASK_AUX:                                                                    \
+      KERNEL<OMNI_EPI_MASK_AUX><<<GRID, BLOCK, 0, st>>>(ws, S, M, N, q);                       \
+      break;                                                                                   \
+    case OMNI_EPI_RELU: KERNEL<OMNI_EPI_RELU><<<GRID, BLOCK, 0, st>>>(ws, S, M, N, q); break;   \
+    default: KERNEL<OMNI_EPI_STORE><<<GRID, BLOCK, 0, st>>>(ws, S, M, N, q); break;            \
+  }
+  if (q.transpose_c) {
+    const dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 31) / 32));
+    OMNI_REDUCE_MODES(splitk_reduce_t_kernel, grid, 256)
+  } else if (v4) {
+    const int grid = omni::grid_for((long long)M * (N / 4), 256);
+    OMNI_REDUCE_MODES(splitk_reduce_v4_kernel, grid, 256)
+  } else {
+    splitk_reduce_kernel<<<omni::grid_for((long long)M * N, 256), 256, 0, st>>>(ws, S, M, N, q);
+  }
+#undef OMNI_REDUCE_MODES
+  return omni::check_launch("splitk_reduce");
+}
+
 
 // CUDA-core fp32 reference GEMM (OMNI_PREC_FP32_SIMT): 16x16 tiles through
 // shared memory.  Test reference only; never on the training path.
@@ -1216,9 +1304,7 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
     q.C = C;
     q.ldc = ldc;
     q.transpose_c = (im2col == 3 || im2col == 4);
-    splitk_reduce_kernel<<<omni::grid_for((long long)M * N, 256), 256, 0, st>>>(workspace,
-                                                                              pl.splits, M, N, q);
-    rc = omni::check_launch("splitk_reduce");
+    rc = launch_splitk_reduce(workspace, pl.splits, M, N, q, st);
   }
   return rc;
 }
