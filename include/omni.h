@@ -189,6 +189,10 @@ int omni_conv_weight_flip_f32(const float* W, int o, int c, int k, float* Wf, lo
  * stride-1 ceil(k/s) x ceil(k/s) conv of Y with the weights below.            */
 int omni_space_to_depth_f32(const float* X, int b, int n, int c, int cs, int s, float* Y, int n2,
                             int cp, void* stream);
+/* Same, fused with the batch gather: image i of Y is image idx[i] of the
+ * dataset X (the device-resident sample, problems.py:197-199).               */
+int omni_space_to_depth_gather_f32(const float* X, const int64_t* idx, int b, int n, int c, int cs,
+                                   int s, float* Y, int n2, int cp, void* stream);
 /* Weights of that conv, tap-major rows Wt (o x ld, ld >= ceil(k/s)^2 * cp):
  * Wt[o*ld + (kx2*k2 + ky2)*cp + (dx*s + dy)*c + ch] = W[o, ch, s*kx2+dx, s*ky2+dy]
  * (0 past the kernel).  inverse=1 maps a gradient in that layout back to OIHW

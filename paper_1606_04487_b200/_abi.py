@@ -80,6 +80,7 @@ SIGNATURES: dict[str, tuple] = {
     "omni_gather_i32": (_I, [_P, _P, _I, _P, _P]),
     "omni_conv_weight_to_tap_f32": (_I, [_P, _I, _I, _I, _P, _L, _I, _P, _P]),
     "omni_space_to_depth_f32": (_I, [_P, _I, _I, _I, _I, _I, _P, _I, _I, _P]),
+    "omni_space_to_depth_gather_f32": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P]),
     "omni_conv_weight_s2d_f32": (_I, [_P, _I, _I, _I, _I, _I, _P, _L, _I, _P, _P]),
     "omni_transpose_f32": (_I, [_P, _L, _L, _I, _I, _P, _L, _L, _I, _P]),
     "omni_fill_f32": (_I, [_P, _F, _L, _P]),

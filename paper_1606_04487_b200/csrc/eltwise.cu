@@ -286,19 +286,26 @@ __global__ void __launch_bounds__(kThreads) pool_bwd_s2_kernel(
   }
 }
 
-// Softmax cross-entropy: one CTA of 32 warps; warp w owns rows w, w+32, ...
-// Row losses are summed per warp in row order, then across warps in warp
-// order: a fixed reduction tree, so the loss is bit-reproducible.
+// Softmax cross-entropy, one warp per row.
+// Launched as ONE cluster of kSoftmaxCtas CTAs (32 warps each): global warp
+// g = rank*32 + warp owns rows g, g + 32*kSoftmaxCtas, ...; each CTA sums its
+// warps in order, then CTA 0 sums the CTA partials in rank order through
+// distributed shared memory -- a fixed tree, so the loss is bit-reproducible.
+constexpr int kSoftmaxCtas = 8;
 __global__ void __launch_bounds__(1024) softmax_xent_kernel(
     const float* __restrict__ Z, long long ld, const int32_t* __restrict__ y, int b, int C,
     float* __restrict__ loss, float* __restrict__ dZ, long long ldd, float scale) {
   __shared__ float warp_loss[32];
+  __shared__ float cta_loss;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int gwarp = (int)rank * 32 + warp, nwarps = 32 * (int)gridDim.x;
   float my_loss = 0.f;
   if (C <= 1024) {
     // each lane keeps its <= 32 logits in registers: one batch of independent
     // loads per row instead of three dependent sweeps over memory
-    for (int row = warp; row < b; row += 32) {
+    for (int row = gwarp; row < b; row += nwarps) {
       const float* z = Z + (long long)row * ld;
       float v[32];
       float mx = -INFINITY;
@@ -331,7 +338,7 @@ __global__ void __launch_bounds__(1024) softmax_xent_kernel(
       }
     }
   } else
-  for (int row = warp; row < b; row += 32) {
+  for (int row = gwarp; row < b; row += nwarps) {
     const float* z = Z + (long long)row * ld;
     float mx = -INFINITY;
     for (int j = lane; j < C; j += 32) mx = fmaxf(mx, z[j]);
@@ -358,8 +365,25 @@ __global__ void __launch_bounds__(1024) softmax_xent_kernel(
   if (threadIdx.x == 0) {
     float tot = 0.f;
     for (int i = 0; i < 32; ++i) tot += warp_loss[i];
+    cta_loss = tot;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
+  if (rank == 0 && threadIdx.x == 0) {
+    const uint32_t local = (uint32_t)__cvta_generic_to_shared(&cta_loss);
+    float tot = 0.f;
+    for (unsigned r = 0; r < gridDim.x; ++r) {
+      uint32_t remote;
+      float v;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(r));
+      asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+      tot += v;
+    }
     loss[0] = tot / (float)b;
   }
+  // keep every CTA's shared memory alive until CTA 0 has read it
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
 }
 
 __global__ void __launch_bounds__(kThreads) relu_fwd_kernel(const float* __restrict__ X,
@@ -584,8 +608,19 @@ int omni_softmax_xent_f32(const float* logits, long long ld, const int32_t* labe
                           float* loss, float* dlogits, long long ldd, float scale, void* stream) {
   OMNI_REQUIRE(b >= 1 && C >= 1 && ld >= C && (dlogits == nullptr || ldd >= C),
                "softmax_xent: bad shape");
-  softmax_xent_kernel<<<1, 1024, 0, omni::as_stream(stream)>>>(logits, ld, labels, b, C, loss,
-                                                               dlogits, ldd, scale);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kSoftmaxCtas);
+  cfg.blockDim = dim3(1024);
+  cfg.stream = omni::as_stream(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kSoftmaxCtas;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  OMNI_CUDA_TRY(cudaLaunchKernelEx(&cfg, softmax_xent_kernel, logits, ld, labels, b, C, loss,
+                                   dlogits, ldd, scale));
   return omni::check_launch("softmax_xent");
 }
 

@@ -301,9 +301,10 @@ __global__ void __launch_bounds__(kThreads) weight_flip_kernel(
 // (0 outside the image or for padded channels).  A stride-s k x k conv of X
 // is then a stride-1 ceil(k/s)^2 conv of Y with s*s*c (-> cp) channels, which
 // tiles the 32-channel TMA im2col boxes of the implicit GEMM.
+// idx != nullptr: image img of Y is image idx[img] of X (fused batch gather).
 __global__ void __launch_bounds__(kThreads) space_to_depth_kernel(
-    const float* __restrict__ X, int b, int n, int c, int cs, int s, float* __restrict__ Y, int n2,
-    int cp) {
+    const float* __restrict__ X, const int64_t* __restrict__ idx, int b, int n, int c, int cs,
+    int s, float* __restrict__ Y, int n2, int cp) {
   // one block per output row (img, X2); shared decode table j -> (dx, dy, ch)
   extern __shared__ int s2d_tab[];
   const int sc = s * c;
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(kThreads) space_to_depth_kernel(
   __syncthreads();
   for (int row = blockIdx.x; row < b * n2; row += gridDim.x) {
     const int img = row / n2, X2 = row - (row / n2) * n2;
-    const float* Xi = X + (long long)img * n * n * cs;
+    const float* Xi = X + (idx ? idx[img] : (long long)img) * n * n * cs;
     float* out = Y + (long long)row * n2 * cp;
     const int total = n2 * cp;
     // 4 independent loads in flight per thread before the (coalesced) stores
@@ -352,8 +353,8 @@ __global__ void __launch_bounds__(kThreads) space_to_depth_kernel(
 // 4 contiguous input floats of one input row; table per group: (dx, dy of the
 // group's first element, offset within the s-pixel run).
 __global__ void __launch_bounds__(kThreads) space_to_depth_v4_kernel(
-    const float* __restrict__ X, int b, int n, int c, int s, float* __restrict__ Y, int n2,
-    int cp) {
+    const float* __restrict__ X, const int64_t* __restrict__ idx, int b, int n, int c, int s,
+    float* __restrict__ Y, int n2, int cp) {
   extern __shared__ int s2d_tab[];
   const int sc = s * c, g4 = cp / 4;
   for (int t = threadIdx.x; t < g4; t += blockDim.x) {
@@ -368,6 +369,7 @@ __global__ void __launch_bounds__(kThreads) space_to_depth_v4_kernel(
   __syncthreads();
   for (int row = blockIdx.x; row < b * n2; row += gridDim.x) {
     const int img = row / n2, X2 = row - (row / n2) * n2;
+    const long long src_img = idx ? idx[img] : (long long)img;
     float4* out = reinterpret_cast<float4*>(Y + (long long)row * n2 * cp);
     const int total = n2 * g4;
     for (int q0 = threadIdx.x; q0 < total; q0 += 2 * blockDim.x) {
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__(kThreads) space_to_depth_v4_kernel(
           const int ix = s * X2 + (e >> 16);
           if (e >= 0 && ix < n) {
             const int off = e & 0xffff;
-            const float* src = X + (((long long)img * n + ix) * n + (long long)s * Y2) * c + off;
+            const float* src = X + ((src_img * n + ix) * n + (long long)s * Y2) * c + off;
             const int iy0 = s * Y2 + off / c;   // pixel of the first element; others may spill past n
             float a[4];
 #pragma unroll
@@ -631,8 +633,8 @@ int omni_conv_weight_flip_f32(const float* W, int o, int c, int k, float* Wf, lo
   return omni::check_launch("conv_weight_flip");
 }
 
-int omni_space_to_depth_f32(const float* X, int b, int n, int c, int cs, int s, float* Y, int n2,
-                            int cp, void* stream) {
+static int space_to_depth(const float* X, const int64_t* idx, int b, int n, int c, int cs, int s,
+                          float* Y, int n2, int cp, void* stream) {
   OMNI_REQUIRE(b >= 0 && n >= 1 && c >= 1 && cs >= c && s >= 1 && n2 * s >= n && cp >= s * s * c &&
                    cp % 4 == 0 && ((uintptr_t)Y % 16) == 0,
                "space_to_depth: bad shape");
@@ -644,11 +646,22 @@ int omni_space_to_depth_f32(const float* X, int b, int n, int c, int cs, int s, 
   const int grid = rows < omni::sm_count_cached(dev) * 16 ? rows : omni::sm_count_cached(dev) * 16;
   if (cs == c && (s * c) % 4 == 0)
     space_to_depth_v4_kernel<<<grid, kThreads, (cp / 4) * sizeof(int), omni::as_stream(stream)>>>(
-        X, b, n, c, s, Y, n2, cp);
+        X, idx, b, n, c, s, Y, n2, cp);
   else
     space_to_depth_kernel<<<grid, kThreads, cp * sizeof(int), omni::as_stream(stream)>>>(
-        X, b, n, c, cs, s, Y, n2, cp);
+        X, idx, b, n, c, cs, s, Y, n2, cp);
   return omni::check_launch("space_to_depth");
+}
+
+int omni_space_to_depth_f32(const float* X, int b, int n, int c, int cs, int s, float* Y, int n2,
+                            int cp, void* stream) {
+  return space_to_depth(X, nullptr, b, n, c, cs, s, Y, n2, cp, stream);
+}
+
+int omni_space_to_depth_gather_f32(const float* X, const int64_t* idx, int b, int n, int c, int cs,
+                                   int s, float* Y, int n2, int cp, void* stream) {
+  OMNI_REQUIRE(idx != nullptr, "space_to_depth_gather: idx is NULL");
+  return space_to_depth(X, idx, b, n, c, cs, s, Y, n2, cp, stream);
 }
 
 int omni_conv_weight_s2d_f32(float* W, int o, int c, int k, int s, int cp, float* Wt, long long ld,

@@ -229,6 +229,7 @@ class GpuNet:
         self.gemm_ws = z(max(ws // 4, 4))
         self.gemm_ws_side = z(max(ws // 4, 4))   # weight-gradient GEMMs run on a side stream
         self._ws_active = self.gemm_ws
+        self._s2d_ready = 0   # batch size whose space-to-depth input gather_batch wrote
         self.side_stream = torch.cuda.Stream(device=self.device)
         self.bias_ws = z(max(bws, 4))
         self.ddhat = z(max(dd, 4))
@@ -301,7 +302,10 @@ class GpuNet:
             return op.inp.value[:b], op.c_in, op.k, op.s, op.p
         st, k2, p2, n2, cp = op.s2d
         if transform:
-            K.space_to_depth(op.inp.value[:b], op.c_in, st, op.s2d_buf[:b])
+            if self._s2d_ready == b and op.inp is self.input:
+                self._s2d_ready = 0          # written by the fused gather
+            else:
+                K.space_to_depth(op.inp.value[:b], op.c_in, st, op.s2d_buf[:b])
         return op.s2d_buf[:b], cp, k2, 1, p2
 
     def _conv(self, op_code, X, c, k, s, p, d, G, ldg, Y, ldy, epi=_abi.EPI_STORE, bias=None,
@@ -539,13 +543,23 @@ class GpuNet:
     # ------------------------------------------------------------- input --
     def load_batch(self, X_nhwc: torch.Tensor, y: torch.Tensor) -> None:
         b = X_nhwc.shape[0]
+        self._s2d_ready = 0
         self.input.value[:b].copy_(X_nhwc)
         self.labels[:b].copy_(y)
 
     def gather_batch(self, data: torch.Tensor, labels: torch.Tensor, idx: torch.Tensor) -> None:
         """Device gather of a sampled batch (problems.py:197-199) from a
-        device-resident NHWC dataset."""
-        K.gather_rows(data, idx, self.input.value)
+        device-resident NHWC dataset.  When the first layer runs on the
+        space-to-depth form of the input, the gather writes that form directly
+        (one fused pass; the raw input buffer is not materialised)."""
+        first = self.ops[0] if self.ops else None
+        if (first is not None and first.kind == "conv" and first.s2d is not None
+                and first.inp is self.input and idx.dtype == torch.int64):
+            K.space_to_depth_gather(data, idx, first.c_in, first.s2d[0],
+                                    first.s2d_buf[:idx.numel()])
+            self._s2d_ready = idx.numel()
+        else:
+            K.gather_rows(data, idx, self.input.value)
         K.gather_i32(labels, idx, self.labels)
 
     def loss_and_grad(self, W: torch.Tensor, b: int | None = None):

@@ -302,6 +302,19 @@ def space_to_depth(X: torch.Tensor, c: int, s: int, Y: torch.Tensor) -> None:
          _stream())
 
 
+def space_to_depth_gather(data: torch.Tensor, idx: torch.Tensor, c: int, s: int,
+                          Y: torch.Tensor) -> None:
+    """Y[i] = space_to_depth(data[idx[i]]): batch gather fused into the transform."""
+    _require_cuda(data, idx, Y)
+    if idx.dtype != torch.int64:
+        raise ValueError("idx must be int64")
+    _, n, _, cs = data.shape
+    b = idx.numel()
+    _fits(Y, b * Y.shape[1] * Y.shape[2] * Y.shape[3], "Y")
+    call("omni_space_to_depth_gather_f32", _ptr(data), _ptr(idx), b, n, c, cs, s, _ptr(Y),
+         Y.shape[1], Y.shape[3], _stream())
+
+
 def conv_weight_s2d(W: torch.Tensor, o: int, c: int, k: int, s: int, cp: int, Wt: torch.Tensor,
                     ld: int, inverse: bool = False, bias: torch.Tensor | None = None) -> None:
     call("omni_conv_weight_s2d_f32", _ptr(W), o, c, k, s, cp, _ptr(Wt), ld, int(inverse),

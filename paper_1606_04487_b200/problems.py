@@ -180,6 +180,7 @@ class DeviceSession:
         eng = self.engine
         own = (eng.input.value, eng.labels)
         eng.input.value, eng.labels = self._slots[slot]   # consume the staged buffers in place
+        eng._s2d_ready = 0                                # the input comes from the slot
         try:
             self._compute(wr, b)
         finally:

@@ -544,6 +544,19 @@ def test_conv_implicit_fprop_transposed_form(epi, monkeypatch):
         assert rel_err(Y, ref) < 5e-6 * max(1.0, (c * k * k / 1000) ** 0.5)
 
 
+def test_space_to_depth_gather_equals_gather_then_transform():
+    gen = torch.Generator().manual_seed(43)
+    data = torch.randn(20, 27, 27, 3, generator=gen).to(DEV)
+    idx = torch.tensor([5, 0, 19, 5, 7], dtype=torch.int64, device=DEV)
+    s, n2, cp = 4, 7, 64
+    Y1 = torch.full((5, n2, n2, cp), float("nan"), device=DEV)
+    Y2 = torch.full((5, n2, n2, cp), float("nan"), device=DEV)
+    K.space_to_depth_gather(data, idx, 3, s, Y1)
+    K.space_to_depth(data[idx], 3, s, Y2)
+    torch.cuda.synchronize()
+    assert torch.equal(Y1.cpu(), Y2.cpu())
+
+
 def test_space_to_depth_conv1_large_batch():
     """CaffeNet conv1 geometry at a batch where the implicit GEMM spans all SMs."""
     b, n, c, k, s, d = 8, 227, 3, 11, 4, 96
