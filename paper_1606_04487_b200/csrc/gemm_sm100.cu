@@ -823,29 +823,27 @@ __global__ void __launch_bounds__(256) splitk_reduce_v4_kernel(const float* __re
 
 // Transposed store C[j*ldc + i] (weight gradients with im2col as A) through a
 // 32 x 32 shared-memory tile: coalesced partial reads and C^T writes.
+// One thread per element (1024-thread blocks): the split loop is the long,
+// dependent part, so it gets all the parallelism.
 template <int MODE>
-__global__ void __launch_bounds__(256) splitk_reduce_t_kernel(const float* __restrict__ ws, int S,
-                                                              int M, int N, Params p) {
+__global__ void __launch_bounds__(1024) splitk_reduce_t_kernel(const float* __restrict__ ws, int S,
+                                                               int M, int N, Params p) {
   __shared__ float tile[32][33];
   const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const long long MN = (long long)M * N;
-#pragma unroll
-  for (int r = ty; r < 32; r += 8) {
-    const int i = i0 + r, j = j0 + tx;
+  {
+    const int i = i0 + ty, j = j0 + tx;
     float acc = 0.f;
     if (i < M && j < N) {
       const float* src = ws + (long long)i * N + j;
       for (int sp = 0; sp < S; ++sp) acc += src[sp * MN];
     }
-    tile[r][tx] = acc;
+    tile[ty][tx] = acc;
   }
   __syncthreads();
-#pragma unroll
-  for (int r = ty; r < 32; r += 8) {
-    const int j = j0 + r, i = i0 + tx;
-    if (i < M && j < N) p.C[(long long)j * p.ldc + i] = epi_one<MODE>(tile[tx][r], p, i, j, nullptr);
-  }
+  const int j = j0 + ty, i = i0 + tx;
+  if (i < M && j < N) p.C[(long long)j * p.ldc + i] = epi_one<MODE>(tile[tx][ty], p, i, j, nullptr);
 }
 
 int launch_splitk_reduce(const float* ws, int S, int M, int N, const Params& q, cudaStream_t st) {
@@ -866,7 +864,7 @@ int launch_splitk_reduce(const float* ws, int S, int M, int N, const Params& q, 
   }
   if (q.transpose_c) {
     const dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 31) / 32));
-    OMNI_REDUCE_MODES(splitk_reduce_t_kernel, grid, 256)
+    OMNI_REDUCE_MODES(splitk_reduce_t_kernel, grid, 1024)
   } else if (v4) {
     const int grid = omni::grid_for((long long)M * (N / 4), 256);
     OMNI_REDUCE_MODES(splitk_reduce_v4_kernel, grid, 256)

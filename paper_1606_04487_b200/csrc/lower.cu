@@ -372,10 +372,10 @@ __global__ void __launch_bounds__(kThreads) space_to_depth_v4_kernel(
     const long long src_img = idx ? idx[img] : (long long)img;
     float4* out = reinterpret_cast<float4*>(Y + (long long)row * n2 * cp);
     const int total = n2 * g4;
-    for (int q0 = threadIdx.x; q0 < total; q0 += 2 * blockDim.x) {
-      float4 v[2];
+    for (int q0 = threadIdx.x; q0 < total; q0 += 4 * blockDim.x) {
+      float4 v[4];  // 4 independent 16-byte loads in flight per thread
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < 4; ++u) {
         const int q = q0 + u * blockDim.x;
         float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
         if (q < total) {
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kThreads) space_to_depth_v4_kernel(
         v[u] = r;
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < 4; ++u)
         if (q0 + u * blockDim.x < total) out[q0 + u * blockDim.x] = v[u];
     }
   }
