@@ -42,6 +42,7 @@ struct Params {
   int raster_m_inner;
   int epilogue;
   int vec_ok;         // C row stride % 4 == 0 and C 16-byte aligned
+  int vec_aux;        // aux row stride % 4 == 0 and aux 16-byte aligned
   int use_tma_store;  // epilogue stages 32x32 sub-tiles in smem and TMA-stores them
   float* C;
   long long ldc;
@@ -333,6 +334,19 @@ __device__ __forceinline__ float epi_apply(int mode, float acc, const Params& p,
 template <int MODE, int N>
 __device__ __forceinline__ void epi_chunk_t(float (&v)[N], const uint32_t* r, const Params& p,
                                             int row, int col0) {
+  if (MODE == OMNI_EPI_MASK_AUX && p.vec_aux && !p.transpose_c && row < p.M && col0 + N <= p.N) {
+    // each lane owns one row: read its N mask values as 16-byte vectors
+    const float4* a = reinterpret_cast<const float4*>(p.aux + (long long)row * p.ld_aux + col0);
+#pragma unroll
+    for (int q = 0; q < N / 4; ++q) {
+      const float4 m = __ldg(a + q);
+      v[4 * q] = m.x > 0.f ? __uint_as_float(r[4 * q]) : 0.f;
+      v[4 * q + 1] = m.y > 0.f ? __uint_as_float(r[4 * q + 1]) : 0.f;
+      v[4 * q + 2] = m.z > 0.f ? __uint_as_float(r[4 * q + 2]) : 0.f;
+      v[4 * q + 3] = m.w > 0.f ? __uint_as_float(r[4 * q + 3]) : 0.f;
+    }
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < N; ++j) v[j] = epi_one<MODE>(__uint_as_float(r[j]), p, row, col0 + j, nullptr);
 }
@@ -1239,6 +1253,7 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
   p.bias = bias;
   p.aux = aux;
   p.ld_aux = ld_aux;
+  p.vec_aux = aux && ld_aux % 4 == 0 && ((uintptr_t)aux & 15) == 0;
   // The implicit weight gradient (im2col A, both operands MN-major) runs 64-deep
   // K stages in TF32 mode: half the TMA ops per byte, 64-pixel im2col boxes.
   const int bkt = im2col == 3 ? wgrad_bkt(precision) : BK;
