@@ -315,12 +315,17 @@ def run_ours(args):
                     dist.barrier()
                 t0 = time.perf_counter()
             sess.prefetch(host[0])
+            fut = None
             for i in range(n_e2e if rep else 3):
                 hb = host[i % 2]
                 sess.step(hb)                     # consumes the prefetched copy
                 sess.prefetch(host[(i + 1) % 2])  # next batch's H2D overlaps this step
-                _ = sess.last_loss()              # D2H of the step's loss (syncs the host)
+                nxt = sess.loss_future()          # D2H of this step's loss, async
+                if fut is not None:
+                    _ = fut.result()              # previous step's loss on the host
+                fut = nxt
             sess.step(host[(n_e2e if rep else 3) % 2])   # drain the last prefetch
+            _ = fut.result()
             _ = sess.last_loss()
         torch.cuda.synchronize()
         n_e2e += 1
@@ -333,7 +338,8 @@ def run_ours(args):
                "h2d_bytes_per_step": host[0].X.numel() * 4 + host[0].y.numel() * 4,
                "d2h_bytes_per_step": 4,
                "path": "CNNProblem.device_session(): prefetch(HostBatch(pinned X, y)) on a copy "
-                       "stream overlapping step(); last_loss() each step"}
+                       "stream overlapping step(); every step's loss read on the host via "
+                       "loss_future() (async D2H, read one step later)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

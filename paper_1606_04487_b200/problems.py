@@ -89,6 +89,17 @@ class DeviceBatch:
         return int(self.idx.numel())
 
 
+class LossFuture:
+    """A step's loss on its way to the host (DeviceSession.loss_future)."""
+
+    def __init__(self, buf: torch.Tensor, event):
+        self._buf, self._event = buf, event
+
+    def result(self) -> float:
+        self._event.synchronize()
+        return float(self._buf[0])
+
+
 class DeviceSession:
     """W, V resident in HBM; one step = batch load + forward + backward + K8.
 
@@ -248,6 +259,17 @@ class DeviceSession:
     def last_loss(self) -> float:
         """Mean loss of the last step's batch (one 4-byte device-to-host read)."""
         return float(self.engine.loss_buf.item())
+
+    def loss_future(self) -> "LossFuture":
+        """Start the device-to-host copy of the last step's loss without
+        blocking: ``.result()`` waits for that step only, so a caller that reads
+        step i's loss after enqueuing step i+1 never drains the GPU pipeline."""
+        # each future owns its pinned scalar (torch's caching host allocator)
+        dst = torch.empty(1, dtype=torch.float32, pin_memory=True)
+        dst.copy_(self.engine.loss_buf.view(-1)[:1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return LossFuture(dst, ev)
 
     def state(self) -> SGDState:
         return SGDState(W=self.W.double().cpu().numpy(), V=self.V.double().cpu().numpy(), t=self.t)

@@ -57,3 +57,17 @@ def test_prefetched_host_batches_equal_device_batches():
             b.prefetch(hbs[i + 1])
     torch.cuda.synchronize()
     assert torch.equal(a.W, b.W) and torch.equal(a.V, b.V)
+
+
+def test_loss_future_matches_last_loss():
+    prob = CNNProblem("lenet", n_examples=32, seed=3, precision="tf32")
+    hp = P.Hyperparams(eta=0.01, mu=0.9, b=8)
+    sess = prob.device_session(prob.initial_state(), hp)
+    futs, sync = [], []
+    for i in range(5):
+        sess.step(DeviceBatch(torch.arange(i, i + 8).cuda()))
+        futs.append(sess.loss_future())
+        if i >= 2:   # results read lagging behind, like bench.py's e2e loop
+            futs[i - 2].result()
+        sync.append(sess.last_loss())
+    assert [f.result() for f in futs] == sync
