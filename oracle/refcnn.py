@@ -434,12 +434,13 @@ def run_sync(layers, in_ch, in_size, images, labels, W0, eta, mu, lam, b, steps,
 
 
 def simulate(grad_fn, sample_fn, W0, g, t_conv, t_fc, eta, mu, lam, b, max_updates, seed,
-             exponential=False):
+             exponential=False, models=None):
     """The g-group event loop (simulator.py:123-213) with a pluggable gradient.
 
     grad_fn(W, batch) -> gradient; sample_fn(rng, b) -> batch.  Returns
     (final W, final V, events) with events = [(group, read_step, write_step,
-    staleness, start, enqueue, finish)].
+    staleness, start, enqueue, finish)].  ``models`` (a list) receives the
+    master model after every write, initial model first (record_models).
     """
     brng = [batch_stream(seed, i) for i in range(g)]
     srng = [service_stream(seed, i) for i in range(g)] if exponential else None
@@ -452,6 +453,8 @@ def simulate(grad_fn, sample_fn, W0, g, t_conv, t_fc, eta, mu, lam, b, max_updat
     W = np.asarray(W0, dtype=np.float64).copy()
     V = np.zeros_like(W)
     t = 0
+    if models is not None:
+        models.append(W.copy())
     heap, seq = [], 0
     for i in range(g):
         cd, fs = services(i)
@@ -466,10 +469,48 @@ def simulate(grad_fn, sample_fn, W0, g, t_conv, t_fc, eta, mu, lam, b, max_updat
         W, V = sgd_step(W, V, grad_fn(snap, batch), snap, eta, mu, lam)
         t += 1
         events.append((i, read_step, t, t - 1 - read_step, read_time, conv_done, finish))
+        if models is not None:
+            models.append(W.copy())
         cd, fs2 = services(i)
         heapq.heappush(heap, (finish + cd, seq, i, W.copy(), t, finish, sample_fn(brng[i], b), fs2))
         seq += 1
     return W, V, events
+
+
+def child_seed(seed: int, *key: int) -> int:
+    """sgd.py:43-46"""
+    return int(np.random.SeedSequence(seed, spawn_key=tuple(key)).generate_state(1, dtype=np.uint64)[0])
+
+
+def estimate_implicit_momentum(grad_fn, full_grad_fn, sample_fn, W0, g, t_conv, t_fc, eta, lam, b,
+                               max_updates, seed, n_runs, burn_in=None, signal_floor=0.02):
+    """simulator.py:244-321 restated (exponential service, explicit mu = 0):
+    average the master trajectories of runs seeded child_seed(seed, 3, r), then
+    least-squares fit V(t+1) ~ a V(t) - c grad(W(t)) over the live-signal
+    window; returns a.  (The reference also drops diverged runs; the oracle's
+    callers use step sizes that do not diverge.)"""
+    if burn_in is None:
+        burn_in = 3 * g + 10
+    paths = []
+    for r in range(n_runs):
+        models = []
+        simulate(grad_fn, sample_fn, W0, g, t_conv, t_fc, eta, 0.0, lam, b, max_updates,
+                 child_seed(seed, 3, r), exponential=True, models=models)
+        paths.append(np.array(models))
+    mean_path = np.mean(paths, axis=0)
+    V = np.diff(mean_path, axis=0)
+    mags = np.max(np.abs(V), axis=1)
+    threshold = signal_floor * float(np.mean(mags[burn_in:burn_in + 10]))
+    t_end = mean_path.shape[0] - 1
+    for t in range(burn_in + 20, mean_path.shape[0] - 1):
+        if mags[t] < threshold:
+            t_end = t
+            break
+    X = np.concatenate([np.column_stack([V[t - 1], -full_grad_fn(mean_path[t])])
+                        for t in range(burn_in + 1, t_end)])
+    y = np.concatenate([V[t] for t in range(burn_in + 1, t_end)])
+    beta, *_ = np.linalg.lstsq(X, y, rcond=None)
+    return float(beta[0])
 
 
 def deterministic_schedule(g: int, t: int):

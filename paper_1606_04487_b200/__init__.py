@@ -17,8 +17,8 @@ from .sgd import (DIVERGENCE_FACTOR, LOSS_WINDOW, Hyperparams, LossTrace, SGDSta
                   service_stream, sgd_step, smoothed, stale_step)
 from .tensors import (ConvSpec, LoweredMatrix, Tensor4, blowup_ratio, conv_direct, conv_lowered,
                       gemm, lift, lower, lower_kernel)
-from .simulator import (SimConfig, SimEvent, SimTrace, StalenessStats, measured_he, simulate,
-                        staleness_stats)
+from .simulator import (SimConfig, SimEvent, SimTrace, StalenessStats, estimate_implicit_momentum,
+                        measured_he, simulate, staleness_stats)
 
 
 def __getattr__(name):

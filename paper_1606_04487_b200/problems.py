@@ -394,9 +394,12 @@ class CNNProblem(TrainingProblem):
         return self.full_loss_device(self._w(W))
 
     def full_grad(self, W, chunk: int = 256) -> np.ndarray:
+        return self.full_grad_device(self._w(W), chunk).cpu().numpy()
+
+    def full_grad_device(self, Wd: torch.Tensor, chunk: int = 256) -> torch.Tensor:
+        """Mean gradient over the whole dataset at device weights (float64, on device)."""
         n = self._n
         e = self.engine(min(n, chunk))
-        Wd = self._w(W)
         acc = torch.zeros(self.dim, dtype=torch.float64, device=self.device)
         for s0 in range(0, n, e.b):
             b = min(e.b, n - s0)
@@ -404,7 +407,7 @@ class CNNProblem(TrainingProblem):
             e.gather_batch(self.data, self.data_labels, idx)
             _, G = e.loss_and_grad(Wd, b)
             acc += G.double() * (b / n)
-        return acc.cpu().numpy()
+        return acc
 
     def device_session(self, state: SGDState, hp: Hyperparams, process_group=None,
                        use_graph: bool = True) -> DeviceSession:

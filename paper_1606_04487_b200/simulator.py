@@ -14,14 +14,14 @@ GPUs.
 from __future__ import annotations
 
 import heapq
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 from typing import Optional
 
 import numpy as np
 
 from .cluster import ExecutionPlan, PhaseProfile, t_conv
 from .sgd import (DIVERGENCE_FACTOR, Hyperparams, LossTrace, SGDState, TrainingProblem,
-                  batch_stream, service_stream, sgd_step)
+                  batch_stream, child_seed, service_stream, sgd_step)
 
 DEFAULT_BURN_IN = 100
 
@@ -155,6 +155,13 @@ class _DeviceModel:
 
 def simulate(cfg: SimConfig) -> SimTrace:
     """Run the event loop until the update or sim-time budget, or divergence."""
+    return _simulate(cfg)
+
+
+def _simulate(cfg: SimConfig, on_write=None) -> SimTrace:
+    """simulate(), plus ``on_write(i, model)`` after the i-th master update
+    (i = 0 for the initial model) -- how the implicit-momentum estimator
+    records device-resident trajectories without host copies."""
     g = cfg.plan.g
     conv_mean = t_conv(cfg.plan.k, cfg.profile)
     fc_mean = cfg.profile.t_fc
@@ -171,6 +178,8 @@ def simulate(cfg: SimConfig) -> SimTrace:
     models = [model.model_copy()] if cfg.record_models else None
     diverged = not np.isfinite(initial_loss)
     t0 = model.t
+    if on_write is not None:
+        on_write(0, model)
 
     def draw(i):
         if exponential:
@@ -201,6 +210,8 @@ def simulate(cfg: SimConfig) -> SimTrace:
         events.append(SimEvent(i, read_step, t, t - 1 - read_step, read_time, conv_done, finish))
         if models is not None:
             models.append(model.model_copy())
+        if on_write is not None:
+            on_write(t - t0, model)
         if not model.finite():
             diverged = True
         if (t - t0) % cfg.loss_sample_interval == 0 or diverged:
@@ -242,3 +253,116 @@ def staleness_stats(trace: SimTrace, burn_in: int = 0) -> StalenessStats:
         raise ValueError("trace has no events past burn_in")
     v, c = np.unique(s, return_counts=True)
     return StalenessStats(mean=float(s.mean()), histogram={int(a): int(b) for a, b in zip(v, c)})
+
+
+def _signal_window(mags: np.ndarray, burn_in: int, signal_floor: float, n_models: int) -> int:
+    """End of the fit window (simulator.py:296-304): the first t >= burn_in + 20
+    where the averaged increment drops below signal_floor x its early level."""
+    if burn_in + 21 >= mags.shape[0]:
+        raise ValueError("max_updates too small for the burn-in window")
+    threshold = signal_floor * float(np.mean(mags[burn_in:burn_in + 10]))
+    for t in range(burn_in + 20, n_models - 1):
+        if mags[t] < threshold:
+            return t
+    return n_models - 1
+
+
+def estimate_implicit_momentum(cfg: SimConfig, n_runs: int, burn_in: Optional[int] = None,
+                               signal_floor: float = 0.02) -> float:
+    """Regression estimate of the momentum asynchrony induces (simulator.py:244-321,
+    Theorem 1): average the master trajectories of ``n_runs`` seeded runs
+    (seed child_seed(cfg.seed, 3, r)), then least-squares fit
+    V(t+1) ~ a V(t) - c grad(W(t)) over the window where the averaged signal is
+    alive, pooling time steps and coordinates; returns ``a``.
+
+    With a GPU problem every trajectory stays in HBM (written by the event
+    loop's update hook), the runs are summed in float64 on the device, the
+    full gradients along the mean path are device passes, and the two-column
+    least squares is solved from its 2x2 normal equations in float64."""
+    if cfg.hp.mu != 0.0:
+        raise ValueError("implicit-momentum estimation requires explicit momentum 0")
+    if cfg.service_mode != "exponential":
+        raise ValueError("implicit-momentum estimation requires exponential service")
+    if cfg.max_updates is None:
+        raise ValueError("cfg.max_updates must be set")
+    if burn_in is None:
+        burn_in = 3 * cfg.plan.g + 10
+    if not hasattr(cfg.problem, "device_session"):
+        return _estimate_host(cfg, n_runs, burn_in, signal_floor)
+
+    import torch
+
+    prob = cfg.problem
+    T = cfg.max_updates + 1
+    total = None
+    n_ok = 0
+    for r in range(n_runs):
+        run_cfg = replace(cfg, seed=child_seed(cfg.seed, 3, r), record_models=False)
+        path = torch.empty((T, prob.dim), dtype=torch.float32, device=prob.device)
+        written = [0]
+
+        def on_write(i, model, path=path, written=written):
+            path[i].copy_(model.s.W)
+            written[0] = i + 1
+
+        trace = _simulate(run_cfg, on_write)
+        if trace.diverged or written[0] != T:
+            continue
+        if total is None:
+            total = path.double()
+        else:
+            total.add_(path)
+        n_ok += 1
+    if total is None:
+        raise ValueError("no usable runs (all diverged or cut short)")
+    mean_path = total.div_(n_ok)
+    V = mean_path[1:] - mean_path[:-1]
+    mags = V.abs().amax(dim=1).cpu().numpy()
+    t_end = _signal_window(mags, burn_in, signal_floor, T)
+    # normal equations of [V(t-1), -grad(t)] beta = V(t), accumulated in float64
+    a11 = a12 = a22 = b1 = b2 = torch.zeros((), dtype=torch.float64, device=prob.device)
+    rows = 0
+    for t in range(burn_in + 1, t_end):
+        gr = prob.full_grad_device(mean_path[t].float())
+        v, y = V[t - 1], V[t]
+        a11 = a11 + v.dot(v)
+        a12 = a12 - v.dot(gr)
+        a22 = a22 + gr.dot(gr)
+        b1 = b1 + v.dot(y)
+        b2 = b2 - gr.dot(y)
+        rows += prob.dim
+    if rows == 0:
+        raise ValueError("signal window is empty; lower burn_in or raise max_updates")
+    if n_ok * rows < 1000:
+        raise ValueError(f"insufficient samples: {n_ok * rows} pooled triples < 1000")
+    A = torch.stack([torch.stack([a11, a12]), torch.stack([a12, a22])]).cpu().numpy()
+    bvec = torch.stack([b1, b2]).cpu().numpy()
+    beta, *_ = np.linalg.lstsq(A, bvec, rcond=None)
+    return float(beta[0])
+
+
+def _estimate_host(cfg: SimConfig, n_runs: int, burn_in: int, signal_floor: float) -> float:
+    """The same estimator for host problems (recorded float64 trajectories)."""
+    paths = []
+    for r in range(n_runs):
+        trace = simulate(replace(cfg, seed=child_seed(cfg.seed, 3, r), record_models=True))
+        if trace.diverged or trace.models is None or trace.models.shape[0] != cfg.max_updates + 1:
+            continue
+        paths.append(trace.models)
+    if not paths:
+        raise ValueError("no usable runs (all diverged or cut short)")
+    mean_path = np.mean(paths, axis=0)
+    V = np.diff(mean_path, axis=0)
+    mags = np.max(np.abs(V), axis=1)
+    t_end = _signal_window(mags, burn_in, signal_floor, mean_path.shape[0])
+    xs, ys = [], []
+    for t in range(burn_in + 1, t_end):
+        xs.append(np.column_stack([V[t - 1], -cfg.problem.full_grad(mean_path[t])]))
+        ys.append(V[t])
+    if not xs:
+        raise ValueError("signal window is empty; lower burn_in or raise max_updates")
+    X, y = np.concatenate(xs), np.concatenate(ys)
+    if len(paths) * X.shape[0] < 1000:
+        raise ValueError(f"insufficient samples: {len(paths) * X.shape[0]} pooled triples < 1000")
+    beta, *_ = np.linalg.lstsq(X, y, rcond=None)
+    return float(beta[0])

@@ -103,6 +103,21 @@ def main() -> None:
                     np.array([2.0]), np.array([1.0]))
     arrs["sgd_kat"] = np.array([s.W[0], s.V[0]])
     np.savez_compressed(os.path.join(OUT, "tinycnn.npz"), **arrs)
+
+    # 7. implicit-momentum estimator (simulator.py:244-321) on the TinyCNN,
+    #    exponential service, explicit momentum 0, g = 2 and 4
+    from omnisim.simulator import estimate_implicit_momentum
+
+    arrs = {}
+    prob = om.make_tiny_cnn(8, 4, seed=3, n_examples=64)
+    hp0 = om.Hyperparams(eta=0.05, mu=0.0, lam=0.0, b=8)
+    prof0 = om.PhaseProfile(T_cc=4.0, T_nc=0.0, t_fc=0.01)
+    arrs["im_cfg"] = np.array([8, 4, 64, 3, 0.05, 8, 4.0, 0.01, 80, 3, 8])  # size classes n_ex seed eta b T_cc t_fc max_updates sim_seed n_runs
+    for g in (2, 4):
+        cfg = om.SimConfig(plan=om.ExecutionPlan(N=4, g=g), profile=prof0, hp=hp0, problem=prob,
+                           service_mode="exponential", max_updates=80, seed=3)
+        arrs[f"im_g{g}"] = np.array(estimate_implicit_momentum(cfg, n_runs=8))
+    np.savez_compressed(os.path.join(OUT, "implicit_momentum.npz"), **arrs)
     print("wrote fixtures to", OUT)
 
 

@@ -175,3 +175,28 @@ def test_conv_geometry_errors_match_reference_rules():
         R.conv_out(5, 7, 1, 0)
     with pytest.raises(ValueError):
         R.conv_out(8, 3, 2, 0)
+
+
+def test_implicit_momentum_estimator_vs_reference():
+    """oracle restatement of simulator.py:244-321 == the reference's estimator."""
+    z = load("implicit_momentum.npz")
+    size, classes, n_ex, pseed, eta, b, T_cc, t_fc, max_updates, seed, n_runs = z["im_cfg"]
+    size, classes, n_ex, b = int(size), int(classes), int(n_ex), int(b)
+    images, labels = R.tiny_cnn_data(size, classes, int(pseed), n_ex)
+    layers = R.tiny_cnn_layers(size, classes)
+    W0 = 0.01 * R.problem_rng(int(pseed), 1).standard_normal(R.param_count(layers, 1, size))
+
+    def grad_fn(W, batch):
+        return R.grad(layers, 1, size, W, *batch)
+
+    def full_grad_fn(W):
+        return R.grad(layers, 1, size, W, images, labels)
+
+    def sample_fn(rng, bb):
+        idx = rng.integers(0, n_ex, size=bb)
+        return images[idx], labels[idx]
+
+    for g in (2, 4):   # N = 4, T_nc = 0: t_conv(k) = T_cc / k (cluster.py:76-80)
+        a = R.estimate_implicit_momentum(grad_fn, full_grad_fn, sample_fn, W0, g, T_cc / (4 // g),
+                                         t_fc, eta, 0.0, b, int(max_updates), int(seed), int(n_runs))
+        assert abs(a - float(z[f"im_g{g}"])) < 1e-9, (g, a, float(z[f"im_g{g}"]))
