@@ -58,3 +58,44 @@ def worker(rank, world, port, g, rounds, hp_tuple, out_dir):
                 np.array([[e.group_id, e.read_step, e.write_step, e.staleness] for e in rt.events]))
     finally:
         dist.destroy_process_group()
+
+
+class JitterBackend(OracleBackend):
+    """OracleBackend with random compute delays: the asynchronous arrival order
+    then differs from run to run (what replay must be robust to)."""
+
+    def __init__(self, seed):
+        super().__init__()
+        self.rng = np.random.default_rng(seed)
+
+    def grad(self, W, idx):
+        import time
+
+        time.sleep(float(self.rng.uniform(0.0, 0.02)))
+        return super().grad(W, idx)
+
+
+def async_worker(rank, world, port, g, max_updates, hp_tuple, out_dir):
+    """paper_1606_04487_b200.async_groups: rank 0 serves, ranks 1.. compute."""
+    from paper_1606_04487_b200 import async_groups as A
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        eta, mu, lam, b = hp_tuple
+        hp = Hyperparams(eta=eta, mu=mu, lam=lam, b=b)
+        plan = ExecutionPlan(world - 1, g)
+        W0 = torch.from_numpy(initial_weights())
+        if rank == 0:
+            res = A.run_server(plan, OracleBackend(), hp, W0, max_updates)
+            Wr, _ = A.replay(res.events, plan, OracleBackend(), hp, W0, N_EX, seed=11)
+            np.save(os.path.join(out_dir, "W.npy"), res.W.numpy())
+            np.save(os.path.join(out_dir, "Wreplay.npy"), Wr.numpy())
+            np.save(os.path.join(out_dir, "ev.npy"),
+                    np.array([[e.group_id, e.read_step, e.write_step, e.staleness, e.batch_index]
+                              for e in res.events]))
+        else:
+            A.run_worker(plan, JitterBackend(1000 + rank), hp, W0, N_EX, seed=11)
+    finally:
+        dist.destroy_process_group()
