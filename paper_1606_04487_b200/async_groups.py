@@ -67,8 +67,18 @@ def worker_ranks(plan: ExecutionPlan, group: int) -> list[int]:
 
 
 def _new_groups(plan: ExecutionPlan):
-    # every rank creates every subgroup, in the same order (torch.distributed rule)
-    return [dist.new_group(worker_ranks(plan, i)) for i in range(plan.g)]
+    """Intra-group process groups, plus (NCCL) one server<->leader group per
+    worker group: point-to-point traffic of different groups then runs on
+    separate communicators / streams, so a receive still pending from one
+    group never queues the replies to another (on one shared P2P stream the
+    groups end up taking turns).  Every rank creates every subgroup, in the
+    same order (torch.distributed rule)."""
+    intra = [dist.new_group(worker_ranks(plan, i)) for i in range(plan.g)]
+    if dist.get_backend() == "nccl":
+        pair = [dist.new_group([0, worker_ranks(plan, i)[0]]) for i in range(plan.g)]
+    else:   # gloo: the server's any-source receive needs the default group
+        pair = [None] * plan.g
+    return intra, pair
 
 
 def run_server(plan: ExecutionPlan, backend, hp: Hyperparams, W0: torch.Tensor,
@@ -76,7 +86,7 @@ def run_server(plan: ExecutionPlan, backend, hp: Hyperparams, W0: torch.Tensor,
     """Rank 0.  Returns the update log and the final master model."""
     if dist.get_rank() != 0:
         raise RuntimeError("run_server runs on rank 0")
-    _new_groups(plan)
+    _, pair = _new_groups(plan)
     dev = W0.device
     W = W0.clone()
     V = torch.zeros_like(W)
@@ -95,7 +105,8 @@ def run_server(plan: ExecutionPlan, backend, hp: Hyperparams, W0: torch.Tensor,
     nccl = dist.get_backend() == "nccl"
     by_leader = {r: i for i, r in enumerate(leaders)}
     anybuf = None if nccl else torch.empty_like(W)
-    pending = [dist.irecv(bufs[i], src=leaders[i]) for i in range(plan.g)] if nccl else None
+    pending = ([dist.irecv(bufs[i], src=leaders[i], group=pair[i]) for i in range(plan.g)]
+               if nccl else None)
 
     def next_arrival() -> int:
         if not nccl:
@@ -123,12 +134,12 @@ def run_server(plan: ExecutionPlan, backend, hp: Hyperparams, W0: torch.Tensor,
         snaps[i].copy_(W)                            # the group's next snapshot (and w_read)
         read_step[i] = t
         if t < max_updates:
-            dist.send(go, dst=leaders[i])
-            dist.send(snaps[i], dst=leaders[i])
+            dist.send(go, dst=leaders[i], group=pair[i])
+            dist.send(snaps[i], dst=leaders[i], group=pair[i])
             if nccl:
-                pending[i] = dist.irecv(bufs[i], src=leaders[i])
+                pending[i] = dist.irecv(bufs[i], src=leaders[i], group=pair[i])
         else:
-            dist.send(stop, dst=leaders[i])           # its last gradient was applied
+            dist.send(stop, dst=leaders[i], group=pair[i])   # its last gradient was applied
             done[i] = True
     if dev.type == "cuda":
         torch.cuda.synchronize(dev)
@@ -139,7 +150,7 @@ def run_server(plan: ExecutionPlan, backend, hp: Hyperparams, W0: torch.Tensor,
             pending[i].wait()
         else:
             i = by_leader[dist.recv(anybuf, src=None)]
-        dist.send(stop, dst=leaders[i])
+        dist.send(stop, dst=leaders[i], group=pair[i])
         done[i] = True
     return AsyncResult(events, W, V, seconds)
 
@@ -150,11 +161,12 @@ def run_worker(plan: ExecutionPlan, backend, hp: Hyperparams, W0: torch.Tensor, 
     rank = dist.get_rank()
     if rank == 0:
         raise RuntimeError("rank 0 is the server")
-    pgs = _new_groups(plan)
+    intra, pair = _new_groups(plan)
     group = (rank - 1) // plan.k
     member = (rank - 1) % plan.k
     ranks = worker_ranks(plan, group)
-    pg = pgs[group]
+    pg = intra[group]
+    sg = pair[group]   # server <-> leader
     if hp.b % plan.k:
         raise ValueError(f"group batch b={hp.b} is not divisible by k={plan.k}")
     per = hp.b // plan.k
@@ -168,15 +180,15 @@ def run_worker(plan: ExecutionPlan, backend, hp: Hyperparams, W0: torch.Tensor, 
         if plan.k > 1:
             dist.all_reduce(G, group=pg)            # sum of k slice means
         if member == 0:
-            dist.send(G, dst=0)
-            dist.recv(flag, src=0)
+            dist.send(G, dst=0, group=sg)
+            dist.recv(flag, src=0, group=sg)
         if plan.k > 1:
             dist.broadcast(flag, src=ranks[0], group=pg)
         n += 1
         if int(flag.item()) == 0:
             return n
         if member == 0:
-            dist.recv(W, src=0)
+            dist.recv(W, src=0, group=sg)
         if plan.k > 1:
             dist.broadcast(W, src=ranks[0], group=pg)
 
