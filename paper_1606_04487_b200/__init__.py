@@ -22,6 +22,10 @@ from .simulator import (SimConfig, SimEvent, SimTrace, StalenessStats, estimate_
 
 
 def __getattr__(name):
+    if name in ("optimizer", "async_groups", "groups"):
+        import importlib
+
+        return importlib.import_module(f".{name}", __name__)
     # problems / engine import torch CUDA state lazily
     if name in ("CNNProblem", "TinyCNNProblem", "make_tiny_cnn", "make_cnn", "Batch"):
         from . import problems
