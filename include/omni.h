@@ -36,6 +36,11 @@ int omni_version(void);
 int omni_device_sm_count(int device);
 /* Kernels launched by this library so far (process-wide; for launch accounting). */
 long long omni_launch_count(void);
+/* SMs the persistent GEMM grids leave free for concurrent communication
+ * kernels (data parallel; default 0 or $OMNI_SM_RESERVE).  Plans (and so
+ * split-K workspace sizes) depend on it: set it before sizing workspaces.   */
+int omni_set_sm_reserve(int sms);
+int omni_get_sm_reserve(void);
 
 /* ---------------------------------------------------------------- K1 --
  * Batched lowering (type-1 im2col over b_p images starting at `start`).

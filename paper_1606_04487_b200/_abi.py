@@ -47,6 +47,8 @@ SIGNATURES: dict[str, tuple] = {
     "omni_version": (_I, []),
     "omni_device_sm_count": (_I, [_I]),
     "omni_launch_count": (_L, []),
+    "omni_set_sm_reserve": (_I, [_I]),
+    "omni_get_sm_reserve": (_I, []),
     "omni_lower_nchw_f32": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P]),
     "omni_lower_nchw_f64": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P]),
     "omni_lower_nhwc_f32": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P]),

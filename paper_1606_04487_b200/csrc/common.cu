@@ -81,4 +81,23 @@ int omni_device_sm_count(int device) { return omni::sm_count_cached(device); }
 
 long long omni_launch_count(void) { return omni::g_launches.load(std::memory_order_relaxed); }
 
+static std::atomic<int> g_sm_reserve{-1};
+
+int omni_set_sm_reserve(int sms) {
+  OMNI_REQUIRE(sms >= 0 && sms <= 64, "sm reserve must be in [0, 64]");
+  g_sm_reserve.store(sms);
+  return OMNI_OK;
+}
+
+int omni_get_sm_reserve(void) {
+  int r = g_sm_reserve.load();
+  if (r < 0) {   // first use: OMNI_SM_RESERVE from the environment, default 0
+    const char* e = getenv("OMNI_SM_RESERVE");
+    r = e ? atoi(e) : 0;
+    if (r < 0 || r > 64) r = 0;
+    g_sm_reserve.store(r);
+  }
+  return r;
+}
+
 }  // extern "C"

@@ -1083,7 +1083,9 @@ Plan plan_for(int precision, int M, int N, int K, bool b_mn, int im2col) {
   cudaGetDevice(&dev);
   const int bkt = im2col == 3 ? wgrad_bkt(precision) : BK;
   const bool b_mn_eff = b_mn || im2col == 2 || im2col == 3;
-  const int sms = omni::sm_count_cached(dev);
+  // SMs left free for concurrent communication kernels (data parallel: the
+  // persistent GEMM grids would otherwise hold every SM and delay NCCL)
+  const int sms = omni::sm_count_cached(dev) - omni_get_sm_reserve();
   bool pair = pair_ok(precision, M, im2col);
   if (pair && b_mn_eff) {
     // MN-major B is split into 32-column halves: a tile width that does not

@@ -317,17 +317,38 @@ def test_bias_grad_sgd_gather_transpose():
     assert torch.equal(out.cpu(), T.transpose(1, 2))
 
 
-def test_conv_weight_tap_roundtrip():
-    o, c, k = 7, 3, 5
-    W = torch.randn(o, c, k, k)
-    ld = K.round_up(c * k * k, 4)
-    Wt = torch.empty(o, ld, device=DEV)
-    K.conv_weight_to_tap(W.to(DEV), o, c, k, Wt, ld)
+@pytest.mark.parametrize("o,c,k", [(7, 3, 5), (96, 3, 11), (256, 96, 5), (384, 256, 3), (512, 512, 3),
+                                   (50, 20, 5)])
+def test_conv_weight_tap_roundtrip(o, c, k):
+    gen = torch.Generator().manual_seed(o + c + k)
+    W = torch.randn(o, c, k, k, generator=gen)
+    bias = torch.randn(o, generator=gen)
+    ld = K.round_up(c * k * k + 1, 32)
+    Wt = torch.full((o, ld), float("nan"), device=DEV)
+    K.conv_weight_to_tap(W.to(DEV), o, c, k, Wt, ld, bias=bias.to(DEV))
     ref = W.permute(0, 2, 3, 1).reshape(o, k * k * c)
-    assert torch.equal(Wt.cpu()[:, : c * k * k], ref)
+    got = Wt.cpu()
+    assert torch.equal(got[:, : c * k * k], ref)
+    assert torch.equal(got[:, c * k * k], bias)
+    assert (got[:, c * k * k + 1:] == 0).all()                       # row padding zeroed
     back = torch.empty(o, c, k, k, device=DEV)
-    K.conv_weight_to_tap(back, o, c, k, Wt, ld, inverse=True)
-    assert torch.equal(back.cpu(), W)
+    bb = torch.empty(o, device=DEV)
+    K.conv_weight_to_tap(back, o, c, k, Wt, ld, inverse=True, bias=bb)
+    assert torch.equal(back.cpu(), W) and torch.equal(bb.cpu(), bias)
+
+
+@pytest.mark.parametrize("o,c,k", [(96, 256, 5), (384, 256, 3), (256, 384, 3), (50, 20, 5), (70, 33, 11)])
+def test_conv_weight_flip_layout(o, c, k):
+    """Wf[ch*ld + (kx*k + ky)*o + oo] = W[oo, ch, k-1-kx, k-1-ky], zero row padding."""
+    gen = torch.Generator().manual_seed(o * c + k)
+    W = torch.randn(o, c, k, k, generator=gen)
+    ld = K.round_up(o * k * k, 32) + 32
+    Wf = torch.full((c, ld), float("nan"), device=DEV)
+    K.conv_weight_flip(W.to(DEV), o, c, k, Wf, ld)
+    ref = W.flip(2, 3).permute(1, 2, 3, 0).reshape(c, k * k * o)
+    got = Wf.cpu()
+    assert torch.equal(got[:, : o * k * k], ref)
+    assert (got[:, o * k * k:] == 0).all()
 
 
 @pytest.mark.parametrize("geom", [(2, 3, 27, 11, 4, 0), (2, 8, 10, 3, 1, 1), (1, 5, 9, 3, 1, 1)])
