@@ -230,6 +230,8 @@ class GpuNet:
         self.gemm_ws_side = z(max(ws // 4, 4))   # weight-gradient GEMMs run on a side stream
         self._ws_active = self.gemm_ws
         self._s2d_ready = 0   # batch size whose space-to-depth input gather_batch wrote
+        self._staged_for = None   # W whose layouts prestage() put in flight
+        self._staged_ev = None
         self.side_stream = torch.cuda.Stream(device=self.device)
         self.bias_ws = z(max(bws, 4))
         self.ddhat = z(max(dd, 4))
@@ -344,13 +346,34 @@ class GpuNet:
                 d = op.layer.d_out
                 K.transpose(W[op.woff:op.woff + op.wsz], d, 0, op.f_in, d, op.wstage, op.flat.cs, 0, 1)
 
+    def prestage(self, W: torch.Tensor) -> None:
+        """Stage W's layouts on the side stream, after the main stream's pending
+        work (the previous update), so they overlap whatever the main stream
+        does next (the batch gather); forward(W) then only waits for them."""
+        if not self.overlap:
+            return
+        main = torch.cuda.current_stream(self.device)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        self.side_stream.wait_event(ev)
+        with torch.cuda.stream(self.side_stream):
+            self.stage_weights(W)
+            self._staged_ev = torch.cuda.Event()
+            self._staged_ev.record(self.side_stream)
+        self._staged_for = W
+
     # ----------------------------------------------------------- forward --
     def forward(self, W: torch.Tensor, b: int | None = None, need_grad: bool = True) -> torch.Tensor:
         """Run the forward pass on self.input / self.labels (first b rows);
         leaves the mean loss in self.loss_buf and, if need_grad, dlogits in
         the logits' grad buffer.  W is the flat fp32 parameter vector."""
         b = self.b if b is None else int(b)
-        self.stage_weights(W)
+        staged = self._staged_for
+        self._staged_for = None
+        if staged is not None:
+            torch.cuda.current_stream(self.device).wait_event(self._staged_ev)
+        if staged is None or staged is not W:
+            self.stage_weights(W)
         for op in self.ops:
             L = op.layer
             if op.kind == "conv":

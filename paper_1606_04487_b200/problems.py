@@ -232,6 +232,7 @@ class DeviceSession:
                     self._gidx = torch.empty_like(batch.idx)
                 self._gidx.copy_(batch.idx)
                 with torch.cuda.graph(g):
+                    self.engine.prestage(wr)
                     self.engine.gather_batch(self.problem.data, self.problem.data_labels, self._gidx)
                     self._compute(wr, batch.size)
             else:
@@ -245,6 +246,7 @@ class DeviceSession:
             if staged is not None:
                 self._run_on_slot(staged[0], batch.size, wr)
             else:
+                self.engine.prestage(wr)          # weight layouts overlap the batch gather
                 b = self.problem.load_batch(self.engine, batch)
                 self._compute(wr, b)
         if staged is not None:
