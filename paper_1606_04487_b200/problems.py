@@ -183,9 +183,9 @@ class DeviceSession:
                 w.wait()   # the compute stream waits for the NCCL stream
             n = self.world   # eta (G_sum/n + lam w) = (eta/n) (G_sum + n lam w)
             K.sgd_momentum(self.W, self.V, self.engine.grad, wr, hp.eta / n, hp.mu, hp.lam * n)
-        else:
-            self.engine.loss_and_grad(wr, b)
-            K.sgd_momentum(self.W, self.V, self.engine.grad, wr, hp.eta, hp.mu, hp.lam)
+        else:   # the update runs layer by layer inside the backward
+            self.engine.forward(wr, b)
+            self.engine.backward(b, update=(self.W, self.V, wr, hp.eta, hp.mu, hp.lam))
 
     def _run_on_slot(self, slot: int, b: int, wr: torch.Tensor) -> None:
         eng = self.engine
