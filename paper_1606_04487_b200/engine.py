@@ -433,7 +433,8 @@ class GpuNet:
         ``on_grad(lo, hi)`` (optional) is called as soon as the launches that
         write G[lo:hi] (one layer's weight + bias gradient) are enqueued, in
         backward order -- the hook a data-parallel caller uses to overlap the
-        gradient allreduce of finished layers with the rest of the backward.
+        gradient allreduce of finished layers with the rest of the backward; if
+        it returns an async work handle, that layer's update waits for it.
 
         ``update = (W, V, w_read, eta, mu, lam)`` (single device) applies the
         momentum update (K8) layer by layer as soon as a layer's gradient is
@@ -449,12 +450,11 @@ class GpuNet:
 
         def done(op):
             hi = op.boff + op.layer.d_out if op.boff >= 0 else op.woff + op.wsz
-            if on_grad is not None:
-                on_grad(op.woff, hi)
+            work = on_grad(op.woff, hi) if on_grad is not None else None
             if update is not None:
                 ev = torch.cuda.Event()
                 ev.record(torch.cuda.current_stream(self.device))   # after the wgrad launches
-                pending.append((op.woff, hi, ev))
+                pending.append((op.woff, hi, ev, work))
 
         def flush():
             """Issue the updates of layers whose data gradient is enqueued."""
@@ -465,9 +465,11 @@ class GpuNet:
             ev_main = torch.cuda.Event()
             ev_main.record(main)                                     # the dgrads read W in place
             us.wait_event(ev_main)
-            for lo, hi, ev in pending:
+            for lo, hi, ev, work in pending:
                 us.wait_event(ev)
                 with torch.cuda.stream(us):
+                    if work is not None:
+                        work.wait()      # this layer's gradient allreduce (update stream waits)
                     K.sgd_momentum(Wu[lo:hi], Vu[lo:hi], G[lo:hi], wr[lo:hi], eta, mu, lam)
             pending.clear()
 

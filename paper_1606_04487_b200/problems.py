@@ -143,7 +143,9 @@ class DeviceSession:
         G = self.engine.grad
 
         def hook(lo, hi):
-            works.append(dist.all_reduce(G[lo:hi], group=self.pg, async_op=True))
+            w = dist.all_reduce(G[lo:hi], group=self.pg, async_op=True)
+            works.append(w)
+            return w
 
         return hook
 
@@ -176,13 +178,15 @@ class DeviceSession:
         already in the engine's input buffers."""
         hp = self.hp
         if self.world > 1:
+            # each layer's gradient is allreduced as soon as it exists and that
+            # layer's update follows its allreduce (inside the backward)
             works = []
-            self.engine.forward(wr, b)
-            self.engine.backward(b, on_grad=self._allreduce_hook(works))
-            for w in works:
-                w.wait()   # the compute stream waits for the NCCL stream
             n = self.world   # eta (G_sum/n + lam w) = (eta/n) (G_sum + n lam w)
-            K.sgd_momentum(self.W, self.V, self.engine.grad, wr, hp.eta / n, hp.mu, hp.lam * n)
+            self.engine.forward(wr, b)
+            self.engine.backward(b, on_grad=self._allreduce_hook(works),
+                                 update=(self.W, self.V, wr, hp.eta / n, hp.mu, hp.lam * n))
+            for w in works:
+                w.wait()   # (already waited for by the updates; keeps the handles honest)
         else:   # the update runs layer by layer inside the backward
             self.engine.forward(wr, b)
             self.engine.backward(b, update=(self.W, self.V, wr, hp.eta, hp.mu, hp.lam))
