@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--mu", type=float, default=0.9)
     ap.add_argument("--lam", type=float, default=5e-4)
     ap.add_argument("--profile-out", default="", help="write per-GEMM timing breakdown (json)")
+    ap.add_argument("--merged-fc", action="store_true",
+                    help="N > 1: FC layers on rank 0 for the global batch (PAPER.md:936-959)")
     ap.add_argument("--groups", type=int, default=1,
                     help="compute groups g (g > 1: groups.GroupRuntime, deterministic round-robin "
                          "async schedule; momentum retuned per g by Theorem 1)")
@@ -218,7 +220,8 @@ def run_ours(args):
                       labels="uniform", precision=args.precision, device=dev)
     hp = Hyperparams(eta=args.eta, mu=args.mu, lam=args.lam, b=b)
     sess = prob.device_session(SGDState.fresh(np.zeros(1)), hp,
-                               process_group=dist.group.WORLD if world > 1 else None)
+                               process_group=dist.group.WORLD if world > 1 else None,
+                               merged_fc=args.merged_fc and world > 1)
     gw = torch.Generator(device=dev)
     gw.manual_seed(args.seed)                     # identical initial model on every rank
     sess.W = 0.01 * torch.randn(net.dim, generator=gw, device=dev)
@@ -353,7 +356,8 @@ def run_ours(args):
             "dtype": args.precision, "data": "synthetic (Gaussian images, uniform labels, random-init weights)",
             "config": {"workload": f"{args.net} train step, b={b} per GPU, synthetic {s}x{s}x{c}, g=1",
                        "net": args.net, "per_gpu_batch": b, "global_batch": b * world, "g": 1,
-                       "parallelism": f"dp{world}", "precision": args.precision,
+                       "parallelism": f"dp{world}" + ("+merged-fc" if args.merged_fc and world > 1 else ""),
+                       "precision": args.precision,
                        "l2": "working set larger than L2 (~8 GB of DRAM traffic per step: "
                              "activations, weights, momentum, gradients)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

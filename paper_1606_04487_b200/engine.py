@@ -96,7 +96,7 @@ class GpuNet:
     """Device buffers + launch sequence for one NetSpec at a fixed max batch."""
 
     def __init__(self, net: NetSpec, batch: int, device=None, precision: str = "tf32",
-                 explicit_only: bool = False):
+                 explicit_only: bool = False, input_grad: bool = False, input_cs: int | None = None):
         if precision not in ("tf32", "3xtf32"):
             raise ValueError("precision must be 'tf32' or '3xtf32'")
         self.net = net
@@ -109,12 +109,18 @@ class GpuNet:
         self._zeros = z
         geom = net.geometry()
         c0 = net.in_channels
-        self.input = Act(True, c0, net.in_size, c0)
-        self.input.value = z(self.b, net.in_size, net.in_size, c0)
+        cs0 = c0 if input_cs is None else int(input_cs)   # pixel stride of the input
+        if cs0 < c0:
+            raise ValueError(f"input_cs {cs0} < channels {c0}")
+        self.input = Act(True, c0, net.in_size, cs0)
+        self.input.value = z(self.b, net.in_size, net.in_size, cs0)
         self.labels = z(self.b, dtype=torch.int32)
         self.ops: list[Op] = []
         cur = self.input
-        first_param = True
+        # input_grad: the gradient w.r.t. the input is needed too (the merged-FC
+        # head, whose input is the conv part's pool5 activation), so no layer is
+        # treated as the first parameter layer (that one skips its data gradient)
+        first_param = not input_grad
         i = 0
         while i < len(geom):
             g = geom[i]
@@ -212,6 +218,9 @@ class GpuNet:
             op.out.grad = z(*op.out.shape(self.b))
             if op.kind == "fc" and op.flat is not op.inp and not op.first_param_layer:
                 op.flat.grad = z(self.b, op.flat.cs)
+        if input_grad:
+            self.input.grad = z(*self.input.shape(self.b))
+        self.first_fc = next((i for i, op in enumerate(self.ops) if op.kind == "fc"), len(self.ops))
         self.loss_buf = z(1)
         self.dim = net.dim
         self.grad = z(self.dim)
@@ -364,10 +373,13 @@ class GpuNet:
         self._staged_for = W
 
     # ----------------------------------------------------------- forward --
-    def forward(self, W: torch.Tensor, b: int | None = None, need_grad: bool = True) -> torch.Tensor:
+    def forward(self, W: torch.Tensor, b: int | None = None, need_grad: bool = True,
+                stop: int | None = None) -> torch.Tensor:
         """Run the forward pass on self.input / self.labels (first b rows);
         leaves the mean loss in self.loss_buf and, if need_grad, dlogits in
-        the logits' grad buffer.  W is the flat fp32 parameter vector."""
+        the logits' grad buffer.  W is the flat fp32 parameter vector.
+        ``stop``: run ops[:stop] only (the conv part of a merged-FC mapping; no
+        loss) -- the activation then waits in ops[stop].inp.value."""
         b = self.b if b is None else int(b)
         staged = self._staged_for
         self._staged_for = None
@@ -375,7 +387,7 @@ class GpuNet:
             torch.cuda.current_stream(self.device).wait_event(self._staged_ev)
         if staged is None or staged is not W:
             self.stage_weights(W)
-        for op in self.ops:
+        for op in (self.ops if stop is None else self.ops[:stop]):
             L = op.layer
             if op.kind == "conv":
                 d = L.d_out
@@ -421,13 +433,16 @@ class GpuNet:
                 else:
                     self._gemm(b, d, op.f_in, op.flat.value, op.flat.cs, False, op.wstage,
                                op.flat.cs, False, op.out.value, op.out.cs, epi, bias)
+        if stop is not None:
+            return None
         C = self.net.classes
         K.softmax_xent(self.logits.value, self.logits.cs, self.labels, b, C, self.loss_buf,
                        self.logits.grad if need_grad else None, self.logits.cs, 1.0 / b)
         return self.loss_buf
 
     # ---------------------------------------------------------- backward --
-    def backward(self, b: int | None = None, on_grad=None, update=None) -> torch.Tensor:
+    def backward(self, b: int | None = None, on_grad=None, update=None,
+                 start: int | None = None) -> torch.Tensor:
         """Gradient of the mean loss w.r.t. the flat parameters -> self.grad.
 
         ``on_grad(lo, hi)`` (optional) is called as soon as the launches that
@@ -440,7 +455,10 @@ class GpuNet:
         momentum update (K8) layer by layer as soon as a layer's gradient is
         final and its data gradient no longer needs W, on a third stream: the
         FC layers' update (94% of CaffeNet's parameters) overlaps the conv
-        backward instead of ending the step."""
+        backward instead of ending the step.
+
+        ``start``: back-propagate through ops[:start] only, from the gradient
+        already placed in ops[start].inp.grad (merged-FC conv part)."""
         b = self.b if b is None else int(b)
         G = self.grad
         main = torch.cuda.current_stream(self.device)
@@ -490,7 +508,7 @@ class GpuNet:
                 net._ws_active = net.gemm_ws
                 return self.ctx.__exit__(*exc)
 
-        for op in reversed(self.ops):
+        for op in reversed(self.ops if start is None else self.ops[:start]):
             flush()
             L = op.layer
             if op.kind == "fc":

@@ -247,3 +247,21 @@ def get(name: str, **kw) -> NetSpec:
         return PRESETS[name](**kw)
     except KeyError:
         raise ValueError(f"unknown network {name!r}; choose from {sorted(PRESETS)}") from None
+
+
+def fc_head(net: NetSpec) -> tuple[NetSpec, int]:
+    """Split at the first fully connected layer (the merged-FC mapping,
+    PAPER.md:936-959): returns the FC head as its own NetSpec, whose input is
+    the conv part's last activation, and the flat-parameter offset where the
+    head's parameters start (FC layers come last in the packing, so the head's
+    parameter vector is W[offset:])."""
+    geo = net.geometry()
+    j = next((g.index for g in geo if g.layer.kind == "fc"), None)
+    if j is None or len(geo[j].in_shape) != 3:
+        raise ValueError("merged FC needs a conv part followed by fully connected layers")
+    c, n, _ = geo[j].in_shape
+    head = NetSpec(f"{net.name}_fc_head", c, n, tuple(net.layers[j:]))
+    off = geo[j].param_offsets[0]
+    if head.dim != net.dim - off:
+        raise ValueError("FC head parameters are not the tail of the packing")
+    return head, off

@@ -110,7 +110,7 @@ class DeviceSession:
     and the mean over ranks is folded into the fused update."""
 
     def __init__(self, problem: "CNNProblem", state: SGDState, hp: Hyperparams,
-                 process_group=None, use_graph: bool = True):
+                 process_group=None, use_graph: bool = True, merged_fc: bool = False):
         self.problem = problem
         self.hp = hp
         dev = problem.device
@@ -132,10 +132,26 @@ class DeviceSession:
         self._seen: dict = {}
         self._gidx = None
         self.world = 1
+        self.rank = 0
         if process_group is not None:
             import torch.distributed as dist
 
             self.world = dist.get_world_size(process_group)
+            self.rank = dist.get_rank(process_group)
+        # Merged FC: rank 0 runs the fully connected layers for
+        # the whole global batch on the gathered pool5 activations (FC model and
+        # FC compute co-located, FC gradients never exchanged); the conv part is
+        # data parallel and only the conv gradients are allreduced.
+        self.merged_fc = bool(merged_fc)
+        self.head = None
+        if self.merged_fc:
+            if process_group is None:
+                raise ValueError("merged_fc needs a process group (data parallel)")
+            head_spec, self.fc_off = nets.fc_head(problem.net)
+            if self.rank == 0:
+                f = self.engine.first_fc
+                self.head = GpuNet(head_spec, self.world * hp.b, dev, problem.precision,
+                                   input_grad=True, input_cs=self.engine.ops[f].inp.cs)
 
     def _allreduce_hook(self, works):
         import torch.distributed as dist
@@ -173,11 +189,58 @@ class DeviceSession:
         self._staged[id(batch)] = (slot, ready)
 
     # ------------------------------------------------------------ steps --
+    def _compute_merged(self, wr: torch.Tensor, b: int) -> None:
+        import torch.distributed as dist
+
+        hp, eng, pg = self.hp, self.engine, self.pg
+        f = eng.first_fc
+        eng.forward(wr, b, stop=f)                          # conv part, data parallel
+        act, dact = eng.ops[f].inp.value[:b], eng.ops[f].inp.grad[:b]
+        labels = eng.labels[:b]
+        head = self.head
+        root = dist.get_global_rank(pg, 0) if pg is not dist.group.WORLD else 0
+        if self.rank == 0:
+            gx = [head.input.value[r * b:(r + 1) * b] for r in range(self.world)]
+            gy = [head.labels[r * b:(r + 1) * b] for r in range(self.world)]
+        else:
+            gx = gy = None
+        dist.gather(act.contiguous(), gx, dst=root, group=pg)
+        dist.gather(labels.contiguous(), gy, dst=root, group=pg)
+        nb = self.world * b
+        if self.rank == 0:                                  # FC head on the whole global batch
+            Wfc = wr[self.fc_off:]
+            if Wfc.data_ptr() % 16:                         # the head stages from 16-byte-aligned W
+                if getattr(self, "_wfc", None) is None:
+                    self._wfc = torch.empty_like(Wfc)
+                self._wfc.copy_(Wfc)
+                Wfc = self._wfc
+            head.forward(Wfc, nb)
+            head.backward(nb)
+            sx = [head.input.grad[r * b:(r + 1) * b] for r in range(self.world)]
+        else:
+            sx = None
+        dist.scatter(dact, sx, src=root, group=pg)
+        works = []
+
+        def hook(lo, hi):   # conv gradients only; the head's 1/(N b) makes SUM the mean
+            w = dist.all_reduce(eng.grad[lo:hi], group=pg, async_op=True)
+            works.append(w)
+            return w
+
+        eng.backward(b, on_grad=hook, update=(self.W, self.V, wr, hp.eta, hp.mu, hp.lam), start=f)
+        for w in works:
+            w.wait()
+        if self.rank == 0:
+            K.sgd_momentum(self.W[self.fc_off:], self.V[self.fc_off:], head.grad, Wfc,
+                           hp.eta, hp.mu, hp.lam)
+
     def _compute(self, wr: torch.Tensor, b: int) -> None:
         """forward + backward (+ overlapped allreduce) + fused update on the batch
         already in the engine's input buffers."""
         hp = self.hp
-        if self.world > 1:
+        if self.merged_fc:
+            self._compute_merged(wr, b)
+        elif self.world > 1:
             # each layer's gradient is allreduced as soon as it exists and that
             # layer's update follows its allreduce (inside the backward)
             works = []
@@ -263,7 +326,16 @@ class DeviceSession:
         return self.problem.full_loss_device(self.W)
 
     def last_loss(self) -> float:
-        """Mean loss of the last step's batch (one 4-byte device-to-host read)."""
+        """Mean loss of the last step's batch (one 4-byte device-to-host read).
+        Merged FC: the global-batch loss, computed on rank 0 and broadcast
+        (a collective: every rank calls it)."""
+        if self.merged_fc:
+            import torch.distributed as dist
+
+            buf = (self.head.loss_buf if self.rank == 0 else torch.zeros(1, device=self.W.device))
+            root = dist.get_global_rank(self.pg, 0) if self.pg is not dist.group.WORLD else 0
+            dist.broadcast(buf, src=root, group=self.pg)
+            return float(buf.item())
         return float(self.engine.loss_buf.item())
 
     def loss_future(self) -> "LossFuture":
@@ -276,6 +348,17 @@ class DeviceSession:
         ev = torch.cuda.Event()
         ev.record()
         return LossFuture(dst, ev)
+
+    def sync_fc(self) -> None:
+        """Merged FC: copy rank 0's FC parameters and momentum to every rank
+        (the other ranks never update them).  A collective."""
+        if not self.merged_fc:
+            return
+        import torch.distributed as dist
+
+        root = dist.get_global_rank(self.pg, 0) if self.pg is not dist.group.WORLD else 0
+        dist.broadcast(self.W[self.fc_off:].contiguous(), src=root, group=self.pg)
+        dist.broadcast(self.V[self.fc_off:].contiguous(), src=root, group=self.pg)
 
     def state(self) -> SGDState:
         return SGDState(W=self.W.double().cpu().numpy(), V=self.V.double().cpu().numpy(), t=self.t)
@@ -416,8 +499,8 @@ class CNNProblem(TrainingProblem):
         return acc
 
     def device_session(self, state: SGDState, hp: Hyperparams, process_group=None,
-                       use_graph: bool = True) -> DeviceSession:
-        return DeviceSession(self, state, hp, process_group, use_graph)
+                       use_graph: bool = True, merged_fc: bool = False) -> DeviceSession:
+        return DeviceSession(self, state, hp, process_group, use_graph, merged_fc)
 
 
 def make_cnn(net: str, n_examples: int = 128, seed: int = 0, **kw) -> CNNProblem:

@@ -27,15 +27,18 @@ def main():
     torch.cuda.set_device(dev)
     dist.init_process_group("nccl", device_id=dev)
     net = sys.argv[1] if len(sys.argv) > 1 else "cifar10_quick"
+    merged = len(sys.argv) > 2 and sys.argv[2] == "merged"
     b, steps = 32, 4
     prob = CNNProblem(net, n_examples=256, seed=3, precision="3xtf32", device=dev)
     hp = Hyperparams(eta=0.01, mu=0.9, lam=5e-4, b=b)
     state = prob.initial_state()
     rng = np.random.default_rng(11)
     idx = [[rng.integers(0, 256, size=b) for _ in range(world)] for _ in range(steps)]
-    sess = prob.device_session(state, hp, process_group=dist.group.WORLD)
+    sess = prob.device_session(state, hp, process_group=dist.group.WORLD, merged_fc=merged)
     for t in range(steps):
         sess.step(DeviceBatch(torch.from_numpy(idx[t][rank]).to(dev)))
+    loss = sess.last_loss()            # (merged FC: a collective)
+    sess.sync_fc()
     torch.cuda.synchronize()
     W_dp = sess.W.double().cpu().numpy()
     if rank == 0:
@@ -52,7 +55,8 @@ def main():
             V = hp.mu * V - hp.eta * (G + hp.lam * W)
             W = W + V
         rel = float(np.linalg.norm(W_dp - W) / np.linalg.norm(W))
-        print(f"{net}: N={world} data-parallel session vs replay: normwise {rel:.3e}")
+        print(f"{net}: N={world} data-parallel{' merged-FC' if merged else ''} session vs replay: "
+              f"normwise {rel:.3e} (last loss {loss:.4f})")
         assert rel < 1e-5, rel
     dist.destroy_process_group()
 
