@@ -1393,7 +1393,8 @@ int omni_gemm_f32(int precision, int M, int N, int K, const float* A, long long 
 // K = 576, is faster untransposed).
 static bool conv_fprop_transposed(int d_out, int pixels, int K) {
   static const bool off = getenv("OMNI_NO_TRANSPOSED_FPROP") != nullptr;
-  return !off && d_out <= 128 && pixels >= 128 * 148 && K >= 2048;
+  static const bool force = getenv("OMNI_FORCE_TRANSPOSED_FPROP") != nullptr;   // tuning probe
+  return !off && d_out <= 128 && pixels >= 128 * 148 && (K >= 2048 || force);
 }
 
 static int conv_shape(int op, int b, int n, int c, int k, int stride, int pad, int d_out, int* M,
