@@ -214,3 +214,196 @@ def replay(events: list, plan: ExecutionPlan, backend, hp: Hyperparams, W0: torc
         backend.sgd(W, V, G, snaps[e.group_id], hp_sum)
         snaps[e.group_id] = W.clone()
     return W, V
+
+
+# ----------------------------------------------------------- merged FC --
+# The paper's physical mapping: the server also owns the
+# fully connected layers.  A group runs its conv forward on its (stale)
+# snapshot, ships the pool5 activations to the server, which runs the FC
+# layers with the CURRENT FC model, updates it at once (FC staleness 0) and
+# returns d(pool5); the group back-propagates the conv part and ships the conv
+# gradient, which the server applies FIFO like above.  Groups of one GPU.
+
+@dataclass(frozen=True)
+class MergedEvent:
+    kind: str            # "fc" (FC update from a group's activations) or "conv"
+    group_id: int
+    read_step: int       # conv model version the group computed on
+    write_step: int      # conv model version after this event (conv events advance it)
+    fc_step: int         # FC model version after this event
+    arrive_time: float
+    batch_index: int
+
+
+def _split_buffers(eng, b):
+    f = eng.first_fc
+    return f, eng.ops[f].inp.value[:b], eng.ops[f].inp.grad[:b]
+
+
+def run_server_merged(plan: ExecutionPlan, head, hp: Hyperparams, W0: torch.Tensor, fc_off: int,
+                      act_shape: tuple, max_updates: int):
+    """Rank 0 with merged FC.  ``head``: a GpuNet for the FC layers at the group
+    batch with input_grad=True.  Returns (events, W, V, seconds)."""
+    from . import kernels as K
+
+    if plan.k != 1:
+        raise ValueError("merged-FC asynchronous groups use one GPU per group (k = 1)")
+    _, pair = _new_groups(plan)
+    if dist.get_backend() != "nccl":
+        raise RuntimeError("merged-FC asynchronous groups need NCCL (CUDA engines)")
+    dev = W0.device
+    W = W0.clone()
+    V = torch.zeros_like(W)
+    b = hp.b
+    leaders = [worker_ranks(plan, i)[0] for i in range(plan.g)]
+    acts = [torch.empty(act_shape, device=dev) for _ in range(plan.g)]
+    labs = [torch.empty(b, dtype=torch.int32, device=dev) for _ in range(plan.g)]
+    grads = [torch.empty(fc_off, device=dev) for _ in range(plan.g)]
+    snaps = [W0[:fc_off].clone() for _ in range(plan.g)]
+    read_step = [0] * plan.g
+    drawn = [0] * plan.g
+    phase = ["act"] * plan.g
+    go = torch.ones(1, dtype=torch.int32, device=dev)
+    stop = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def post(i):
+        if phase[i] == "act":
+            return [dist.irecv(acts[i], src=leaders[i], group=pair[i]),
+                    dist.irecv(labs[i], src=leaders[i], group=pair[i])]
+        return [dist.irecv(grads[i], src=leaders[i], group=pair[i])]
+
+    pending = [post(i) for i in range(plan.g)]
+    events = []
+    t = fc_t = 0
+    t0 = time.perf_counter()
+    Wfc, Vfc = W[fc_off:], V[fc_off:]
+    while t < max_updates:
+        i = None
+        while i is None:
+            for j in range(plan.g):
+                if all(w.is_completed() for w in pending[j]):
+                    i = j
+                    break
+            if i is None:
+                time.sleep(0)
+        for w in pending[i]:
+            w.wait()
+        if phase[i] == "act":                       # FC phase for group i, current FC model
+            head.input.value[:b].copy_(acts[i])
+            head.labels[:b].copy_(labs[i])
+            head.forward(Wfc, b)
+            head.backward(b)
+            K.sgd_momentum(Wfc, Vfc, head.grad, Wfc, hp.eta, hp.mu, hp.lam)
+            fc_t += 1
+            events.append(MergedEvent("fc", i, read_step[i], t, fc_t, time.perf_counter() - t0,
+                                      drawn[i]))
+            dist.send(head.input.grad[:b].contiguous(), dst=leaders[i], group=pair[i])
+            phase[i] = "grad"
+        else:                                        # conv update, FIFO, stale snapshot
+            K.sgd_momentum(W[:fc_off], V[:fc_off], grads[i], snaps[i], hp.eta, hp.mu, hp.lam)
+            t += 1
+            events.append(MergedEvent("conv", i, read_step[i], t, fc_t, time.perf_counter() - t0,
+                                      drawn[i]))
+            drawn[i] += 1
+            snaps[i].copy_(W[:fc_off])
+            read_step[i] = t
+            phase[i] = "act"
+            if t < max_updates:
+                dist.send(go, dst=leaders[i], group=pair[i])
+                dist.send(snaps[i], dst=leaders[i], group=pair[i])
+            else:
+                dist.send(stop, dst=leaders[i], group=pair[i])
+                pending[i] = []
+                continue
+        pending[i] = post(i)
+    torch.cuda.synchronize(dev)
+    seconds = time.perf_counter() - t0
+    # drain: finish every other group's current iteration, then stop it
+    for i in range(plan.g):
+        if not pending[i]:
+            continue
+        while True:
+            for w in pending[i]:
+                w.wait()
+            if phase[i] == "act":                   # serve its FC phase without updating
+                head.input.value[:b].copy_(acts[i])
+                head.labels[:b].copy_(labs[i])
+                head.forward(Wfc, b)
+                head.backward(b)
+                dist.send(head.input.grad[:b].contiguous(), dst=leaders[i], group=pair[i])
+                phase[i] = "grad"
+                pending[i] = post(i)
+                continue
+            dist.send(stop, dst=leaders[i], group=pair[i])
+            break
+    return events, W, V, seconds
+
+
+def run_worker_merged(plan: ExecutionPlan, eng, problem, hp: Hyperparams, W0: torch.Tensor,
+                      fc_off: int, seed: int) -> int:
+    """Ranks 1..g (one GPU per group): conv forward -> activations to the
+    server -> d(pool5) back -> conv backward -> conv gradient to the server."""
+    rank = dist.get_rank()
+    _, pair = _new_groups(plan)
+    group = rank - 1
+    sg = pair[group]
+    b = hp.b
+    rng = batch_stream(seed, group)
+    W = W0.clone()
+    f, act, dact = _split_buffers(eng, b)
+    flag = torch.zeros(1, dtype=torch.int32, device=W.device)
+    n = 0
+    while True:
+        idx = torch.from_numpy(rng.integers(0, problem._n, size=b)).to(W.device)
+        eng.gather_batch(problem.data, problem.data_labels, idx)
+        eng.forward(W, b, stop=f)
+        dist.send(act.contiguous(), dst=0, group=sg)
+        dist.send(eng.labels[:b].contiguous(), dst=0, group=sg)
+        dist.recv(dact, src=0, group=sg)
+        eng.backward(b, start=f)
+        dist.send(eng.grad[:fc_off].contiguous(), dst=0, group=sg)
+        dist.recv(flag, src=0, group=sg)
+        n += 1
+        if int(flag.item()) == 0:
+            return n
+        dist.recv(W[:fc_off], src=0, group=sg)
+
+
+def replay_merged(events: list, plan: ExecutionPlan, eng, head, problem, hp: Hyperparams,
+                  W0: torch.Tensor, fc_off: int, seed: int):
+    """Re-apply a merged-FC run's log in order on one device (bit-exact: same
+    kernels, same batches; a group's conv forward is recomputed from its
+    snapshot before its backward)."""
+    from . import kernels as K
+
+    b = hp.b
+    W = W0.clone()
+    V = torch.zeros_like(W)
+    Wfc, Vfc = W[fc_off:], V[fc_off:]
+    rngs = [batch_stream(seed, i) for i in range(plan.g)]
+    snaps = [W0.clone() for _ in range(plan.g)]      # full-size vectors; conv part used
+    idx_of = {}
+    dacts = {}
+    f, act, dact = _split_buffers(eng, b)
+    for e in events:
+        i = e.group_id
+        if e.kind == "fc":
+            idx = torch.from_numpy(rngs[i].integers(0, problem._n, size=b)).to(W.device)
+            idx_of[i] = idx
+            eng.gather_batch(problem.data, problem.data_labels, idx)
+            eng.forward(snaps[i], b, stop=f)
+            head.input.value[:b].copy_(act)
+            head.labels[:b].copy_(eng.labels[:b])
+            head.forward(Wfc, b)
+            head.backward(b)
+            K.sgd_momentum(Wfc, Vfc, head.grad, Wfc, hp.eta, hp.mu, hp.lam)
+            dacts[i] = head.input.grad[:b].clone()
+        else:
+            eng.gather_batch(problem.data, problem.data_labels, idx_of[i])
+            eng.forward(snaps[i], b, stop=f)
+            dact.copy_(dacts[i])
+            eng.backward(b, start=f)
+            K.sgd_momentum(W[:fc_off], V[:fc_off], eng.grad[:fc_off], snaps[i][:fc_off],
+                           hp.eta, hp.mu, hp.lam)
+            snaps[i][:fc_off].copy_(W[:fc_off])
+    return W, V
