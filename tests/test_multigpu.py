@@ -1,0 +1,48 @@
+"""Multi-GPU parity checks (NCCL, one process per GPU), run through torchrun
+when the box has >= 2 GPUs (skipped on single-GPU boxes):
+
+* data-parallel DeviceSession (per-layer async allreduce, layer-wise update)
+  and its merged-FC variant == the float64 replay of the mean-gradient update;
+* the round-synchronous compute-group runtime == the oracle's deterministic
+  simulate (event log and weights)."""
+
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def torchrun(n, script, *args):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}",
+           os.path.join(ROOT, "tools", script), *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    return r.stdout
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("mode", ["", "merged"])
+def test_data_parallel_session_equals_replay(mode):
+    out = torchrun(2, "dp_check.py", "cifar10_quick", *([mode] if mode else []))
+    assert "normwise" in out
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_group_runtime_equals_oracle_schedule():
+    out = torchrun(2, "groups_check.py")
+    assert '"pass": true' in out
