@@ -38,25 +38,29 @@ def test_graph_replay_equals_eager(net, b):
     assert torch.equal(W0, W1) and torch.equal(V0, V1) and l0 == l1
 
 
-def test_prefetched_host_batches_equal_device_batches():
-    prob = CNNProblem("cifar10_quick", n_examples=32, seed=5, precision="tf32")
-    hp = P.Hyperparams(eta=0.01, mu=0.9, b=8)
+@pytest.mark.parametrize("net,b", [("cifar10_quick", 8), ("caffenet", 4)])
+def test_prefetched_host_batches_equal_device_batches(net, b):
+    """caffenet: the host batch goes through the zero-copy space-to-depth kernel
+    (transfer + conv1 layout in one pass); the device batch through the fused
+    gather + space-to-depth.  Both must give the same weights, bit for bit."""
+    prob = CNNProblem(net, n_examples=32, seed=5, precision="tf32")
+    hp = P.Hyperparams(eta=0.01, mu=0.9, b=b)
     state = prob.initial_state()
     rng = np.random.default_rng(1)
-    idxs = [rng.integers(0, 32, size=8) for _ in range(6)]
+    idxs = [rng.integers(0, 32, size=b) for _ in range(6)]
     a = prob.device_session(state, hp, use_graph=False)
     for idx in idxs:
         a.step(DeviceBatch(torch.from_numpy(idx).cuda()))
-    b = prob.device_session(state, hp)   # graphed: steps 2.. replay per-slot graphs
+    sb = prob.device_session(state, hp)   # graphed: steps 2.. replay per-slot graphs
     hbs = [HostBatch(prob.data[torch.from_numpy(i).cuda()].cpu().pin_memory(),
                      prob.data_labels[torch.from_numpy(i).cuda()].cpu().pin_memory()) for i in idxs]
-    b.prefetch(hbs[0])
+    sb.prefetch(hbs[0])
     for i, hb in enumerate(hbs):
-        b.step(hb)
+        sb.step(hb)
         if i + 1 < len(hbs):
-            b.prefetch(hbs[i + 1])
+            sb.prefetch(hbs[i + 1])
     torch.cuda.synchronize()
-    assert torch.equal(a.W, b.W) and torch.equal(a.V, b.V)
+    assert torch.equal(a.W, sb.W) and torch.equal(a.V, sb.V)
 
 
 def test_loss_future_matches_last_loss():
