@@ -75,3 +75,30 @@ def test_loss_future_matches_last_loss():
             futs[i - 2].result()
         sync.append(sess.last_loss())
     assert [f.result() for f in futs] == sync
+
+
+def test_ragged_batch_step_equals_oracle_update():
+    """A step on a batch smaller than the session's b (the eager path) is the
+    momentum update with the mean gradient over exactly those images."""
+    from oracle import refcnn as R
+
+    prob = CNNProblem("lenet", n_examples=32, seed=6, precision="3xtf32")
+    hp = P.Hyperparams(eta=0.05, mu=0.9, lam=1e-3, b=8)
+    state = prob.initial_state()
+    sess = prob.device_session(state, hp)
+    idx = np.array([3, 17, 5, 29, 11])                       # 5 < b = 8
+    sess.step(DeviceBatch(torch.from_numpy(idx).cuda()))
+    X = prob.data[torch.from_numpy(idx).cuda()].permute(0, 3, 1, 2).double().cpu().numpy()
+    y = prob.data_labels[torch.from_numpy(idx).cuda()].long().cpu().numpy()
+    g = R.grad(prob.net.to_dicts(), 1, 28, state.W, X, y)
+    V = -hp.eta * (g + hp.lam * state.W)
+    W = state.W + V
+    got = sess.W.double().cpu().numpy()
+    assert np.linalg.norm(got - W) / np.linalg.norm(W) < 1e-6
+
+
+def test_empty_batch_fails_loudly():
+    prob = CNNProblem("lenet", n_examples=16, seed=6, precision="tf32")
+    sess = prob.device_session(prob.initial_state(), P.Hyperparams(eta=0.01, b=8))
+    with pytest.raises((ValueError, RuntimeError)):
+        sess.step(DeviceBatch(torch.zeros(0, dtype=torch.int64, device="cuda")))
