@@ -82,7 +82,7 @@ class GroupEvent:
 
 class GroupRuntime:
     def __init__(self, plan: ExecutionPlan, backend: Backend, hp: Hyperparams, W0: torch.Tensor,
-                 n_examples: int, seed: int):
+                 n_examples: int, seed: int, sharded: bool = True):
         if not dist.is_initialized():
             raise RuntimeError("GroupRuntime needs torch.distributed initialised (one rank per GPU)")
         world, rank = dist.get_world_size(), dist.get_rank()
@@ -98,17 +98,48 @@ class GroupRuntime:
         # every rank creates every subgroup, in the same order (torch.distributed rule)
         self.group_pgs = [dist.new_group(plan.group_ranks(i)) for i in range(plan.g)]
         self.cross_pgs = [dist.new_group([i * plan.k + j for i in range(plan.g)]) for j in range(plan.k)]
-        self.W = W0.clone()
-        self.V = torch.zeros_like(self.W)
-        self.snaps = [self.W.clone() for _ in range(plan.g)]
+        self.sharded = bool(sharded)
         self.snap_step = [0] * plan.g
         self.t = 0
         self.rng = batch_stream(seed, self.group)
         self.events: list[GroupEvent] = []
-        self._gather = [torch.empty_like(self.W) for _ in range(plan.g)]
+        self.dim = W0.numel()
+        if self.sharded:
+            # rank r owns elements [r*S, (r+1)*S) of W, V and of every group's snapshot
+            N = world
+            S = -(-self.dim // N)
+            S = -(-S // 4) * 4                     # 16-byte aligned shards
+            self._S = S
+            lo, hi = rank * S, min((rank + 1) * S, self.dim)
+            self._W = torch.zeros(S, dtype=W0.dtype, device=W0.device)
+            self._W[:max(0, hi - lo)] = W0[lo:hi]
+            self._V = torch.zeros_like(self._W)
+            self._snapsh = [self._W.clone() for _ in range(plan.g)]
+            self._snap_own = W0.clone()              # this rank's group snapshot, full length
+            self._pad = torch.zeros(N * S - self.dim, dtype=W0.dtype, device=W0.device)
+        else:
+            self._W = W0.clone()
+            self._V = torch.zeros_like(self._W)
+            self.snaps = [self._W.clone() for _ in range(plan.g)]
+            self._gather = [torch.empty_like(self._W) for _ in range(plan.g)]
         # gradients arrive as the SUM of k slice means; fold the 1/k into the fused
         # update: eta (G/k + lam w) = (eta/k) (G + k lam w)
         self._hp_sum = hp.replace(eta=hp.eta / plan.k, lam=hp.lam * plan.k)
+
+    def _full(self, shard: torch.Tensor) -> torch.Tensor:
+        parts = [torch.empty_like(shard) for _ in range(self.plan.N)]
+        dist.all_gather(parts, shard)
+        return torch.cat(parts)[:self.dim]
+
+    @property
+    def W(self) -> torch.Tensor:
+        """The master model (sharded runtime: assembled from every rank's shard,
+        a collective -- every rank calls it)."""
+        return self._full(self._W) if self.sharded else self._W
+
+    @property
+    def V(self) -> torch.Tensor:
+        return self._full(self._V) if self.sharded else self._V
 
     def _my_slice(self, idx: np.ndarray) -> np.ndarray:
         per = self.hp.b // self.plan.k
@@ -120,6 +151,8 @@ class GroupRuntime:
 
     def round(self) -> None:
         """One round = g master updates, one per group, in group order."""
+        if self.sharded:
+            return self._round_sharded()
         plan = self.plan
         idx = self.rng.integers(0, self.n_examples, size=self.hp.b)
         G = self.backend.grad(self.snaps[self.group], self._my_slice(idx))
@@ -131,8 +164,38 @@ class GroupRuntime:
         else:
             grads = [G]
         for i in range(plan.g):
-            self.backend.sgd(self.W, self.V, grads[i], self.snaps[i], self._hp_sum)
+            self.backend.sgd(self._W, self._V, grads[i], self.snaps[i], self._hp_sum)
             self.t += 1
             self.events.append(GroupEvent(i, self.snap_step[i], self.t, self.t - 1 - self.snap_step[i]))
-            self.snaps[i].copy_(self.W)       # group i reads W(t) next round
+            self.snaps[i].copy_(self._W)      # group i reads W(t) next round
             self.snap_step[i] = self.t
+
+    def _round_sharded(self) -> None:
+        """The same round with the update work partitioned: one all-to-all gives
+        every rank its shard of each group's gradient (summed over the group's
+        members in member order), each rank applies the g ordered updates to its
+        shard of W, V and of the g snapshots, and a second all-to-all returns to
+        every rank its own group's next snapshot.  Per-rank traffic ~2 models
+        per round (vs a group allreduce plus g models gathered), update work g/N
+        models (vs g)."""
+        plan, N, S = self.plan, self.plan.N, self._S
+        idx = self.rng.integers(0, self.n_examples, size=self.hp.b)
+        G = self.backend.grad(self._snap_own, self._my_slice(idx))
+        send = torch.cat([G, self._pad]) if self._pad.numel() else G
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send)              # row m of recv = rank m's gradient, my shard
+        rows = recv.view(N, S)
+        for i in range(plan.g):
+            ranks = plan.group_ranks(i)
+            Gi = rows[ranks[0]].clone()
+            for m in ranks[1:]:
+                Gi.add_(rows[m])                          # sum of the group's k slice means
+            self.backend.sgd(self._W, self._V, Gi, self._snapsh[i], self._hp_sum)
+            self.t += 1
+            self.events.append(GroupEvent(i, self.snap_step[i], self.t, self.t - 1 - self.snap_step[i]))
+            self._snapsh[i].copy_(self._W)
+            self.snap_step[i] = self.t
+        out = torch.stack([self._snapsh[plan.group_of(m)] for m in range(N)])   # row m -> rank m
+        back = torch.empty_like(out)
+        dist.all_to_all_single(back, out)                # row j = shard j of my group's snapshot
+        self._snap_own = back.view(-1)[:self.dim].clone()

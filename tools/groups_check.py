@@ -42,6 +42,7 @@ def main():
     rt = GroupRuntime(plan, CudaBackend(prob, hp.b // plan.k), hp, W0, prob.n_examples, seed=11)
     rt.run(args.rounds)
     torch.cuda.synchronize()
+    W_master = rt.W                      # (sharded runtime: a collective, every rank)
     if dist.get_rank() == 0:
         layers = R.tiny_cnn_layers(8, 4)
 
@@ -54,7 +55,7 @@ def main():
 
         Wr, _, ev = R.simulate(grad_fn, sample_fn, prob.initial_weights(), args.g, 4.0, 0.5, hp.eta,
                                hp.mu, hp.lam, hp.b, args.rounds * args.g, seed=11)
-        got = rt.W.double().cpu().numpy()
+        got = W_master.double().cpu().numpy()
         err = float(np.linalg.norm(got - Wr) / np.linalg.norm(Wr))
         ev_ok = [(e.group_id, e.read_step, e.write_step, e.staleness) for e in rt.events] == \
                 [tuple(e[:4]) for e in ev]
