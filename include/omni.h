@@ -105,8 +105,11 @@ int omni_gemm_f32(int precision, int M, int N, int K, const float* A, long long 
                   long long ldc, int epilogue, const float* bias, const float* aux,
                   long long ld_aux, float* workspace, long long ws_bytes, void* stream);
 
-/* Implicit-GEMM convolution on tcgen05, operands gathered by TMA im2col from
- * the NHWC activation X (b, n, n, cs) -- no lowered matrix in HBM.  The GEMM
+/* Implicit-GEMM convolution on tcgen05 -- replaces tensors.conv_lowered
+ * (tensors.py:222-256: lower + gemm + lift) for the training path, and the
+ * weight-gradient einsum of problems.py:263-267 -- with the operands gathered
+ * by TMA im2col from the NHWC activation X (b, n, n, cs): no lowered matrix in
+ * HBM.  The GEMM
  * K index is (tap, channel) tap-major, i.e. the column order of
  * omni_lower_nhwc_f32.  Requires d_in = c multiple of 32.
  *   OMNI_CONV_FPROP: Y[pix, o] (op)= sum_{tap,ch} X(pix, tap, ch) G[o*ldg + tap*c + ch]
@@ -177,7 +180,9 @@ int omni_gather_rows_f32(const float* src, long long row_elems, const int64_t* i
                          float* dst, void* stream);
 int omni_gather_i32(const int32_t* src, const int64_t* idx, int nidx, int32_t* dst,
                     void* stream);
-/* Weight layout staging: OIHW (o,c,k,k) <-> tap-major (o, (kx*k+ky)*c + ch)
+/* Weight layout staging (the device counterpart of tensors.lower_kernel,
+ * tensors.py:184-190, in tap-major column order):
+ * OIHW (o,c,k,k) <-> tap-major (o, (kx*k+ky)*c + ch)
  * rows of stride ld (pad columns zeroed).  inverse=0 reads W and writes Wt;
  * inverse=1 reads Wt and writes W.  bias (may be NULL) travels in column
  * c*k*k of Wt in the same direction.                                       */
@@ -187,7 +192,8 @@ int omni_conv_weight_to_tap_f32(float* W, int o, int c, int k, float* Wt, long l
  * Wf[ch*ld + (kx*k + ky)*o + oo] = W[oo, ch, k-1-kx, k-1-ky] (W is OIHW).     */
 int omni_conv_weight_flip_f32(const float* W, int o, int c, int k, float* Wf, long long ld,
                               void* stream);
-/* Space-to-depth with channel padding (first-layer implicit GEMM): X (b, n, n,
+/* Space-to-depth with channel padding (first-layer implicit GEMM; part of
+ * conv_lowered, tensors.py:222-256, for strided narrow layers): X (b, n, n,
  * pixel stride cs, c channels) -> Y (b, n2, n2, cp),
  * Y[img, X, Y, (dx*s + dy)*c + ch] = X[img, s*X + dx, s*Y + dy, ch], zero outside
  * the image and in channels >= s*s*c.  A stride-s k x k conv of X equals a
