@@ -106,3 +106,28 @@ def test_simconfig_validation():
                     service_mode="x", max_updates=1)
     with pytest.raises(ValueError, match="need max_updates"):
         P.SimConfig(plan=P.ExecutionPlan(2, 2), profile=prof, hp=hp, problem=None)
+
+
+@pytest.mark.parametrize("name", ["caffenet", "lenet", "cifar10_quick", "vgg16"])
+def test_fc_head_split(name):
+    """The merged-FC split: the head is the FC tail of the network and its
+    parameters are the tail of the flat packing (problems.py:201-204)."""
+    net = nets.get(name)
+    head, off = nets.fc_head(net)
+    assert all(L.kind in ("fc", "relu") for L in head.layers)
+    assert head.dim == net.dim - off and head.classes == net.classes
+    first_fc = next(g for g in net.geometry() if g.layer.kind == "fc")
+    assert (head.in_channels, head.in_size, head.in_size) == first_fc.in_shape
+    assert off == first_fc.param_offsets[0]
+
+
+def test_bench_l2_note_classifies_working_sets():
+    import importlib.util
+    import os
+
+    spec = importlib.util.spec_from_file_location(
+        "bench", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    assert "> 126 MB L2" in bench.l2_note(nets.get("caffenet"), 256)
+    assert "fits in L2" in bench.l2_note(nets.get("lenet"), 64)
