@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--mu", type=float, default=0.9)
     ap.add_argument("--lam", type=float, default=5e-4)
     ap.add_argument("--profile-out", default="", help="write per-GEMM timing breakdown (json)")
+    ap.add_argument("--groups-overlap", action="store_true",
+                    help="--groups: layer-aligned shards, gradient exchange overlapped with the backward")
     ap.add_argument("--merged-fc", action="store_true",
                     help="N > 1: FC layers on rank 0 for the global batch (PAPER.md:936-959)")
     ap.add_argument("--groups", type=int, default=1,
@@ -442,7 +444,8 @@ def run_groups(args, net, dev, world, rank, local):
     gw = torch.Generator(device=dev)
     gw.manual_seed(args.seed)
     W0 = 0.01 * torch.randn(net.dim, generator=gw, device=dev)
-    rt = GroupRuntime(plan, CudaBackend(prob, args.batch), hp, W0, args.n_examples, args.seed)
+    rt = GroupRuntime(plan, CudaBackend(prob, args.batch), hp, W0, args.n_examples, args.seed,
+                      overlap=args.groups_overlap)
     rt.run(args.warmup)
     torch.cuda.synchronize()
     dist.barrier()

@@ -71,6 +71,26 @@ class CudaBackend:
 
         K.sgd_momentum(W, V, G, w_read, hp.eta, hp.mu, hp.lam)
 
+    def layer_ranges(self) -> list:
+        """Parameter ranges [lo, hi) of the layers, in backward order (the
+        order the engine's on_grad hook reports them)."""
+        out = []
+        for op in reversed(self.engine.ops):
+            if op.kind in ("conv", "fc"):
+                hi = op.boff + op.layer.d_out if op.boff >= 0 else op.woff + op.wsz
+                out.append((op.woff, hi))
+        return out
+
+    def grad_hooked(self, W, idx, on_grad) -> None:
+        """Gradient with on_grad(lo, hi) called as each layer's gradient is
+        enqueued (for overlapped per-layer exchanges); the gradient stays in
+        self.engine.grad."""
+        from .problems import Batch
+
+        b = self.problem.load_batch(self.engine, Batch(self.problem, idx))
+        self.engine.forward(W, b)
+        self.engine.backward(b, on_grad=on_grad)
+
 
 @dataclass(frozen=True)
 class GroupEvent:
@@ -82,7 +102,7 @@ class GroupEvent:
 
 class GroupRuntime:
     def __init__(self, plan: ExecutionPlan, backend: Backend, hp: Hyperparams, W0: torch.Tensor,
-                 n_examples: int, seed: int, sharded: bool = True):
+                 n_examples: int, seed: int, sharded: bool = True, overlap: bool = False):
         if not dist.is_initialized():
             raise RuntimeError("GroupRuntime needs torch.distributed initialised (one rank per GPU)")
         world, rank = dist.get_world_size(), dist.get_rank()
@@ -99,6 +119,7 @@ class GroupRuntime:
         self.group_pgs = [dist.new_group(plan.group_ranks(i)) for i in range(plan.g)]
         self.cross_pgs = [dist.new_group([i * plan.k + j for i in range(plan.g)]) for j in range(plan.k)]
         self.sharded = bool(sharded)
+        self._layered = False
         self.snap_step = [0] * plan.g
         self.t = 0
         self.rng = batch_stream(seed, self.group)
@@ -117,6 +138,9 @@ class GroupRuntime:
             self._snapsh = [self._W.clone() for _ in range(plan.g)]
             self._snap_own = W0.clone()              # this rank's group snapshot, full length
             self._pad = torch.zeros(N * S - self.dim, dtype=W0.dtype, device=W0.device)
+            self._layered = bool(overlap) and hasattr(backend, "grad_hooked")
+            if self._layered:
+                self._init_layered(W0)
         else:
             self._W = W0.clone()
             self._V = torch.zeros_like(self._W)
@@ -126,9 +150,42 @@ class GroupRuntime:
         # update: eta (G/k + lam w) = (eta/k) (G + k lam w)
         self._hp_sum = hp.replace(eta=hp.eta / plan.k, lam=hp.lam * plan.k)
 
+    def _init_layered(self, W0: torch.Tensor) -> None:
+        """Layer-aligned shards: every layer's range [lo, hi) is split into N
+        pieces of q = ceil(len/N); rank r owns piece r of every layer, so each
+        layer's gradient can be exchanged (all-to-all) as soon as it exists."""
+        N, r = self.plan.N, self.rank
+        dev = W0.device
+        self._layers = []                 # (lo, hi, q, shard offset), backward order
+        off = 0
+        for lo, hi in self.backend.layer_ranges():
+            q = -(-(hi - lo) // N)
+            self._layers.append((lo, hi, q, off))
+            off += q
+        S = off
+        self._S = S
+        # gather index: full vector element -> position in the (N, S) array of shards
+        gidx = torch.empty(self.dim, dtype=torch.int64)
+        for lo, hi, q, o in self._layers:
+            e = torch.arange(hi - lo)
+            gidx[lo:hi] = (e // q) * S + o + (e % q)
+        self._gidx = gidx.to(dev)
+        sh = torch.zeros(S, dtype=W0.dtype, device=dev)
+        for lo, hi, q, o in self._layers:
+            a, z = lo + r * q, min(lo + (r + 1) * q, hi)
+            if z > a:
+                sh[o:o + (z - a)] = W0[a:z]
+        self._W = sh
+        self._V = torch.zeros_like(sh)
+        self._snapsh = [sh.clone() for _ in range(self.plan.g)]
+        self._send = {lo: torch.zeros(N * q, dtype=W0.dtype, device=dev) for lo, hi, q, o in self._layers}
+        self._recv = {lo: torch.empty(N * q, dtype=W0.dtype, device=dev) for lo, hi, q, o in self._layers}
+
     def _full(self, shard: torch.Tensor) -> torch.Tensor:
         parts = [torch.empty_like(shard) for _ in range(self.plan.N)]
         dist.all_gather(parts, shard)
+        if getattr(self, "_layered", False):
+            return torch.cat(parts)[self._gidx]
         return torch.cat(parts)[:self.dim]
 
     @property
@@ -152,7 +209,7 @@ class GroupRuntime:
     def round(self) -> None:
         """One round = g master updates, one per group, in group order."""
         if self.sharded:
-            return self._round_sharded()
+            return self._round_layered() if self._layered else self._round_sharded()
         plan = self.plan
         idx = self.rng.integers(0, self.n_examples, size=self.hp.b)
         G = self.backend.grad(self.snaps[self.group], self._my_slice(idx))
@@ -169,6 +226,45 @@ class GroupRuntime:
             self.events.append(GroupEvent(i, self.snap_step[i], self.t, self.t - 1 - self.snap_step[i]))
             self.snaps[i].copy_(self._W)      # group i reads W(t) next round
             self.snap_step[i] = self.t
+
+    def _round_layered(self) -> None:
+        """_round_sharded with layer-aligned shards: each layer's gradient
+        all-to-all is issued from the backward's on_grad hook, overlapping the
+        rest of the backward; group sums, the g ordered updates and the
+        snapshot exchange are as in _round_sharded."""
+        plan, N, S = self.plan, self.plan.N, self._S
+        idx = self.rng.integers(0, self.n_examples, size=self.hp.b)
+        works = []
+        G = self.backend.engine.grad
+        lens = {lo: hi - lo for lo, hi, q, o in self._layers}
+
+        def hook(lo, hi):
+            send = self._send[lo]
+            send[:lens[lo]].copy_(G[lo:hi])                    # (on the gradient's stream)
+            works.append(dist.all_to_all_single(self._recv[lo], send, async_op=True))
+
+        self.backend.grad_hooked(self._snap_own, self._my_slice(idx), hook)
+        for w in works:
+            w.wait()
+        grads = [torch.empty(S, dtype=self._W.dtype, device=self._W.device) for _ in range(plan.g)]
+        for lo, hi, q, o in self._layers:
+            rows = self._recv[lo].view(N, q)
+            for i in range(plan.g):
+                ranks = plan.group_ranks(i)
+                gi = grads[i][o:o + q]
+                gi.copy_(rows[ranks[0]])
+                for m in ranks[1:]:
+                    gi.add_(rows[m])
+        for i in range(plan.g):
+            self.backend.sgd(self._W, self._V, grads[i], self._snapsh[i], self._hp_sum)
+            self.t += 1
+            self.events.append(GroupEvent(i, self.snap_step[i], self.t, self.t - 1 - self.snap_step[i]))
+            self._snapsh[i].copy_(self._W)
+            self.snap_step[i] = self.t
+        out = torch.stack([self._snapsh[plan.group_of(m)] for m in range(N)])
+        back = torch.empty_like(out)
+        dist.all_to_all_single(back, out)
+        self._snap_own = back.view(-1)[self._gidx]
 
     def _round_sharded(self) -> None:
         """The same round with the update work partitioned: one all-to-all gives
