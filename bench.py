@@ -64,6 +64,9 @@ def parse():
     ap.add_argument("--profile-out", default="", help="write per-GEMM timing breakdown (json)")
     ap.add_argument("--groups-overlap", action="store_true",
                     help="--groups: layer-aligned shards, gradient exchange overlapped with the backward")
+    ap.add_argument("--nccl-allreduce", dest="p2p", action="store_false",
+                    help="N > 1: NCCL allreduce + separate update instead of the default fused "
+                         "gradient reduce + update over peer memory (comm.PeerUpdate)")
     ap.add_argument("--merged-fc", action="store_true",
                     help="N > 1: FC layers on rank 0 for the global batch (PAPER.md:936-959)")
     ap.add_argument("--groups", type=int, default=1,
@@ -204,7 +207,8 @@ def arm_config(args, world, net) -> dict:
     return {"workload": f"{args.net} train step, b={b} per GPU, synthetic {s}x{s}x{c}, g=1",
             "net": args.net, "per_gpu_batch": b, "global_batch": b * world, "g": 1,
             "parallelism": f"dp{world}" + ("+merged-fc" if getattr(args, "merged_fc", False) and world > 1
-                                           else ""),
+                                           else "+p2p" if getattr(args, "p2p", False) and world > 1
+                                           else "+nccl" if world > 1 else ""),
             "precision": args.precision, "l2": l2_note(net, b)}
 
 
@@ -250,7 +254,8 @@ def run_ours(args):
     hp = Hyperparams(eta=args.eta, mu=args.mu, lam=args.lam, b=b)
     sess = prob.device_session(SGDState.fresh(np.zeros(1)), hp,
                                process_group=dist.group.WORLD if world > 1 else None,
-                               merged_fc=args.merged_fc and world > 1)
+                               merged_fc=args.merged_fc and world > 1,
+                               p2p=args.p2p and world > 1)
     gw = torch.Generator(device=dev)
     gw.manual_seed(args.seed)                     # identical initial model on every rank
     sess.W = 0.01 * torch.randn(net.dim, generator=gw, device=dev)

@@ -220,6 +220,78 @@ int omni_transpose_f32(const float* src, long long lds, long long src_bstride, i
 /* Fill / scale helpers. */
 int omni_fill_f32(float* X, float value, long long n, void* stream);
 
+/* ------------------------------------------------------------ comm --
+ * Communicators for the multi-GPU path: the gradient
+ * allreduce inside a compute group (replaces the reference's logical
+ * data-parallel mean, simulator.py:3-7 / sgd.py:210-256 with N GPUs) and the
+ * server <-> group-leader transfers of the asynchronous runtime (the
+ * reference's FIFO model server, simulator.py:123-213).  NCCL is loaded at
+ * run time (dlopen "libnccl.so.2"); without it every entry point returns
+ * OMNI_EUNSUPPORTED.  Communicators are opaque pointers (ncclComm_t).
+ * NCCL calls must come from the thread that owns the communicator's device. */
+#define OMNI_COMM_ID_BYTES 128
+#define OMNI_COMM_SPLIT_NOCOLOR (-1)
+int omni_comm_nccl_version(int* version);
+/* One process per GPU: rank 0 makes the id, the host ships it to every rank. */
+int omni_comm_unique_id(void* id /* OMNI_COMM_ID_BYTES */);
+int omni_comm_init_rank(void** comm, int nranks, const void* id, int rank, int device);
+/* One process driving ndev GPUs: comms[i] on devs[i] (devs NULL = 0..ndev-1). */
+int omni_comm_init_all(int ndev, const int* devs, void** comms);
+/* Compute groups: ranks with the same color form one communicator, ordered by
+ * key; OMNI_COMM_SPLIT_NOCOLOR opts out (newcomm = NULL).  Collective.  Inside
+ * a group_start/end bracket *newcomm is written at group end, so the slot
+ * must outlive the bracket.                                                */
+int omni_comm_split(void* comm, int color, int key, void** newcomm);
+int omni_comm_destroy(void* comm);
+int omni_comm_size_rank(void* comm, int* size, int* rank);
+/* In-place sum over the communicator (a group's gradient), on the stream. */
+int omni_allreduce_sum_f32(void* comm, float* buf, size_t n, void* stream);
+/* Point to point (snapshot / gradient exchange with the update server).   */
+int omni_send_f32(void* comm, const float* buf, size_t n, int peer, void* stream);
+int omni_recv_f32(void* comm, float* buf, size_t n, int peer, void* stream);
+/* Bracket several send/recv calls so NCCL fuses them (no deadlock on
+ * simultaneous exchanges).                                                 */
+int omni_comm_group_start(void);
+int omni_comm_group_end(void);
+
+/* ------------------------------------------------------------- p2p --
+ * Peer-memory data-parallel update (one process per GPU, one NVSwitch node):
+ * the gradient allreduce and the momentum update of a layer slice [lo, hi)
+ * fused into one kernel that reads the N ranks' gradients straight out of
+ * their HBM (CUDA IPC mappings), sums them in rank order 0..N-1, applies
+ * V = mu V - eta (G_sum + lam w_read); W += V (sgd.py:92-101; the caller
+ * folds the mean's 1/N into eta and lam) to this rank's part of the slice --
+ * elements [lo + r*c, lo + (r+1)*c) with c = 4*ceil((hi-lo)/(4N)), clipped to
+ * hi; the caller passes that sub-range -- and stores the new W into every
+ * rank's W.  V stays valid on the owning rank only.  grads[p] / weights[p] are
+ * rank p's buffers as mapped in this process (weights[rank] is local), all
+ * with the same 16-byte alignment.  N <= 8.
+ *
+ * Cross-GPU ordering: flag blocks of int64 [2 kinds][N src][max_slots], one
+ * per rank; omni_p2p_step increments this rank's device step counter *step;
+ * omni_p2p_signal stores *step into slot [kind][rank][slot] of every rank's
+ * block (system-scope release, after the stream's previous work);
+ * omni_p2p_wait blocks the stream until this rank's block holds >= *step in
+ * [kind][*][slot_lo, slot_hi) (acquire; traps after 30 s instead of hanging
+ * if a peer died).  All values live on the device, so a CUDA graph of a whole
+ * step replays correctly.                                                   */
+#define OMNI_P2P_GRAD_READY 0 /* src's gradient of the slot is final, W no longer read */
+#define OMNI_P2P_W_DONE 1     /* src wrote its part of the slot's W into every rank */
+#define OMNI_IPC_HANDLE_BYTES 64
+int omni_p2p_step(long long* step, void* stream);
+int omni_p2p_signal(long long* const* flags, int nranks, int rank, int kind, int slot,
+                    int max_slots, const long long* step, void* stream);
+int omni_p2p_wait(const long long* flags, int nranks, int rank, int kind, int slot_lo, int slot_hi,
+                  int max_slots, const long long* step, void* stream);
+int omni_p2p_reduce_sgd_f32(const float* const* grads, float* const* weights, int nranks, int rank,
+                            long long lo, long long hi, float* V, const float* w_read, float eta,
+                            float mu, float lam, void* stream);
+/* IPC: the handle of the allocation holding ptr and ptr's byte offset in it;
+ * open maps a peer's allocation (base pointer; add the offset), close unmaps. */
+int omni_ipc_handle(const void* ptr, void* handle, long long* offset);
+int omni_ipc_open(const void* handle, void** base);
+int omni_ipc_close(void* base);
+
 #ifdef __cplusplus
 }
 #endif

@@ -86,6 +86,25 @@ SIGNATURES: dict[str, tuple] = {
     "omni_conv_weight_s2d_f32": (_I, [_P, _I, _I, _I, _I, _I, _P, _L, _I, _P, _P]),
     "omni_transpose_f32": (_I, [_P, _L, _L, _I, _I, _P, _L, _L, _I, _P]),
     "omni_fill_f32": (_I, [_P, _F, _L, _P]),
+    "omni_comm_nccl_version": (_I, [ctypes.POINTER(_I)]),
+    "omni_comm_unique_id": (_I, [_P]),
+    "omni_comm_init_rank": (_I, [ctypes.POINTER(_P), _I, _P, _I, _I]),
+    "omni_comm_init_all": (_I, [_I, _P, _P]),
+    "omni_comm_split": (_I, [_P, _I, _I, ctypes.POINTER(_P)]),
+    "omni_comm_destroy": (_I, [_P]),
+    "omni_comm_size_rank": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
+    "omni_allreduce_sum_f32": (_I, [_P, _P, ctypes.c_size_t, _P]),
+    "omni_send_f32": (_I, [_P, _P, ctypes.c_size_t, _I, _P]),
+    "omni_recv_f32": (_I, [_P, _P, ctypes.c_size_t, _I, _P]),
+    "omni_comm_group_start": (_I, []),
+    "omni_comm_group_end": (_I, []),
+    "omni_p2p_step": (_I, [_P, _P]),
+    "omni_p2p_signal": (_I, [_P, _I, _I, _I, _I, _I, _P, _P]),
+    "omni_p2p_wait": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _P]),
+    "omni_p2p_reduce_sgd_f32": (_I, [_P, _P, _I, _I, _L, _L, _P, _P, _F, _F, _F, _P]),
+    "omni_ipc_handle": (_I, [_P, _P, ctypes.POINTER(_L)]),
+    "omni_ipc_open": (_I, [_P, ctypes.POINTER(_P)]),
+    "omni_ipc_close": (_I, [_P]),
 }
 
 _lib = None

@@ -442,7 +442,7 @@ class GpuNet:
 
     # ---------------------------------------------------------- backward --
     def backward(self, b: int | None = None, on_grad=None, update=None,
-                 start: int | None = None) -> torch.Tensor:
+                 start: int | None = None, fused_update=None) -> torch.Tensor:
         """Gradient of the mean loss w.r.t. the flat parameters -> self.grad.
 
         ``on_grad(lo, hi)`` (optional) is called as soon as the launches that
@@ -458,7 +458,12 @@ class GpuNet:
         backward instead of ending the step.
 
         ``start``: back-propagate through ops[:start] only, from the gradient
-        already placed in ops[start].inp.grad (merged-FC conv part)."""
+        already placed in ops[start].inp.grad (merged-FC conv part).
+
+        ``fused_update(lo, hi, stream)`` (with ``update``) replaces the layer's
+        allreduce + update: it is called on the update stream once G[lo:hi] is
+        final and W[lo:hi] is no longer read (peer-memory data parallelism,
+        ``comm.PeerUpdate``)."""
         b = self.b if b is None else int(b)
         G = self.grad
         main = torch.cuda.current_stream(self.device)
@@ -486,6 +491,9 @@ class GpuNet:
             for lo, hi, ev, work in pending:
                 us.wait_event(ev)
                 with torch.cuda.stream(us):
+                    if fused_update is not None:
+                        fused_update(lo, hi, us)
+                        continue
                     if work is not None:
                         work.wait()      # this layer's gradient allreduce (update stream waits)
                     K.sgd_momentum(Wu[lo:hi], Vu[lo:hi], G[lo:hi], wr[lo:hi], eta, mu, lam)

@@ -110,7 +110,8 @@ class DeviceSession:
     and the mean over ranks is folded into the fused update."""
 
     def __init__(self, problem: "CNNProblem", state: SGDState, hp: Hyperparams,
-                 process_group=None, use_graph: bool = True, merged_fc: bool = False):
+                 process_group=None, use_graph: bool = True, merged_fc: bool = False,
+                 p2p: bool = False):
         self.problem = problem
         self.hp = hp
         dev = problem.device
@@ -152,6 +153,32 @@ class DeviceSession:
                 f = self.engine.first_fc
                 self.head = GpuNet(head_spec, self.world * hp.b, dev, problem.precision,
                                    input_grad=True, input_cs=self.engine.ops[f].inp.cs)
+
+        # Peer-memory data parallelism: each layer's allreduce + update is one
+        # kernel reading the peers' gradients over NVLink (comm.PeerUpdate).
+        # (Mapped at the first step, and again if W is replaced.)
+        self.p2p = None
+        self.use_p2p = bool(p2p)
+        if p2p and (process_group is None or self.merged_fc):
+            raise ValueError("p2p needs a process group and excludes merged_fc")
+
+    def _peer(self):
+        """The peer-memory update for the current W, or None when the ranks
+        cannot map each other's memory (then every rank uses NCCL allreduce)."""
+        if self.p2p is None or self.p2p.W.data_ptr() != self.W.data_ptr():
+            from .comm import PeerUpdate
+
+            if self.p2p is not None:
+                self.p2p.close()
+            nslots = sum(1 for op in self.engine.ops if op.kind in ("conv", "fc"))
+            try:
+                self.p2p = PeerUpdate(self.engine.grad, self.W, nslots, self.pg)
+            except RuntimeError as e:
+                import warnings
+
+                warnings.warn(f"peer-memory update unavailable ({e}); using NCCL allreduce")
+                self.p2p, self.use_p2p = None, False
+        return self.p2p
 
     def _allreduce_hook(self, works):
         import torch.distributed as dist
@@ -240,6 +267,14 @@ class DeviceSession:
         hp = self.hp
         if self.merged_fc:
             self._compute_merged(wr, b)
+        elif self.use_p2p and self._peer() is not None:
+            n, peer, V = self.world, self.p2p, self.V
+            peer.begin_step()
+            self.engine.forward(wr, b)
+            self.engine.backward(b, update=(self.W, V, wr, hp.eta / n, hp.mu, hp.lam * n),
+                                 fused_update=lambda lo, hi, s: peer.layer(
+                                     lo, hi, V, wr, hp.eta / n, hp.mu, hp.lam * n, s))
+            peer.finish()        # every rank's W writes of this step have landed here
         elif self.world > 1:
             # each layer's gradient is allreduced as soon as it exists and that
             # layer's update follows its allreduce (inside the backward)
@@ -265,7 +300,7 @@ class DeviceSession:
             eng.input.value, eng.labels = own            # launches already hold the pointers
 
     def _graph_key(self, batch, w_read):
-        if not (self.use_graph and self.world == 1 and w_read is None and
+        if not (self.use_graph and (self.world == 1 or self.use_p2p) and w_read is None and
                 self.engine.timer is None and self.engine.overlap):
             return None
         base = (self.W.data_ptr(), self.V.data_ptr())
@@ -360,7 +395,14 @@ class DeviceSession:
         dist.broadcast(self.W[self.fc_off:].contiguous(), src=root, group=self.pg)
         dist.broadcast(self.V[self.fc_off:].contiguous(), src=root, group=self.pg)
 
+    def sync_momentum(self) -> None:
+        """Peer-memory mode: each rank holds V only for the parts it updates;
+        make V complete on every rank (a collective)."""
+        if self.p2p is not None:
+            self.p2p.gather_momentum(self.V)
+
     def state(self) -> SGDState:
+        self.sync_momentum()
         return SGDState(W=self.W.double().cpu().numpy(), V=self.V.double().cpu().numpy(), t=self.t)
 
 
@@ -499,8 +541,9 @@ class CNNProblem(TrainingProblem):
         return acc
 
     def device_session(self, state: SGDState, hp: Hyperparams, process_group=None,
-                       use_graph: bool = True, merged_fc: bool = False) -> DeviceSession:
-        return DeviceSession(self, state, hp, process_group, use_graph, merged_fc)
+                       use_graph: bool = True, merged_fc: bool = False,
+                       p2p: bool = False) -> DeviceSession:
+        return DeviceSession(self, state, hp, process_group, use_graph, merged_fc, p2p)
 
 
 def make_cnn(net: str, n_examples: int = 128, seed: int = 0, **kw) -> CNNProblem:

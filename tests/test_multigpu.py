@@ -36,7 +36,7 @@ def torchrun(n, script, *args):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("mode", ["", "merged"])
+@pytest.mark.parametrize("mode", ["", "merged", "p2p"])
 def test_data_parallel_session_equals_replay(mode):
     out = torchrun(2, "dp_check.py", "cifar10_quick", *([mode] if mode else []))
     assert "normwise" in out
@@ -45,4 +45,10 @@ def test_data_parallel_session_equals_replay(mode):
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 def test_group_runtime_equals_oracle_schedule():
     out = torchrun(2, "groups_check.py")
+    assert '"pass": true' in out
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_c_abi_communicators_one_process_per_gpu():
+    out = torchrun(2, "comm_check.py")
     assert '"pass": true' in out

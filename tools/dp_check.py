@@ -28,19 +28,26 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     net = sys.argv[1] if len(sys.argv) > 1 else "cifar10_quick"
     merged = len(sys.argv) > 2 and sys.argv[2] == "merged"
+    p2p = len(sys.argv) > 2 and sys.argv[2] == "p2p"
     b, steps = 32, 4
     prob = CNNProblem(net, n_examples=256, seed=3, precision="3xtf32", device=dev)
     hp = Hyperparams(eta=0.01, mu=0.9, lam=5e-4, b=b)
     state = prob.initial_state()
     rng = np.random.default_rng(11)
     idx = [[rng.integers(0, 256, size=b) for _ in range(world)] for _ in range(steps)]
-    sess = prob.device_session(state, hp, process_group=dist.group.WORLD, merged_fc=merged)
+    sess = prob.device_session(state, hp, process_group=dist.group.WORLD, merged_fc=merged,
+                                p2p=p2p)
     for t in range(steps):
         sess.step(DeviceBatch(torch.from_numpy(idx[t][rank]).to(dev)))
     loss = sess.last_loss()            # (merged FC: a collective)
     sess.sync_fc()
     torch.cuda.synchronize()
     W_dp = sess.W.double().cpu().numpy()
+    st = sess.state()                  # (p2p: gathers V, a collective)
+    Ws = [None] * world
+    dist.all_gather_object(Ws, float(np.abs(W_dp).sum()))
+    if p2p:                            # one owner computes each element: bit-identical W
+        assert len(set(Ws)) == 1, Ws
     if rank == 0:
         W = np.asarray(state.W, dtype=np.float64).copy()
         V = np.zeros_like(W)
@@ -55,9 +62,19 @@ def main():
             V = hp.mu * V - hp.eta * (G + hp.lam * W)
             W = W + V
         rel = float(np.linalg.norm(W_dp - W) / np.linalg.norm(W))
-        print(f"{net}: N={world} data-parallel{' merged-FC' if merged else ''} session vs replay: "
-              f"normwise {rel:.3e} (last loss {loss:.4f})")
-        assert rel < 1e-5, rel
+        relv = float(np.linalg.norm(st.V - V) / np.linalg.norm(V))
+        print(f"{net}: N={world} data-parallel{' merged-FC' if merged else ' p2p' if p2p else ''} session vs replay: "
+              f"normwise {rel:.3e}, V {relv:.3e} (last loss {loss:.4f})")
+        worst = []
+        for op in eng.ops:
+            if op.kind in ("conv", "fc"):
+                hi = op.boff + op.layer.d_out if op.boff >= 0 else op.woff + op.wsz
+                for nm, lo, h in (("w", op.woff, op.woff + op.wsz), ("b", op.boff, hi)):
+                    if h > lo >= 0:
+                        e = float(np.linalg.norm(st.V[lo:h] - V[lo:h]) / max(np.linalg.norm(V[lo:h]), 1e-30))
+                        worst.append((e, f"{op.kind}@{op.woff}.{nm}[{h - lo}]"))
+        print("worst V slices:", sorted(worst, reverse=True)[:4])
+        assert rel < 1e-5 and relv < 1e-2, (rel, relv)
     dist.destroy_process_group()
 
 
