@@ -265,7 +265,9 @@ int omni_comm_group_end(void);
  * hi; the caller passes that sub-range -- and stores the new W into every
  * rank's W.  V stays valid on the owning rank only.  grads[p] / weights[p] are
  * rank p's buffers as mapped in this process (weights[rank] is local), all
- * with the same 16-byte alignment.  N <= 8.
+ * with the same 16-byte alignment; weights[p] = NULL (p != rank) skips that
+ * store (the copy-engine variant: gradients pushed into local lanes with
+ * omni_copy_async, W sent the same way).  N <= 8.
  *
  * Cross-GPU ordering: flag blocks of int64 [2 kinds][N src][max_slots], one
  * per rank; omni_p2p_step increments this rank's device step counter *step;
@@ -286,6 +288,9 @@ int omni_p2p_wait(const long long* flags, int nranks, int rank, int kind, int sl
 int omni_p2p_reduce_sgd_f32(const float* const* grads, float* const* weights, int nranks, int rank,
                             long long lo, long long hi, float* V, const float* w_read, float eta,
                             float mu, float lam, void* stream);
+/* Asynchronous copy on the stream by the copy engines (peer-mapped pointers
+ * allowed: an NVLink DMA that occupies no SM).                              */
+int omni_copy_async(void* dst, const void* src, long long bytes, void* stream);
 /* IPC: the handle of the allocation holding ptr and ptr's byte offset in it;
  * open maps a peer's allocation (base pointer; add the offset), close unmaps. */
 int omni_ipc_handle(const void* ptr, void* handle, long long* offset);

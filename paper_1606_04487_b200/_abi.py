@@ -102,6 +102,7 @@ SIGNATURES: dict[str, tuple] = {
     "omni_p2p_signal": (_I, [_P, _I, _I, _I, _I, _I, _P, _P]),
     "omni_p2p_wait": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _P]),
     "omni_p2p_reduce_sgd_f32": (_I, [_P, _P, _I, _I, _L, _L, _P, _P, _F, _F, _F, _P]),
+    "omni_copy_async": (_I, [_P, _P, _L, _P]),
     "omni_ipc_handle": (_I, [_P, _P, ctypes.POINTER(_L)]),
     "omni_ipc_open": (_I, [_P, ctypes.POINTER(_P)]),
     "omni_ipc_close": (_I, [_P]),

@@ -24,6 +24,7 @@
 // of hanging the GPU.
 
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -85,35 +86,59 @@ __global__ void p2p_wait_kernel(const long long* __restrict__ flags, int n, int 
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
+inline long long ceil_div_ll(long long a, long long b) { return (a + b - 1) / b; }
+
 struct PeerPtrs {
   const float* g[kMaxRanks];
   float* w[kMaxRanks];
 };
 
-// One element (scalar) or four (float4) of this rank's part.
-template <int N>
-__device__ __forceinline__ void update4(const PeerPtrs& pp, int n, int rank, long long i, float* V,
+// U float4s of this rank's part (i, i + step, ...): every load is issued
+// before any arithmetic, so U * N remote 16-byte loads are in flight per thread.
+template <int N, int U>
+__device__ __forceinline__ void update4(const PeerPtrs& pp, int n, int rank, long long i,
+                                        long long step, long long end, float* V, float* Wl,
                                         const float* wr, float eta, float mu, float lam) {
-  float4 s = *reinterpret_cast<const float4*>(pp.g[0] + i);
+  constexpr int NN = N ? N : kMaxRanks;
+  float4 g[U][NN];
+  float4 v[U], r[U], w[U];
+  bool ok[U];
 #pragma unroll
-  for (int p = 1; p < (N ? N : kMaxRanks); ++p) {
-    if (!N && p >= n) break;
-    const float4 t = *reinterpret_cast<const float4*>(pp.g[p] + i);
-    s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
+  for (int u = 0; u < U; ++u) {
+    const long long j = i + u * step;
+    ok[u] = j < end;
+    if (!ok[u]) continue;
+#pragma unroll
+    for (int p = 0; p < NN; ++p) {
+      if (!N && p >= n) break;
+      g[u][p] = *reinterpret_cast<const float4*>(pp.g[p] + j);
+    }
+    v[u] = *reinterpret_cast<const float4*>(V + j);
+    r[u] = *reinterpret_cast<const float4*>(wr + j);
+    w[u] = *reinterpret_cast<const float4*>(Wl + j);
   }
-  float4 v = *reinterpret_cast<const float4*>(V + i);
-  const float4 r = *reinterpret_cast<const float4*>(wr + i);
-  float4 w = *reinterpret_cast<const float4*>(pp.w[rank] + i);
-  v.x = mu * v.x - eta * (s.x + lam * r.x);
-  v.y = mu * v.y - eta * (s.y + lam * r.y);
-  v.z = mu * v.z - eta * (s.z + lam * r.z);
-  v.w = mu * v.w - eta * (s.w + lam * r.w);
-  w.x += v.x; w.y += v.y; w.z += v.z; w.w += v.w;
-  *reinterpret_cast<float4*>(V + i) = v;
 #pragma unroll
-  for (int p = 0; p < (N ? N : kMaxRanks); ++p) {
-    if (!N && p >= n) break;
-    *reinterpret_cast<float4*>(pp.w[p] + i) = w;
+  for (int u = 0; u < U; ++u) {
+    if (!ok[u]) continue;
+    const long long j = i + u * step;
+    float4 s = g[u][0];
+#pragma unroll
+    for (int p = 1; p < NN; ++p) {
+      if (!N && p >= n) break;
+      s.x += g[u][p].x; s.y += g[u][p].y; s.z += g[u][p].z; s.w += g[u][p].w;
+    }
+    float4 vv = v[u], ww = w[u];
+    vv.x = mu * vv.x - eta * (s.x + lam * r[u].x);
+    vv.y = mu * vv.y - eta * (s.y + lam * r[u].y);
+    vv.z = mu * vv.z - eta * (s.z + lam * r[u].z);
+    vv.w = mu * vv.w - eta * (s.w + lam * r[u].w);
+    ww.x += vv.x; ww.y += vv.y; ww.z += vv.z; ww.w += vv.w;
+    *reinterpret_cast<float4*>(V + j) = vv;
+#pragma unroll
+    for (int p = 0; p < NN; ++p) {
+      if (!N && p >= n) break;
+      if (pp.w[p] != nullptr) *reinterpret_cast<float4*>(pp.w[p] + j) = ww;
+    }
   }
 }
 
@@ -124,14 +149,15 @@ __device__ __forceinline__ void update1(const PeerPtrs& pp, int n, int rank, lon
   const float v = mu * V[i] - eta * (s + lam * wr[i]);
   const float w = pp.w[rank][i] + v;
   V[i] = v;
-  for (int p = 0; p < n; ++p) pp.w[p][i] = w;
+  for (int p = 0; p < n; ++p)
+    if (pp.w[p] != nullptr) pp.w[p][i] = w;
 }
 
-template <int N>
+template <int N, int U>
 __global__ void __launch_bounds__(256) p2p_reduce_sgd_kernel(PeerPtrs pp, int n, int rank,
                                                              long long lo, long long hi, float* V,
-                                                             const float* wr, float eta, float mu,
-                                                             float lam) {
+                                                             float* Wl, const float* wr, float eta,
+                                                             float mu, float lam) {
   // scalar head up to a 16-byte boundary (all buffers share element offsets)
   const long long a0 = min(hi, (lo + 3) & ~3ll);
   const long long a1 = a0 + ((hi - a0) & ~3ll);
@@ -139,8 +165,20 @@ __global__ void __launch_bounds__(256) p2p_reduce_sgd_kernel(PeerPtrs pp, int n,
   const long long stride = (long long)gridDim.x * blockDim.x;
   if (tid < a0 - lo) update1(pp, n, rank, lo + tid, V, wr, eta, mu, lam);
   if (tid < hi - a1) update1(pp, n, rank, a1 + tid, V, wr, eta, mu, lam);
-  for (long long i = a0 + 4 * tid; i < a1; i += 4 * stride)
-    update4<N>(pp, n, rank, i, V, wr, eta, mu, lam);
+  for (long long i = a0 + 4 * tid; i < a1; i += 4 * stride * U)
+    update4<N, U>(pp, n, rank, i, 4 * stride, a1, V, Wl, wr, eta, mu, lam);
+}
+
+template <int U>
+void launch_reduce_sgd(int grid, cudaStream_t s, const PeerPtrs& pp, int n, int rank, long long lo,
+                       long long hi, float* V, float* Wl, const float* wr, float eta, float mu,
+                       float lam) {
+  switch (n) {
+    case 2: p2p_reduce_sgd_kernel<2, U><<<grid, 256, 0, s>>>(pp, n, rank, lo, hi, V, Wl, wr, eta, mu, lam); break;
+    case 4: p2p_reduce_sgd_kernel<4, U><<<grid, 256, 0, s>>>(pp, n, rank, lo, hi, V, Wl, wr, eta, mu, lam); break;
+    case 8: p2p_reduce_sgd_kernel<8, U><<<grid, 256, 0, s>>>(pp, n, rank, lo, hi, V, Wl, wr, eta, mu, lam); break;
+    default: p2p_reduce_sgd_kernel<0, U><<<grid, 256, 0, s>>>(pp, n, rank, lo, hi, V, Wl, wr, eta, mu, lam);
+  }
 }
 
 }  // namespace
@@ -197,10 +235,11 @@ int omni_p2p_reduce_sgd_f32(const float* const* grads, float* const* weights, in
   OMNI_REQUIRE(0 <= lo && lo <= hi, "omni_p2p_reduce_sgd_f32: bad range [%lld, %lld)", lo, hi);
   PeerPtrs pp{};
   for (int p = 0; p < nranks; ++p) {
-    OMNI_REQUIRE(grads[p] != nullptr && weights[p] != nullptr,
-                 "omni_p2p_reduce_sgd_f32: NULL peer pointer %d", p);
+    OMNI_REQUIRE(grads[p] != nullptr && (weights[p] != nullptr || p != rank),
+                 "omni_p2p_reduce_sgd_f32: NULL pointer for rank %d", p);
     OMNI_REQUIRE(((uintptr_t)grads[p] & 15) == ((uintptr_t)grads[0] & 15) &&
-                     ((uintptr_t)weights[p] & 15) == ((uintptr_t)grads[0] & 15) &&
+                     (weights[p] == nullptr ||
+                      ((uintptr_t)weights[p] & 15) == ((uintptr_t)grads[0] & 15)) &&
                      ((uintptr_t)V & 15) == ((uintptr_t)grads[0] & 15) &&
                      ((uintptr_t)w_read & 15) == ((uintptr_t)grads[0] & 15),
                  "omni_p2p_reduce_sgd_f32: buffers must share their 16-byte alignment");
@@ -211,22 +250,27 @@ int omni_p2p_reduce_sgd_f32(const float* const* grads, float* const* weights, in
                "omni_p2p_reduce_sgd_f32: buffers must be 16-byte aligned");
   if (hi == lo) return OMNI_OK;
   const long long n4 = (hi - lo + 3) / 4;
-  const int grid = omni::grid_for(n4, 256);
+  static const int unroll = [] {
+    const char* e = getenv("OMNI_P2P_UNROLL");   // probe knob: 1, 2 or 4 float4s per thread
+    const int u = e ? atoi(e) : 2;
+    return (u == 1 || u == 4) ? u : 2;
+  }();
+  const int grid = omni::grid_for(ceil_div_ll(n4, unroll), 256);
   cudaStream_t s = omni::as_stream(stream);
-  switch (nranks) {
-    case 2:
-      p2p_reduce_sgd_kernel<2><<<grid, 256, 0, s>>>(pp, nranks, rank, lo, hi, V, w_read, eta, mu, lam);
-      break;
-    case 4:
-      p2p_reduce_sgd_kernel<4><<<grid, 256, 0, s>>>(pp, nranks, rank, lo, hi, V, w_read, eta, mu, lam);
-      break;
-    case 8:
-      p2p_reduce_sgd_kernel<8><<<grid, 256, 0, s>>>(pp, nranks, rank, lo, hi, V, w_read, eta, mu, lam);
-      break;
-    default:
-      p2p_reduce_sgd_kernel<0><<<grid, 256, 0, s>>>(pp, nranks, rank, lo, hi, V, w_read, eta, mu, lam);
-  }
+  float* Wl = weights[rank];
+  if (unroll == 1) launch_reduce_sgd<1>(grid, s, pp, nranks, rank, lo, hi, V, Wl, w_read, eta, mu, lam);
+  else if (unroll == 4) launch_reduce_sgd<4>(grid, s, pp, nranks, rank, lo, hi, V, Wl, w_read, eta, mu, lam);
+  else launch_reduce_sgd<2>(grid, s, pp, nranks, rank, lo, hi, V, Wl, w_read, eta, mu, lam);
   return omni::check_launch("p2p_reduce_sgd_kernel");
+}
+
+int omni_copy_async(void* dst, const void* src, long long bytes, void* stream) {
+  OMNI_REQUIRE(bytes >= 0 && (bytes == 0 || (dst != nullptr && src != nullptr)),
+               "omni_copy_async: bad arguments");
+  if (bytes == 0) return OMNI_OK;
+  OMNI_CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault,
+                                omni::as_stream(stream)));
+  return OMNI_OK;
 }
 
 int omni_ipc_handle(const void* ptr, void* handle, long long* offset) {

@@ -172,7 +172,8 @@ class DeviceSession:
                 self.p2p.close()
             nslots = sum(1 for op in self.engine.ops if op.kind in ("conv", "fc"))
             try:
-                self.p2p = PeerUpdate(self.engine.grad, self.W, nslots, self.pg)
+                self.p2p = PeerUpdate(self.engine.grad, self.W, nslots, self.pg,
+                                      mode=os.environ.get("OMNI_P2P_MODE", "dma"))
             except RuntimeError as e:
                 import warnings
 
