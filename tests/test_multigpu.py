@@ -26,11 +26,12 @@ def free_port() -> int:
         return s.getsockname()[1]
 
 
-def torchrun(n, script, *args):
+def torchrun(n, script, *args, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", f"--master-port={free_port()}",
            os.path.join(ROOT, "tools", script), *args]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env=None if env is None else {**os.environ, **env})
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     return r.stdout
 
@@ -52,3 +53,18 @@ def test_group_runtime_equals_oracle_schedule():
 def test_c_abi_communicators_one_process_per_gpu():
     out = torchrun(2, "comm_check.py")
     assert '"pass": true' in out
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("transport", ["dma", "pull"])
+def test_peer_memory_update_both_transports(transport):
+    """dp_check asserts W bit-identical on every rank and equal to the float64
+    replay (<= 1e-5 normwise)."""
+    out = torchrun(2, "dp_check.py", "lenet", "p2p", env={"OMNI_P2P_MODE": transport})
+    assert "p2p session vs replay" in out
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_peer_update_probe_exact():
+    out = torchrun(2, "p2p_probe.py")
+    assert '"W_identical_on_all_ranks": true' in out
