@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--mu", type=float, default=0.9)
     ap.add_argument("--lam", type=float, default=5e-4)
     ap.add_argument("--profile-out", default="", help="write per-GEMM timing breakdown (json)")
+    ap.add_argument("--groups-nccl", dest="groups_p2p", action="store_false",
+                    help="--groups: NCCL all-to-all rounds instead of the default per-layer exchanges "
+                         "over NVLink peer memory (copy-engine DMA)")
     ap.add_argument("--groups-overlap", action="store_true",
                     help="--groups: layer-aligned shards, gradient exchange overlapped with the backward")
     ap.add_argument("--nccl-allreduce", dest="p2p", action="store_false",
@@ -450,7 +453,7 @@ def run_groups(args, net, dev, world, rank, local):
     gw.manual_seed(args.seed)
     W0 = 0.01 * torch.randn(net.dim, generator=gw, device=dev)
     rt = GroupRuntime(plan, CudaBackend(prob, args.batch), hp, W0, args.n_examples, args.seed,
-                      overlap=args.groups_overlap)
+                      overlap=args.groups_overlap, p2p=args.groups_p2p)
     rt.run(args.warmup)
     torch.cuda.synchronize()
     dist.barrier()
@@ -479,7 +482,8 @@ def run_groups(args, net, dev, world, rank, local):
                                    f"b={args.batch} per GPU (group batch {hp.b}), deterministic "
                                    f"round-robin async schedule", "net": args.net,
                        "per_gpu_batch": args.batch, "global_batch": args.batch * world, "g": plan.g,
-                       "k": plan.k, "mu": mu, "parallelism": f"{plan.g} groups x dp{plan.k}",
+                       "k": plan.k, "mu": mu, "parallelism": f"{plan.g} groups x dp{plan.k}"
+                       + ("+p2p" if args.groups_p2p else "+nccl"),
                        "step": "one round = g master updates"},
             "staleness_mean": float(np.mean(st_)) if st_ else 0.0,
             "gpu_launches": None, "clocks": clk, "e2e": None, "cpu_baseline": None,

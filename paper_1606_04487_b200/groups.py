@@ -81,6 +81,16 @@ class CudaBackend:
                 out.append((op.woff, hi))
         return out
 
+    def grad_fused(self, W, idx, fused_update) -> None:
+        """Gradient into self.engine.grad with fused_update(lo, hi, stream)
+        called on the engine's update stream as each layer's gradient is final
+        and its data gradient no longer reads W (peer-memory rounds)."""
+        from .problems import Batch
+
+        b = self.problem.load_batch(self.engine, Batch(self.problem, idx))
+        self.engine.forward(W, b)
+        self.engine.backward(b, update=(W, W, W, 0.0, 0.0, 0.0), fused_update=fused_update)
+
     def grad_hooked(self, W, idx, on_grad) -> None:
         """Gradient with on_grad(lo, hi) called as each layer's gradient is
         enqueued (for overlapped per-layer exchanges); the gradient stays in
@@ -102,7 +112,8 @@ class GroupEvent:
 
 class GroupRuntime:
     def __init__(self, plan: ExecutionPlan, backend: Backend, hp: Hyperparams, W0: torch.Tensor,
-                 n_examples: int, seed: int, sharded: bool = True, overlap: bool = False):
+                 n_examples: int, seed: int, sharded: bool = True, overlap: bool = False,
+                 p2p: bool = False):
         if not dist.is_initialized():
             raise RuntimeError("GroupRuntime needs torch.distributed initialised (one rank per GPU)")
         world, rank = dist.get_world_size(), dist.get_rank()
@@ -125,7 +136,10 @@ class GroupRuntime:
         self.rng = batch_stream(seed, self.group)
         self.events: list[GroupEvent] = []
         self.dim = W0.numel()
-        if self.sharded:
+        self._p2p = bool(p2p) and hasattr(backend, "grad_fused")
+        if self._p2p:
+            self._init_p2p(W0)
+        elif self.sharded:
             # rank r owns elements [r*S, (r+1)*S) of W, V and of every group's snapshot
             N = world
             S = -(-self.dim // N)
@@ -149,6 +163,91 @@ class GroupRuntime:
         # gradients arrive as the SUM of k slice means; fold the 1/k into the fused
         # update: eta (G/k + lam w) = (eta/k) (G + k lam w)
         self._hp_sum = hp.replace(eta=hp.eta / plan.k, lam=hp.lam * plan.k)
+
+    def _init_p2p(self, W0: torch.Tensor) -> None:
+        """Peer-memory rounds (comm.PeerUpdate, copy-engine DMA): rank r owns
+        part r of every layer slice (comm.owned_part) of W, V and of the g
+        snapshots, kept in full-length buffers; each member's own-group
+        snapshot buffer is mapped into every owner, which writes its parts."""
+        from .comm import PeerUpdate
+
+        self.sharded = True
+        self._layers = self.backend.layer_ranges()
+        self._Wf = W0.clone()
+        self._Vf = torch.zeros_like(W0)
+        self._snapf = [W0.clone() for _ in range(self.plan.g)]
+        self._snap_own = W0.clone()
+        self._peer = PeerUpdate(self.backend.engine.grad, self._snap_own, len(self._layers),
+                                dist.group.WORLD, mode="dma")
+
+    def _round_p2p(self) -> None:
+        """One round with every exchange over NVLink peer memory, per layer as
+        the backward produces it: gradient parts DMA'd to their owners, the g
+        ordered updates of each owner's part (sum of the group's k lanes in
+        member order, w_read = that group's snapshot), and the new snapshot
+        parts DMA'd into the group members' snapshot buffers."""
+        import ctypes
+
+        from . import _abi
+        from .comm import owned_part
+
+        plan, N, peer = self.plan, self.plan.N, self._peer
+        idx = self.rng.integers(0, self.n_examples, size=self.hp.b)
+        hp = self._hp_sum
+        esz = self._Wf.element_size()
+        lanes = [[peer.g_lanes[m] for m in plan.group_ranks(i)] for i in range(plan.g)]
+        lanes = [(ctypes.c_void_p * len(l))(*l) for l in lanes]
+        wloc = (ctypes.c_void_p * plan.k)(self._Wf.data_ptr(), *([None] * (plan.k - 1)))
+        V, Wf = self._Vf, self._Wf
+
+        def fused(lo, hi, stream):
+            s = ctypes.c_void_p(stream.cuda_stream)
+            slot = peer.slot
+            peer.slot += 1
+            for p in range(N):                                  # my gradient parts -> owners
+                if p != self.rank:
+                    a, b = owned_part(lo, hi, N, p)
+                    _abi.call("omni_copy_async",
+                              ctypes.c_void_p(peer.r_ptrs[p] + self.rank * peer._lane + a * esz),
+                              ctypes.c_void_p(peer.G.data_ptr() + a * esz), (b - a) * esz, s)
+            _abi.call("omni_p2p_signal", peer.f_ptrs, N, self.rank, peer.GRAD_READY, slot,
+                      peer.max_slots, peer._sp, s)
+            _abi.call("omni_p2p_wait", ctypes.c_void_p(peer.flags.data_ptr()), N, self.rank,
+                      peer.GRAD_READY, slot, slot + 1, peer.max_slots, peer._sp, s)
+            a, b = owned_part(lo, hi, N, self.rank)
+            if b > a:
+                for i in range(plan.g):                         # the g ordered updates
+                    snap = self._snapf[i]
+                    _abi.call("omni_p2p_reduce_sgd_f32", lanes[i], wloc, plan.k, 0, a, b,
+                              ctypes.c_void_p(V.data_ptr()), ctypes.c_void_p(snap.data_ptr()),
+                              float(hp.eta), float(hp.mu), float(hp.lam), s)
+                    _abi.call("omni_copy_async", ctypes.c_void_p(snap.data_ptr() + a * esz),
+                              ctypes.c_void_p(Wf.data_ptr() + a * esz), (b - a) * esz, s)
+                    for m in plan.group_ranks(i):               # group i reads W(t) next round
+                        _abi.call("omni_copy_async", ctypes.c_void_p(peer.w_ptrs[m] + a * esz),
+                                  ctypes.c_void_p(Wf.data_ptr() + a * esz), (b - a) * esz, s)
+            _abi.call("omni_p2p_signal", peer.f_ptrs, N, self.rank, peer.W_DONE, slot,
+                      peer.max_slots, peer._sp, s)
+
+        peer.begin_step()
+        self.backend.grad_fused(self._snap_own, self._my_slice(idx), fused)
+        peer.finish()
+        for i in range(plan.g):
+            self.t += 1
+            self.events.append(GroupEvent(i, self.snap_step[i], self.t, self.t - 1 - self.snap_step[i]))
+            self.snap_step[i] = self.t
+
+    def _assemble(self, full: torch.Tensor) -> torch.Tensor:
+        """Peer-memory mode: the owners' parts of a full-length buffer, summed
+        over ranks (every other element zeroed first: exact)."""
+        from .comm import owned_part
+
+        out = torch.zeros_like(full)
+        for lo, hi in self._layers:
+            a, b = owned_part(lo, hi, self.plan.N, self.rank)
+            out[a:b] = full[a:b]
+        dist.all_reduce(out)
+        return out
 
     def _init_layered(self, W0: torch.Tensor) -> None:
         """Layer-aligned shards: every layer's range [lo, hi) is split into N
@@ -192,10 +291,14 @@ class GroupRuntime:
     def W(self) -> torch.Tensor:
         """The master model (sharded runtime: assembled from every rank's shard,
         a collective -- every rank calls it)."""
+        if self._p2p:
+            return self._assemble(self._Wf)
         return self._full(self._W) if self.sharded else self._W
 
     @property
     def V(self) -> torch.Tensor:
+        if self._p2p:
+            return self._assemble(self._Vf)
         return self._full(self._V) if self.sharded else self._V
 
     def _my_slice(self, idx: np.ndarray) -> np.ndarray:
@@ -208,6 +311,8 @@ class GroupRuntime:
 
     def round(self) -> None:
         """One round = g master updates, one per group, in group order."""
+        if self._p2p:
+            return self._round_p2p()
         if self.sharded:
             return self._round_layered() if self._layered else self._round_sharded()
         plan = self.plan
