@@ -44,8 +44,9 @@ def test_data_parallel_session_equals_replay(mode):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-def test_group_runtime_equals_oracle_schedule():
-    out = torchrun(2, "groups_check.py")
+@pytest.mark.parametrize("mode", ["", "--p2p", "--overlap"])
+def test_group_runtime_equals_oracle_schedule(mode):
+    out = torchrun(2, "groups_check.py", *([mode] if mode else []))
     assert '"pass": true' in out
 
 
