@@ -778,11 +778,30 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
   }
 }
 
-// The ones tile behind OMNI_CONV_WGRAD_BIAS's bias-gradient row (head of the
-// caller's workspace; rewritten per call since split-K partials share it).
+// The ones tile behind OMNI_CONV_WGRAD_BIAS's bias-gradient row: a constant
+// device array (TMA source), so no per-call fill launch.  kOnesBytes of the
+// caller's workspace stay reserved for it (unchanged workspace contract).
 constexpr int kOnesBytes = 64 * 32 * 4;  // BKT (<= 64) K-rows x 32 fp32
-__global__ void fill_ones_kernel(float* __restrict__ p, int n) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = 1.f;
+#define OMNI_ONES4 1.f, 1.f, 1.f, 1.f
+#define OMNI_ONES16 OMNI_ONES4, OMNI_ONES4, OMNI_ONES4, OMNI_ONES4
+#define OMNI_ONES64 OMNI_ONES16, OMNI_ONES16, OMNI_ONES16, OMNI_ONES16
+#define OMNI_ONES256 OMNI_ONES64, OMNI_ONES64, OMNI_ONES64, OMNI_ONES64
+__device__ __align__(128) float g_ones_tile[kOnesBytes / 4] = {
+    OMNI_ONES256, OMNI_ONES256, OMNI_ONES256, OMNI_ONES256,
+    OMNI_ONES256, OMNI_ONES256, OMNI_ONES256, OMNI_ONES256};
+static_assert(kOnesBytes / 4 == 8 * 256, "ones tile initialiser size");
+
+// Device address of g_ones_tile on the current device (cached per device).
+const float* ones_tile() {
+  static const float* addr[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!addr[dev]) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_ones_tile) != cudaSuccess) return nullptr;
+    addr[dev] = static_cast<const float*>(p);
+  }
+  return addr[dev];
 }
 
 // Generic (scalar) split-K reduction.
@@ -1473,15 +1492,13 @@ int omni_conv_implicit_f32(int precision, int op, const float* X, int b, int n, 
   // the B-side form needs) and dY (pixels x ldg) as the MN-major B operand;
   // the epilogue stores C^T, i.e. Y[o*ldy + (tap, ch)].
   OMNI_REQUIRE(epilogue == OMNI_EPI_STORE, "conv wgrad supports the plain store epilogue only");
-  float* ones = nullptr;
+  const float* ones = nullptr;
   if (with_bias) {
     // one more GEMM row (tap*c index k*k*c) fed by a ones chunk: the bias gradient
     OMNI_REQUIRE(workspace && ws_bytes >= gemm::kOnesBytes && ((uintptr_t)workspace & 15) == 0,
                  "conv wgrad+bias: workspace of at least %d bytes required", gemm::kOnesBytes);
-    ones = workspace;
-    gemm::fill_ones_kernel<<<4, 512, 0, st>>>(ones, gemm::kOnesBytes / 4);
-    rc = omni::check_launch("fill_ones");
-    if (rc) return rc;
+    ones = gemm::ones_tile();
+    OMNI_REQUIRE(ones, "conv wgrad+bias: ones tile address unavailable");
     workspace += gemm::kOnesBytes / 4;
     ws_bytes -= gemm::kOnesBytes;
   }
