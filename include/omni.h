@@ -121,7 +121,8 @@ int omni_gemm_f32(int precision, int M, int N, int K, const float* A, long long 
 /*   OMNI_CONV_WGRAD_BIAS: as OMNI_CONV_WGRAD, plus the bias gradient
  *                    Y[o*ldy + k*k*c] = sum_pix G[pix*ldg + o] as one more GEMM row
  *                    (a ones operand chunk; needs ldy > k*k*c).  The workspace
- *                    (size from omni_conv_implicit_plan) holds that ones tile.  */
+ *                    (size from omni_conv_implicit_plan) reserves room for that
+ *                    ones tile; the library reads its own constant copy.  */
 #define OMNI_CONV_FPROP 0
 #define OMNI_CONV_WGRAD 1
 #define OMNI_CONV_WGRAD_BIAS 2
