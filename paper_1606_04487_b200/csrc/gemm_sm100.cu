@@ -825,10 +825,6 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
 
 // Split-K reductions: C[i,j] = epi(sum_s ws[s][i][j]) in ascending s (the same
 // order in every variant, so results do not depend on which one runs).
-// The vector and transposed variants issue up to kReduceBatch split loads
-// before adding: one load in flight per thread left them latency bound
-// (~1.9 TB/s in the CaffeNet step's ncu launch list).
-constexpr int kReduceBatch = 8;
 // Natural store, 4 columns per thread (N, ldc % 4 == 0, C 16-byte aligned).
 template <int MODE>
 __global__ void __launch_bounds__(256) splitk_reduce_v4_kernel(const float* __restrict__ ws, int S,
@@ -841,21 +837,12 @@ __global__ void __launch_bounds__(256) splitk_reduce_v4_kernel(const float* __re
     const int col = (i - row * n4) << 2;
     const float* src = ws + (long long)row * N + col;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);  // 0 + sum, as the generic kernel
-    // kReduceBatch independent loads in flight per thread, then added in
-    // ascending split order (the sum is the same as the one-at-a-time loop)
-    for (int s0 = 0; s0 < S; s0 += kReduceBatch) {
-      float4 v[kReduceBatch];
-#pragma unroll
-      for (int u = 0; u < kReduceBatch; ++u)
-        if (s0 + u < S) v[u] = __ldg(reinterpret_cast<const float4*>(src + (s0 + u) * MN));
-#pragma unroll
-      for (int u = 0; u < kReduceBatch; ++u)
-        if (s0 + u < S) {
-          acc.x += v[u].x;
-          acc.y += v[u].y;
-          acc.z += v[u].z;
-          acc.w += v[u].w;
-        }
+    for (int sp = 0; sp < S; ++sp) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(src + sp * MN));
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
     }
     float* Crow = p.C + (long long)row * p.ldc;
     float4 out;
@@ -883,15 +870,7 @@ __global__ void __launch_bounds__(1024) splitk_reduce_t_kernel(const float* __re
     float acc = 0.f;
     if (i < M && j < N) {
       const float* src = ws + (long long)i * N + j;
-      for (int s0 = 0; s0 < S; s0 += kReduceBatch) {  // batched loads, ordered adds
-        float v[kReduceBatch];
-#pragma unroll
-        for (int u = 0; u < kReduceBatch; ++u)
-          if (s0 + u < S) v[u] = __ldg(src + (s0 + u) * MN);
-#pragma unroll
-        for (int u = 0; u < kReduceBatch; ++u)
-          if (s0 + u < S) acc += v[u];
-      }
+      for (int sp = 0; sp < S; ++sp) acc += src[sp * MN];
     }
     tile[ty][tx] = acc;
   }
