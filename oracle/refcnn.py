@@ -71,11 +71,39 @@ def lower(D: np.ndarray, k: int, s: int, p: int, start: int = 0, b_p: int | None
     return np.ascontiguousarray(g.transpose(0, 2, 3, 1, 4, 5).reshape(b_p * m * m, c * k * k))
 
 
+# "einsum": the reference's blocked einsum (tensors.py:193-210) -- what the CPU
+# baseline times.  "blas": one float64 BLAS product per call; the summation order
+# differs from the blocked einsum only at the 1e-16 level, which is far below
+# every fp32 tolerance, so the large-batch parity tests (CaffeNet at b=256) use
+# it to keep the checker to seconds.  Select with ``gemm_impl("blas")``.
+GEMM_IMPL = "einsum"
+
+
+class gemm_impl:
+    """Context manager: ``with gemm_impl("blas"): ...`` (restores on exit)."""
+
+    def __init__(self, name: str):
+        if name not in ("einsum", "blas"):
+            raise ValueError(name)
+        self.name = name
+
+    def __enter__(self):
+        global GEMM_IMPL
+        self.prev, GEMM_IMPL = GEMM_IMPL, self.name
+        return self
+
+    def __exit__(self, *exc):
+        global GEMM_IMPL
+        GEMM_IMPL = self.prev
+
+
 def gemm(A: np.ndarray, B: np.ndarray) -> np.ndarray:
     """R = A @ B in float64 with the inner dimension consumed in ascending
     GEMM_BLOCK-wide blocks, one einsum per block (tensors.py:193-210)."""
     A = np.asarray(A, dtype=np.float64)
     B = np.asarray(B, dtype=np.float64)
+    if GEMM_IMPL == "blas":
+        return A @ B
     out = np.zeros((A.shape[0], B.shape[1]))
     for j0 in range(0, A.shape[1], GEMM_BLOCK):
         j1 = min(j0 + GEMM_BLOCK, A.shape[1])

@@ -282,6 +282,18 @@ __host__ __device__ constexpr uint32_t instr_desc() {
          ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(MM >> 4) << 24);
 }
 
+// 3xTF32 operand split: hi = x rounded to the nearest tf32 (adding half an
+// ulp of the 10-bit mantissa to the magnitude bits, then truncating), lo =
+// x - hi (exact in fp32, |lo| <= 2^-11 |x|, either sign).  The tensor core
+// truncates lo to tf32 again, so the dropped part is <= 2^-21 |x| and, lo's
+// sign varying, unbiased -- a plain truncating split leaves lo >= 0 relative
+// to x and its truncation error biased, which cancellation in long K sums
+// turns into a ~4x larger normwise error.
+__device__ __forceinline__ void split_tf32(uint32_t x, uint32_t& hi, uint32_t& lo) {
+  hi = (x + 0x1000u) & 0xFFFFE000u;
+  lo = __float_as_uint(__uint_as_float(x) - __uint_as_float(hi));
+}
+
 __device__ __forceinline__ void decode_work(const Params& p, int w, int& mt, int& nt, int& sp) {
   const int per = p.m_tiles * p.n_tiles;
   sp = w / per;
@@ -745,10 +757,10 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
         for (int i = t; i < L::STAGE / 16; i += 128) {
           const uint4 v = hi[i];
           uint4 h, l;
-          h.x = v.x & 0xFFFFE000u; l.x = __float_as_uint(__uint_as_float(v.x) - __uint_as_float(h.x));
-          h.y = v.y & 0xFFFFE000u; l.y = __float_as_uint(__uint_as_float(v.y) - __uint_as_float(h.y));
-          h.z = v.z & 0xFFFFE000u; l.z = __float_as_uint(__uint_as_float(v.z) - __uint_as_float(h.z));
-          h.w = v.w & 0xFFFFE000u; l.w = __float_as_uint(__uint_as_float(v.w) - __uint_as_float(h.w));
+          split_tf32(v.x, h.x, l.x);
+          split_tf32(v.y, h.y, l.y);
+          split_tf32(v.z, h.z, l.z);
+          split_tf32(v.w, h.w, l.w);
           hi[i] = h;
           lo[i] = l;
         }
