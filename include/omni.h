@@ -176,6 +176,11 @@ int omni_bias_grad_f32(const float* dY, long long ld, int M, int N, float* db, f
  * W = W + V.  w_read may alias W (synchronous step).                         */
 int omni_sgd_momentum_f32(float* W, float* V, const float* g, const float* w_read, float eta,
                           float mu, float lam, long long n, void* stream);
+/* K8 in float64 for the drop-in host API (SGDState keeps float64, sgd.py:72-101):
+ * same update, the reference's evaluation order, no FMA contraction, so it
+ * is bit-identical to the NumPy expression.                                  */
+int omni_sgd_momentum_f64(double* W, double* V, const double* g, const double* w_read, double eta,
+                          double mu, double lam, long long n, void* stream);
 /* K9 batch gather (problems.py:197-199): dst[i,:] = src[idx[i],:].            */
 int omni_gather_rows_f32(const float* src, long long row_elems, const int64_t* idx, int nidx,
                          float* dst, void* stream);

@@ -40,6 +40,7 @@ _P = ctypes.c_void_p
 _I = ctypes.c_int
 _L = ctypes.c_longlong
 _F = ctypes.c_float
+_D = ctypes.c_double
 
 # name -> (restype, argtypes); mirrors include/omni.h one to one.
 SIGNATURES: dict[str, tuple] = {
@@ -78,6 +79,7 @@ SIGNATURES: dict[str, tuple] = {
     "omni_bias_grad_ws_elems": (_L, [_I, _I]),
     "omni_bias_grad_f32": (_I, [_P, _L, _I, _I, _P, _P, _P]),
     "omni_sgd_momentum_f32": (_I, [_P, _P, _P, _P, _F, _F, _F, _L, _P]),
+    "omni_sgd_momentum_f64": (_I, [_P, _P, _P, _P, _D, _D, _D, _L, _P]),
     "omni_gather_rows_f32": (_I, [_P, _L, _P, _I, _P, _P]),
     "omni_gather_i32": (_I, [_P, _P, _I, _P, _P]),
     "omni_conv_weight_to_tap_f32": (_I, [_P, _I, _I, _I, _P, _L, _I, _P, _P]),

@@ -486,6 +486,23 @@ __global__ void __launch_bounds__(kThreads) sgd_kernel_scalar(float* W, float* V
   }
 }
 
+// float64 K8 for the drop-in host API (sgd.py:92-101 keeps W, V in float64):
+// the reference's NumPy expression evaluated in its exact order, one rounding
+// per operation and no FMA contraction (the _rn intrinsics), so the result is
+// bit-identical to  V' = mu*V - eta*(g + lam*w);  W' = W + V'.
+__global__ void __launch_bounds__(kThreads) sgd_kernel_f64(double* W, double* V,
+                                                           const double* __restrict__ g,
+                                                           const double* w_read, double eta,
+                                                           double mu, double lam, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double reg = __dadd_rn(g[i], __dmul_rn(lam, w_read[i]));
+    const double v = __dsub_rn(__dmul_rn(mu, V[i]), __dmul_rn(eta, reg));
+    V[i] = v;
+    W[i] = __dadd_rn(W[i], v);
+  }
+}
+
 // One block-stride loop per gathered row: no per-element division.
 template <bool VEC4>
 __global__ void __launch_bounds__(kThreads) gather_rows_kernel(const float* __restrict__ src,
@@ -668,6 +685,15 @@ int omni_sgd_momentum_f32(float* W, float* V, const float* g, const float* w_rea
     sgd_kernel_scalar<<<omni::grid_for(n, kThreads), kThreads, 0, st>>>(W, V, g, w_read, eta, mu,
                                                                        lam, n);
   return omni::check_launch("sgd_momentum");
+}
+
+int omni_sgd_momentum_f64(double* W, double* V, const double* g, const double* w_read, double eta,
+                          double mu, double lam, long long n, void* stream) {
+  OMNI_REQUIRE(n >= 0, "sgd: negative length");
+  if (n == 0) return OMNI_OK;
+  sgd_kernel_f64<<<omni::grid_for(n, kThreads), kThreads, 0, omni::as_stream(stream)>>>(
+      W, V, g, w_read, eta, mu, lam, n);
+  return omni::check_launch("sgd_momentum_f64");
 }
 
 int omni_gather_rows_f32(const float* src, long long row_elems, const int64_t* idx, int nidx,

@@ -280,6 +280,16 @@ def sgd_momentum(W: torch.Tensor, V: torch.Tensor, g: torch.Tensor, w_read: torc
          W.numel(), _stream())
 
 
+def sgd_momentum_f64(W: torch.Tensor, V: torch.Tensor, g: torch.Tensor, w_read: torch.Tensor,
+                     eta: float, mu: float, lam: float) -> None:
+    """float64 K8 (bit-identical to the reference's NumPy update)."""
+    for t in (W, V, g, w_read):
+        if t.dtype != torch.float64:
+            raise ValueError("sgd_momentum_f64 takes float64 tensors")
+    call("omni_sgd_momentum_f64", _ptr(W), _ptr(V), _ptr(g), _ptr(w_read), eta, mu, lam,
+         W.numel(), _stream())
+
+
 def gather_rows(src: torch.Tensor, idx: torch.Tensor, dst: torch.Tensor) -> None:
     row = src[0].numel()
     call("omni_gather_rows_f32", _ptr(src), row, _ptr(idx), idx.numel(), _ptr(dst), _stream())

@@ -27,7 +27,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from .cluster import ExecutionPlan, PhaseProfile, min_saturating_groups, power_of_two_divisors
-from .sgd import Hyperparams, SGDState
+from .sgd import Hyperparams, SGDState, child_seed
 
 TRAILING = 50
 MAX_EXTENSIONS = 5
@@ -96,23 +96,36 @@ class DecisionLog:
 class SimEnv:
     """The simulation environment probes run in: a problem, N devices, a
     PhaseProfile (measured on B200 or synthetic), the group batch and the
-    batch-stream seed every probe shares (paired probes)."""
+    batch-stream seed.  Probes of one search round are paired (same start
+    state, same seed); every training epoch advances ``seed_cursor`` so
+    successive epochs draw fresh batches (the cursor is what a checkpoint
+    records as ``seed_cursor`` to resume the same batch sequence)."""
 
     def __init__(self, problem, N: int, profile: PhaseProfile, b: int, seed: int = 0,
                  service_mode: str = "deterministic", loss_sample_interval: int = 1):
         self.problem, self.N, self.profile, self.b = problem, N, profile, b
         self.seed, self.service_mode, self.loss_sample_interval = seed, service_mode, loss_sample_interval
         self.sim_seconds = 0.0        # everything probed or trained, charged to the budget
+        self.seed_cursor = 0          # training epochs run so far
 
-    def run(self, state: SGDState, g: int, mu: float, eta: float, sim_seconds: float) -> ProbeResult:
+    def current_seed(self) -> int:
+        """Batch-stream seed of the current round: child_seed(seed, 4, cursor)
+        (sgd.py:43-46 derivation), the plain seed before the first epoch."""
+        return self.seed if self.seed_cursor == 0 else child_seed(self.seed, 4, self.seed_cursor)
+
+    def run(self, state: SGDState, g: int, mu: float, eta: float, sim_seconds: float,
+            train: bool = False) -> ProbeResult:
         from .simulator import SimConfig, simulate
 
         cfg = SimConfig(plan=ExecutionPlan(self.N, g), profile=self.profile,
                         hp=Hyperparams(eta=eta, mu=mu, b=self.b), problem=self.problem,
-                        service_mode=self.service_mode, max_sim_seconds=sim_seconds, seed=self.seed,
-                        init=state, loss_sample_interval=self.loss_sample_interval)
+                        service_mode=self.service_mode, max_sim_seconds=sim_seconds,
+                        seed=self.current_seed(), init=state,
+                        loss_sample_interval=self.loss_sample_interval)
         tr = simulate(cfg)
         self.sim_seconds += sim_seconds
+        if train:
+            self.seed_cursor += 1
         losses = np.asarray(tr.loss_values, dtype=np.float64)
         tail = losses[-TRAILING:] if losses.size else np.array([np.inf])
         loss = float(np.mean(tail)) if not tr.diverged else float("inf")
@@ -246,16 +259,16 @@ def optimize(problem, env, grid: GridSpec, epochs: EpochConfig, checkpoint_dir: 
             if mu == 0.0:
                 mu = refine_zero_momentum(grid, state, g, env, eta)
         probe = env.sim_seconds - before
-        r = env.run(state, g, mu, eta, epochs.T)
+        r = env.run(state, g, mu, eta, epochs.T, train=True)
         state = r.state
         ckpt = ""
         if checkpoint_dir is not None:
             import os
 
-            ckpt = os.path.join(checkpoint_dir, f"epoch{epoch}.omnickpt.npz")
+            # (g, mu, eta) of the epoch are in the decision log row that names the file
+            ckpt = os.path.join(checkpoint_dir, f"epoch{epoch}.omnickpt")
             save_checkpoint(Checkpoint(W=np.asarray(state.W), V=np.asarray(state.V), t=state.t,
-                                       rng_cursor={"seed": env.seed, "epoch": epoch},
-                                       context={"g": g, "mu": mu, "eta": eta}), ckpt)
+                                       seed_cursor=env.seed_cursor), ckpt)
         log.records.append(DecisionRecord(epoch, g, mu, eta, probe / (probe + epochs.T), r.loss, ckpt))
         if r.diverged or (epochs.target_loss is not None and r.loss <= epochs.target_loss):
             break
@@ -263,47 +276,64 @@ def optimize(problem, env, grid: GridSpec, epochs: EpochConfig, checkpoint_dir: 
 
 
 # ---------------------------------------------------------- checkpoints --
-CKPT_FORMAT = "omni-checkpoint"
-CKPT_VERSION = 1
+CKPT_MAGIC = "OMNISIM-CKPT"
+CKPT_VERSION = "v1"
 
 
 @dataclass
 class Checkpoint:
+    """text header ``OMNISIM-CKPT v1 dim=<d> t=<t> seed_cursor=<u64>``
+    followed by d decimal values for W then d for V, newline-separated; each
+    value is the shortest decimal that round-trips the binary64 exactly
+    (Python's repr), so the format is lossless and human-inspectable."""
+
     W: np.ndarray
     V: np.ndarray
     t: int
-    rng_cursor: dict
-    context: dict
+    seed_cursor: int = 0
 
 
 def save_checkpoint(ck: Checkpoint, path) -> None:
-    """Lossless: float64 W, V plus a JSON header (format, version, dim, t, rng
-    cursor, decision context)."""
     W = np.asarray(ck.W, dtype=np.float64)
     V = np.asarray(ck.V, dtype=np.float64)
     if W.shape != V.shape or W.ndim != 1:
         raise ValueError("checkpoint W and V must be 1-D and the same length")
-    header = {"format": CKPT_FORMAT, "version": CKPT_VERSION, "dim": int(W.shape[0]), "t": int(ck.t),
-              "rng_cursor": ck.rng_cursor, "context": ck.context}
-    with open(path, "wb") as f:
-        np.savez(f, header=np.frombuffer(json.dumps(header).encode(), dtype=np.uint8), W=W, V=V)
+    if not (0 <= int(ck.seed_cursor) < 2 ** 64) or int(ck.t) < 0:
+        raise ValueError("checkpoint t must be >= 0 and seed_cursor a u64")
+    with open(path, "w") as f:
+        f.write(f"{CKPT_MAGIC} {CKPT_VERSION} dim={W.shape[0]} t={int(ck.t)} seed_cursor={int(ck.seed_cursor)}\n")
+        f.write("\n".join(map(repr, W.tolist())))
+        f.write("\n")
+        if V.size:
+            f.write("\n".join(map(repr, V.tolist())))
+            f.write("\n")
 
 
 def load_checkpoint(path) -> Checkpoint:
-    with np.load(path, allow_pickle=False) as z:
+    """Parse the SPEC format; a malformed header names the offending field."""
+    with open(path) as f:
+        header = f.readline().rstrip("\n").split(" ")
+        body = f.read().split()
+    if len(header) < 1 or header[0] != CKPT_MAGIC:
+        raise ValueError(f"checkpoint header field 'magic': expected {CKPT_MAGIC!r}, got {header[:1]!r}")
+    if len(header) < 2 or header[1] != CKPT_VERSION:
+        got = header[1] if len(header) > 1 else None
+        raise ValueError(f"checkpoint header field 'version': expected {CKPT_VERSION!r}, got {got!r}")
+    fields = {}
+    for tok in header[2:]:
+        k, _, v = tok.partition("=")
+        fields[k] = v
+    vals = {}
+    for key in ("dim", "t", "seed_cursor"):
+        if key not in fields:
+            raise ValueError(f"checkpoint header field {key!r}: missing")
         try:
-            header = json.loads(bytes(z["header"]).decode())
-        except Exception as e:  # noqa: BLE001
-            raise ValueError(f"checkpoint header: unreadable ({e})") from None
-        for key, want in (("format", CKPT_FORMAT), ("version", CKPT_VERSION)):
-            if header.get(key) != want:
-                raise ValueError(f"checkpoint header field {key!r}: expected {want!r}, got {header.get(key)!r}")
-        for key in ("dim", "t", "rng_cursor", "context"):
-            if key not in header:
-                raise ValueError(f"checkpoint header field {key!r}: missing")
-        W, V = z["W"], z["V"]
-        if W.shape != (header["dim"],) or V.shape != (header["dim"],):
-            raise ValueError(f"checkpoint header field 'dim': {header['dim']} does not match W/V")
-        return Checkpoint(W=W.copy(), V=V.copy(), t=int(header["t"]), rng_cursor=header["rng_cursor"],
-                          context=header["context"])
-
+            vals[key] = int(fields[key])
+        except ValueError:
+            raise ValueError(f"checkpoint header field {key!r}: not an integer ({fields[key]!r})") from None
+    d = vals["dim"]
+    if d < 0 or len(body) != 2 * d:
+        raise ValueError(f"checkpoint header field 'dim': {d} does not match the {len(body)} values "
+                         "(expected 2 x dim)")
+    data = np.array([float(x) for x in body], dtype=np.float64)
+    return Checkpoint(W=data[:d].copy(), V=data[d:].copy(), t=vals["t"], seed_cursor=vals["seed_cursor"])

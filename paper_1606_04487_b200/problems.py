@@ -120,7 +120,12 @@ class DeviceSession:
         self.t = state.t
         self.engine = problem.engine(hp.b)
         self.pg = process_group
-        self._staged: dict[int, tuple] = {}   # id(HostBatch) -> (slot, ready event)
+        # id(HostBatch) -> (slot, ready event, the batch itself): the entry is
+        # only honoured for that very object (an id can be reused once the
+        # batch is garbage collected); _slot_owner[s] is the staged batch that
+        # slot s holds and no step has consumed yet
+        self._staged: dict[int, tuple] = {}
+        self._slot_owner = [None, None]
         self._slots = None
         self._slot_free = [None, None]
         self._next_slot = 0
@@ -204,6 +209,9 @@ class DeviceSession:
             self._slots = [(torch.empty_like(eng.input.value), torch.empty_like(eng.labels))
                            for _ in range(2)]
         slot = self._next_slot
+        if self._slot_owner[slot] is not None:
+            raise ValueError("prefetch: both staging slots hold prefetched batches that have not been "
+                             "stepped yet (at most two outstanding prefetches)")
         self._next_slot ^= 1
         X, y = self._slots[slot]
         b = batch.size
@@ -214,7 +222,8 @@ class DeviceSession:
             y[:b].copy_(batch.y, non_blocking=True)
             ready = torch.cuda.Event()
             ready.record(self._copy_stream)
-        self._staged[id(batch)] = (slot, ready)
+        self._staged[id(batch)] = (slot, ready, batch)
+        self._slot_owner[slot] = batch
 
     # ------------------------------------------------------------ steps --
     def _compute_merged(self, wr: torch.Tensor, b: int) -> None:
@@ -300,6 +309,14 @@ class DeviceSession:
         finally:
             eng.input.value, eng.labels = own            # launches already hold the pointers
 
+    def _staged_entry(self, batch) -> bool:
+        """Whether ``batch`` (this very object) sits prefetched in a slot."""
+        e = self._staged.get(id(batch))
+        if e is not None and e[2] is not batch:      # a recycled id: stale entry
+            del self._staged[id(batch)]
+            return False
+        return e is not None
+
     def _graph_key(self, batch, w_read):
         if not (self.use_graph and (self.world == 1 or self.use_p2p) and w_read is None and
                 self.engine.timer is None and self.engine.overlap):
@@ -307,7 +324,7 @@ class DeviceSession:
         base = (self.W.data_ptr(), self.V.data_ptr())
         if isinstance(batch, DeviceBatch) and batch.size == self.engine.b:
             return ("device", self.problem.data.data_ptr()) + base
-        if isinstance(batch, HostBatch) and batch.size == self.engine.b and id(batch) in self._staged:
+        if isinstance(batch, HostBatch) and batch.size == self.engine.b and self._staged_entry(batch):
             return ("host", self._staged[id(batch)][0]) + base
         return None
 
@@ -319,7 +336,10 @@ class DeviceSession:
         captured in a CUDA graph on their second occurrence and replayed after."""
         wr = self.W if w_read is None else w_read
         key = self._graph_key(batch, w_read)
-        staged = self._staged.pop(id(batch), None) if isinstance(batch, HostBatch) else None
+        staged = None
+        if isinstance(batch, HostBatch) and self._staged_entry(batch):
+            staged = self._staged.pop(id(batch))
+            self._slot_owner[staged[0]] = None
         cur = torch.cuda.current_stream()
         if staged is not None:
             cur.wait_event(staged[1])                     # H2D of this batch done

@@ -20,12 +20,18 @@ Two views of one training step:
   are compared (errors compound through 8 layers; argmax flips between fp32
   and fp64 near-ties are counted and reported).
 
-Bounds (normwise relative error; DESIGN.md section 4 states them):
+Bounds (normwise relative error; DESIGN.md section 4 states them with the
+measured values):
 
-  layer-isolated   3xTF32 <= 2e-5      TF32 <= 5e-3
-  cascade          3xTF32 <= 1e-4      TF32 <= 2e-2 (activations 1e-2)
-  g=1 multi-step weights (update W_T - W_0 after 10 steps):
-                   3xTF32 <= 1e-4      TF32 <= 2e-2
+  layer-isolated, forward / data gradient     3xTF32 <= 5e-5   TF32 <= 5e-3
+  layer-isolated, weight / bias gradient      3xTF32 <= 3e-4   TF32 <= 5e-3
+      (fp32 accumulation over K = b*m^2 = 43,264 .. 774,400 terms)
+  max-pool values, argmax indices             bit-identical
+  cascade activations                         3xTF32 <= 2e-4   TF32 <= 1e-2
+  cascade gradients                           <= 2 sqrt(max activation error)
+      (ReLU-mask / argmax flips; see the cascade test)
+  g=1 run_sync, 10 steps: W_T                 <= 1e-4 (both)
+                          W_T - W_0, V_T      3xTF32 <= 2e-4   TF32 <= 2e-2
 """
 
 import os
@@ -44,10 +50,10 @@ pytestmark = pytest.mark.gpu
 
 ISO = {"3xtf32": 5e-5, "tf32": 5e-3}          # forward / data-gradient products, K <= 9216
 ISO_RED = {"3xtf32": 3e-4, "tf32": 5e-3}      # weight / bias gradients: K = b*m^2 up to 774,400
-CASCADE = {"3xtf32": 1e-2, "tf32": 5e-2}      # parameter gradients through the whole step
 CASCADE_ACT = {"3xtf32": 2e-4, "tf32": 1e-2}  # activations through the whole step
+CASCADE_GRAD_K = 2.0   # cascade gradients: <= K * sqrt(max activation error), see the cascade test
 SYNC_W = 1e-4                                 # run_sync: W_T normwise, both modes
-SYNC_DW = {"3xtf32": 3e-3, "tf32": 3e-2}      # run_sync: the learned update W_T - W_0
+SYNC_DW = {"3xtf32": 2e-4, "tf32": 2e-2}      # run_sync: the learned update W_T - W_0
 
 
 def nrel(x, ref):
@@ -242,22 +248,33 @@ def oracle_outputs(net, W, X):
 @pytest.mark.parametrize("precision", ["3xtf32", "tf32"])
 def test_caffenet_b256_cascade(precision, blas):
     """The whole step from the same batch and weights: per-layer activations,
-    loss and every parameter gradient against the oracle's cascade."""
+    loss and every parameter gradient against the oracle's cascade.
+
+    Activations carry the compounded arithmetic error (bounded absolutely).
+    Gradients are discontinuous in the activations: a ReLU mask bit
+    (problems.py:261, strict z > 0) or a max-pool argmax (:215-216) flips
+    wherever an activation within the forward error of 0 / of a tie sits, and
+    each flip moves a whole O(|dZ|) gradient entry.  The flipped fraction grows
+    linearly with the activation error e, so the gradient error grows like
+    sqrt(e); the bound is CASCADE_GRAD_K * sqrt(max activation error), with the
+    flip counts printed.  The per-kernel arithmetic is bounded tightly by the
+    layer-isolated test."""
     net = nets.caffenet()
     b = 256
     W = he_weights(net, 5)
     e, X, y, G = run_step(net, b, precision, W)
     dicts = net.to_dicts()
     outs, args = oracle_outputs(net, W, X)
-    bound_a, bound_g = CASCADE_ACT[precision], CASCADE[precision]
-    report, flips = [], {}
+    report, flips, mask_flips = [], {}, {}
     li = 0
     for op in e.ops:
         while dicts[li]["kind"] != op.kind:
             li += 1
         last = li + 1 if op.kind in ("conv", "fc") and op.relu else li   # fused ReLU
-        got = host(op.out, b=b)
-        report.append((last, f"{op.kind} out", nrel(got.reshape(outs[last].shape), outs[last])))
+        got = host(op.out, b=b).reshape(outs[last].shape)
+        report.append((last, f"{op.kind} out", nrel(got, outs[last])))
+        if last != li:   # ReLU mask: GPU (post-ReLU > 0) vs oracle (pre-ReLU > 0)
+            mask_flips[li] = int(((got > 0) != (outs[li] > 0)).sum())
         if op.kind == "pool" and li in args:
             ga = op.argmax[: b * op.m * op.m * op.inp.c].view(b, op.m, op.m, op.inp.c)
             flips[li] = int((ga.permute(0, 3, 1, 2).cpu().numpy() != args[li]).sum())
@@ -271,17 +288,17 @@ def test_caffenet_b256_cascade(precision, blas):
         for off, sz, nm in zip(geo.param_offsets, geo.param_sizes, ("weight", "bias")):
             if sz:
                 greport.append((geo.index, f"{geo.layer.kind} {nm} grad", nrel(G[off:off + sz], ref_g[off:off + sz])))
-    print(f"\nCaffeNet b=256 {precision} cascade: loss {loss:.7f} vs {ref_loss:.7f}; "
-          f"argmax flips vs fp64 per pool layer {flips} of "
-          f"{ {li: int(a.size) for li, a in args.items()} } windows")
+    act_err = max(err for _, _, err in report)
+    gbound = CASCADE_GRAD_K * np.sqrt(act_err)
+    print(f"\nCaffeNet b=256 {precision} cascade: loss {loss:.7f} vs {ref_loss:.7f}; max activation error "
+          f"{act_err:.2e} -> gradient bound {gbound:.2e}\n  argmax flips per max-pool layer {flips} of "
+          f"{ {li: int(a.size) for li, a in args.items()} } windows; ReLU mask flips per layer {mask_flips}")
     for li, what, err in report + greport:
         print(f"  layer {li!s:>3} {what:<16} {err:.3e}")
-    for _, _, err in report:
-        assert err < bound_a, (report, flips)
-    assert abs(loss - ref_loss) < bound_a * max(1.0, ref_loss)
+    assert act_err < CASCADE_ACT[precision], report
+    assert abs(loss - ref_loss) < CASCADE_ACT[precision] * max(1.0, ref_loss)
     for _, _, err in greport:
-        assert err < bound_g, (greport, flips)
-    assert nrel(G, ref_g) < bound_g
+        assert err < gbound, (greport, flips, mask_flips)
 
 
 # --------------------------------------------- g = 1 multi-step weights ---

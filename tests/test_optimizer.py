@@ -20,7 +20,7 @@ class StubEnv:
         self.f, self.N, self.profile, self.seed = f, N, profile, 0
         self.calls, self.sim_seconds = [], 0.0
 
-    def run(self, state, g, mu, eta, secs):
+    def run(self, state, g, mu, eta, secs, train=False):
         self.calls.append((g, mu, eta, secs))
         self.sim_seconds += secs
         loss = self.f(g, mu, eta, secs)
@@ -108,24 +108,42 @@ def test_init_groups_is_the_smallest_saturating_count():
 
 
 def test_checkpoint_round_trip_and_corrupt_header(tmp_path):
+    """SPEC.md:574 text format: lossless decimal round trip of binary64 and a
+    header whose errors name the field."""
     rng = np.random.default_rng(0)
-    ck = O.Checkpoint(W=rng.standard_normal(101), V=rng.standard_normal(101), t=42,
-                      rng_cursor={"seed": 7, "epoch": 3}, context={"g": 4, "mu": 0.3, "eta": 0.01})
-    path = tmp_path / "a.npz"
+    W = rng.standard_normal(101) * 10.0 ** rng.integers(-300, 300, 101)
+    W[:3] = [0.1, -0.0, 5e-324]
+    ck = O.Checkpoint(W=W, V=rng.standard_normal(101), t=42, seed_cursor=2 ** 64 - 1)
+    path = tmp_path / "a.omnickpt"
     O.save_checkpoint(ck, path)
+    text = path.read_text().splitlines()
+    assert text[0] == f"OMNISIM-CKPT v1 dim=101 t=42 seed_cursor={2 ** 64 - 1}"
+    assert len(text) == 1 + 2 * 101 and text[1] == "0.1"
     back = O.load_checkpoint(path)
     assert np.array_equal(back.W, ck.W) and np.array_equal(back.V, ck.V)
-    assert (back.t, back.rng_cursor, back.context) == (ck.t, ck.rng_cursor, ck.context)
-    import json
-    z = dict(np.load(path))
-    h = json.loads(bytes(z["header"]).decode())
-    h["version"] = 99
-    z["header"] = np.frombuffer(json.dumps(h).encode(), dtype=np.uint8)
-    bad = tmp_path / "bad.npz"
-    with open(bad, "wb") as f:
-        np.savez(f, **z)
+    assert np.array_equal(np.signbit(back.W), np.signbit(ck.W))
+    assert (back.t, back.seed_cursor) == (42, 2 ** 64 - 1)
+    bad = tmp_path / "bad.omnickpt"
+    bad.write_text("\n".join(["OMNISIM-CKPT v2 dim=101 t=42 seed_cursor=0"] + text[1:]) + "\n")
     with pytest.raises(ValueError, match="'version'"):
         O.load_checkpoint(bad)
+    bad.write_text("\n".join(["OMNISIM-CKPT v1 dim=100 t=42 seed_cursor=0"] + text[1:]) + "\n")
+    with pytest.raises(ValueError, match="'dim'"):
+        O.load_checkpoint(bad)
+    bad.write_text("\n".join(["OMNISIM-CKPT v1 dim=101 t=42"] + text[1:]) + "\n")
+    with pytest.raises(ValueError, match="'seed_cursor'"):
+        O.load_checkpoint(bad)
+
+
+def test_training_epochs_advance_the_seed_cursor():
+    """Probes of one round share the batch-stream seed (paired); every training
+    epoch advances the cursor, so epochs do not replay the same batches."""
+    env = O.SimEnv(None, N=8, profile=PhaseProfile(T_cc=1.0, T_nc=0.0, t_fc=0.1), b=4, seed=9)
+    s0 = env.current_seed()
+    env.seed_cursor += 1
+    s1 = env.current_seed()
+    env.seed_cursor += 1
+    assert len({s0, s1, env.current_seed()}) == 3 and s0 == 9
 
 
 def test_decision_log_csv(tmp_path):

@@ -221,3 +221,48 @@ def test_full_grad_and_chunked_loss():
     assert nrel(prob.full_grad(W), ref) < 2e-5
     ref_loss = R.loss(net.to_dicts(), 1, 28, W, prob.images, prob.labels)
     assert abs(prob.full_loss(W) - ref_loss) < 1e-5
+
+
+def test_sgd_step_bit_exact_vs_oracle():
+    """The drop-in sgd_step (float64 K8) equals the reference's NumPy update
+    (sgd.py:92-101) bit for bit, stale regulariser snapshot included."""
+    rng = np.random.default_rng(4)
+    n = 100_003
+    W, V, g, wr = (rng.standard_normal(n) for _ in range(4))
+    hp = P.Hyperparams(eta=0.0123, mu=0.87, lam=3e-4)
+    s = P.sgd_step(P.SGDState(W=W, V=V, t=5), hp, g, wr)
+    W2, V2 = R.sgd_step(W, V, g, wr, hp.eta, hp.mu, hp.lam)
+    assert np.array_equal(s.V, V2) and np.array_equal(s.W, W2) and s.t == 6
+
+
+@pytest.mark.parametrize("g", [1, 2, 4, 8])
+def test_measured_he_deterministic(g):
+    """measured_he (simulator.py:216-223) after a 100-event burn-in is within
+    2% of he_predict for deterministic services (SPEC measured_he examples);
+    g = 1 is exactly t_conv(N) + t_fc; the N = 8, g = 8 profile of the SPEC
+    example is FC-saturated at t_fc."""
+    prob = TinyCNNProblem(8, 4, seed=3, n_examples=64)
+    plan = P.ExecutionPlan(N=8, g=g)
+    prof = P.PhaseProfile(T_cc=10.0, T_nc=0.1, t_fc=2.0)
+    cfg = P.SimConfig(plan=plan, profile=prof, hp=P.Hyperparams(eta=0.01, mu=0.5, b=8), problem=prob,
+                      max_updates=300, seed=1)
+    tr = P.simulate(cfg)
+    he = P.measured_he(tr, burn_in=100)
+    pred = P.he_predict(plan, prof)
+    if g == 1:
+        assert abs(he - (P.t_conv(8, prof) + prof.t_fc)) < 1e-9
+    if g == 8:
+        assert P.fc_saturated(plan, prof) and abs(he - 2.0) < 1e-9
+    assert abs(he - pred) <= 0.02 * pred, (g, he, pred)
+
+
+def test_measured_he_exponential():
+    """Exponential services, 10k events: within 10% of he_predict (SPEC)."""
+    prob = TinyCNNProblem(8, 4, seed=3, n_examples=64)
+    plan = P.ExecutionPlan(N=8, g=4)
+    prof = P.PhaseProfile(T_cc=10.0, T_nc=0.1, t_fc=2.0)
+    cfg = P.SimConfig(plan=plan, profile=prof, hp=P.Hyperparams(eta=0.001, mu=0.0, b=4), problem=prob,
+                      service_mode="exponential", max_updates=10_000, loss_sample_interval=10_000, seed=2)
+    tr = P.simulate(cfg)
+    he, pred = P.measured_he(tr, burn_in=100), P.he_predict(plan, prof)
+    assert abs(he - pred) <= 0.10 * pred, (he, pred)

@@ -102,3 +102,22 @@ def test_empty_batch_fails_loudly():
     sess = prob.device_session(prob.initial_state(), P.Hyperparams(eta=0.01, b=8))
     with pytest.raises((ValueError, RuntimeError)):
         sess.step(DeviceBatch(torch.zeros(0, dtype=torch.int64, device="cuda")))
+
+
+def test_prefetch_refuses_a_third_outstanding_batch():
+    """Two staging slots: a third prefetch before any of the two staged batches
+    is stepped must fail loudly instead of overwriting a staged slot."""
+    prob = CNNProblem("lenet", n_examples=32, seed=3, precision="tf32")
+    sess = prob.device_session(prob.initial_state(), P.Hyperparams(eta=0.01, mu=0.9, b=8))
+    hbs = [HostBatch(torch.randn(8, 28, 28, 1).pin_memory(),
+                     torch.randint(0, 10, (8,), dtype=torch.int32).pin_memory()) for _ in range(4)]
+    sess.prefetch(hbs[0])
+    sess.prefetch(hbs[1])
+    with pytest.raises(ValueError, match="staging slots"):
+        sess.prefetch(hbs[2])
+    sess.step(hbs[0])                   # frees slot 0
+    sess.prefetch(hbs[2])
+    sess.step(hbs[1])
+    sess.step(hbs[2])
+    sess.step(hbs[3])                   # never prefetched: plain upload path
+    assert np.isfinite(sess.last_loss())
