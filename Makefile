@@ -10,7 +10,7 @@ LIB := paper_1606_04487_b200/libomni.so
 
 all: $(LIB)
 
-$(BUILD)/%.o: $(SRC_DIR)/%.cu $(SRC_DIR)/common.cuh include/omni.h
+$(BUILD)/%.o: $(SRC_DIR)/%.cu $(SRC_DIR)/common.cuh $(SRC_DIR)/tc_ptx.cuh include/omni.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/$*.ptxas.log || (cat $(BUILD)/$*.ptxas.log; exit 1)
 

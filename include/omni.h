@@ -172,6 +172,22 @@ int omni_relu_bwd_f32(const float* dY, const float* Y, float* dX, long long n, v
 long long omni_bias_grad_ws_elems(int M, int N);
 int omni_bias_grad_f32(const float* dY, long long ld, int M, int N, float* db, float* ws,
                        void* stream);
+/* Window implicit GEMM of a space-to-depth first layer (conv_window.cu):
+ * Xs is the (b, n2, n2, 48) space-to-depth image (omni_space_to_depth_f32,
+ * cp = 48), the conv is k2 x k2, stride 1, no padding, m = n2 - k2 + 1.
+ *   OMNI_CONV_FPROP:      Y[pix*ldy + o] = epi(sum_{tap,ch} Xs(pix, tap, ch) G[o*ldg + tap*48 + ch])
+ *                         (G = omni_conv_weight_s2d_f32 rows; d_out in {32, 64, 96, 128};
+ *                          epilogue STORE / BIAS / BIAS_RELU / RELU)
+ *   OMNI_CONV_WGRAD_BIAS: Y[o*ldy + tap*48 + ch] = sum_pix G[pix*ldg + o] Xs(pix, tap, ch),
+ *                         Y[o*ldy + k2*k2*48] = sum_pix G[pix*ldg + o]  (ldy >= k2*k2*48 + 16;
+ *                          d_out <= 128; workspace per omni_conv_window_plan)
+ * TF32 only (the 3xTF32 path keeps the generic implicit GEMM with cp = 64).
+ * omni_conv_window_plan returns the workspace bytes, or -1 when the window
+ * kernels do not cover the geometry (window rows > 256, k2 > 3, ...).         */
+long long omni_conv_window_plan(int op, int b, int n2, int cp, int k2, int d_out);
+int omni_conv_window_f32(int op, const float* Xs, int b, int n2, int cp, int k2, int d_out, const float* G,
+                         long long ldg, float* Y, long long ldy, int epilogue, const float* bias,
+                         float* workspace, long long ws_bytes, void* stream);
 /* K8 fused momentum SGD (sgd.py:92-101): V = mu*V - eta*(g + lam*w_read);
  * W = W + V.  w_read may alias W (synchronous step).                         */
 int omni_sgd_momentum_f32(float* W, float* V, const float* g, const float* w_read, float eta,

@@ -67,6 +67,8 @@ SIGNATURES: dict[str, tuple] = {
         [_I, _I, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _L, _P, _L, _I, _P, _P, _L, _P, _L, _P],
     ),
     "omni_conv_weight_flip_f32": (_I, [_P, _I, _I, _I, _P, _L, _P]),
+    "omni_conv_window_plan": (_L, [_I, _I, _I, _I, _I, _I]),
+    "omni_conv_window_f32": (_I, [_I, _P, _I, _I, _I, _I, _I, _P, _L, _P, _L, _I, _P, _P, _L, _P]),
     "omni_pool_out_size": (_I, [_I, _I, _I, _I, _I]),
     "omni_pool_fwd_nhwc_f32": (_I, [_I, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "omni_pool_bwd_nhwc_f32": (

@@ -1,0 +1,702 @@
+// Window implicit GEMM for the space-to-depth first layer (CaffeNet conv1:
+// 11x11 / stride 4 over 3 channels -> a 3x3 stride-1 conv over the
+// 48-channel space-to-depth image, lower.cu) -- the layer the generic im2col
+// path runs worst: its 128-pixel tiles re-read every input pixel once per
+// filter tap (9 im2col boxes per channel block) and pad the 48 channels to 64.
+//
+// Padded-width indexing: with the s2d image flattened to rows
+// q = (img * n2 + h) * n2 + w (pixel pitch cp = 48 floats), output pixel
+// (img, h, w) of a stride-1 k2 x k2 conv without padding reads, for filter tap
+// (kx, ky), exactly row q + kx * n2 + ky.  So a tile of 128 consecutive q
+// needs ONE contiguous window of 128 + (k2-1)(n2+1) rows (244 for conv1), and
+// each tap's A operand is that window shifted by a whole number of rows: the
+// tcgen05 descriptor simply starts kx*n2+ky rows in (tools/desc_probe.cu: a
+// descriptor may start at any 128 B / 64 B row of a TMA-swizzled tile).  Rows
+// q with h >= m or w >= m are junk (6.9% for conv1) and never stored.
+//
+//  * fprop  (C[q, o] = sum_{tap, ch} X[q + off(tap), ch] W[o, tap, ch]):
+//    CTA pairs (cta_group::2, M = 256 pixels, N = d_out); each CTA keeps its
+//    half of ALL the weights resident in shared memory for the whole launch
+//    and streams one 244-row window per tile: channels 0-31 as a 128-byte
+//    swizzled box, 32-47 as a 64-byte swizzled box (K = 432, not 576).
+//    A tile costs 244 rows x 192 B of L2->SM traffic instead of 9 x 128 rows
+//    x 256 B plus the weights.
+//  * wgrad  (dW[o, tap, ch] = sum_pix dZ[pix, o] X[q(pix) + off(tap), ch]):
+//    M = d_out (<= 128), N = taps x 48 + 16 (the bias: a resident all-ones
+//    operand) <= 512 TMEM columns, K = pixels, one K-block per output row
+//    (m pixels, padded to a multiple of 8 by the dZ box's zero fill).  The
+//    window is the MN-major B operand; every tap is one N = 48 MMA whose
+//    descriptor starts off(tap) rows into it.  Each CTA reduces a contiguous
+//    range of output rows; a fixed-order reduction sums the per-CTA partials
+//    (deterministic, no atomics).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <string.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace cwin {
+using namespace gemm;
+
+constexpr int CP = 48;        // space-to-depth channels (4 x 4 x 3)
+constexpr int C0 = 32;        // channels in the 128-byte swizzled box
+constexpr int C1 = CP - C0;   // channels in the 64-byte swizzled box
+constexpr int MAX_TAPS = 9;   // k2 <= 3
+constexpr int WIN_MAX = 256;  // TMA box rows
+
+PFN_cuTensorMapEncodeTiled_v12000 encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+int tmap(CUtensorMap* m, const float* p, int rank, const cuuint64_t* dims, const cuuint64_t* strides_b,
+         const cuuint32_t* box, CUtensorMapSwizzle sw) {
+  auto fn = encode();
+  if (!fn) {
+    omni::set_error("cuTensorMapEncodeTiled unavailable");
+    return OMNI_ECUDA;
+  }
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(p), dims, strides_b, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    omni::set_error("conv window: cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return OMNI_ECUDA;
+  }
+  return OMNI_OK;
+}
+
+// ------------------------------------------------------------- fprop ----
+struct FParams {
+  int b, n2, m, k2, n2sq;
+  long long rows;     // b * n2 * n2
+  int units;          // pair tiles of 256 padded pixels
+  int win_rows;       // 128 + (k2 - 1) * (n2 + 1)
+  int epilogue;
+  const float* bias;
+  float* Y;
+  long long ldy;
+};
+
+template <int BN>
+struct FLayout {
+  static constexpr int BNL = BN / 2;                 // weight rows (output channels) per CTA
+  static constexpr int B0_TAP = BNL * 128;           // one tap: BNL rows x 32 K, SW128
+  static constexpr int B1_TAP = BNL * 64;            // one tap: BNL rows x 16 K, SW64
+  static constexpr int B1_OFF = MAX_TAPS * B0_TAP;
+  static constexpr int B_ALLOC = (MAX_TAPS * (B0_TAP + B1_TAP) + 1023) / 1024 * 1024;
+  static constexpr int A0 = WIN_MAX * 128;           // window, channels 0-31
+  static constexpr int A1 = WIN_MAX * 64;            // window, channels 32-47
+  static constexpr int STAGE = A0 + A1;
+  static constexpr int STAGES = 2;
+  static constexpr int STAGE_OFF = B_ALLOC;
+  static constexpr int BAR_OFF = STAGE_OFF + STAGES * STAGE;
+  static constexpr int BIAS_OFF = BAR_OFF + 256;    // BN floats
+  static constexpr int STG_PITCH = 36;               // floats per staged row (32 + 4: conflict-free)
+  static constexpr int STG_OFF = BIAS_OFF + 512;     // 4 warps x 32 rows x STG_PITCH floats
+  static constexpr int BYTES = STG_OFF + 4 * 32 * STG_PITCH * 4 + 1024;
+  static constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : 256);
+  static constexpr int ACC_STRIDE = TMEM_COLS / 2;
+  static_assert(BYTES <= 232448, "fprop window layout exceeds shared memory");
+  static_assert(B0_TAP % 1024 == 0 && B1_TAP % 512 == 0 && B1_OFF % 1024 == 0, "swizzle alignment");
+};
+
+template <int MODE>
+__device__ __forceinline__ float fepi(float acc, const float* bias, int col) {   // bias: shared memory
+  if (MODE == OMNI_EPI_BIAS) return acc + bias[col];
+  if (MODE == OMNI_EPI_BIAS_RELU) return fmaxf(acc + bias[col], 0.f);
+  if (MODE == OMNI_EPI_RELU) return fmaxf(acc, 0.f);
+  return acc;
+}
+
+// Apply the epilogue to one lane's 32 accumulator columns and stage them as
+// that lane's row of the warp's 32 x 32 staging tile (pitch 36 floats).
+template <int MODE>
+__device__ __forceinline__ void fstage32(float* srow, const uint32_t (&r0)[16], const uint32_t (&r1)[16],
+                                         const float* bias, int c0) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t* r = j < 4 ? r0 : r1;
+    const int k = (j & 3) * 4;
+    float4 v;
+    v.x = fepi<MODE>(__uint_as_float(r[k]), bias, c0 + 4 * j);
+    v.y = fepi<MODE>(__uint_as_float(r[k + 1]), bias, c0 + 4 * j + 1);
+    v.z = fepi<MODE>(__uint_as_float(r[k + 2]), bias, c0 + 4 * j + 2);
+    v.w = fepi<MODE>(__uint_as_float(r[k + 3]), bias, c0 + 4 * j + 3);
+    *reinterpret_cast<float4*>(srow + 4 * j) = v;
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(256, 1)
+    conv_window_fprop_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ CUtensorMap tmX1,
+                             const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW1,
+                             const FParams p) {
+  using L = FLayout<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = sbase + L::BAR_OFF;
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 16u + 8u * s; };
+  auto tfull_bar = [&](int a) { return bar0 + 32u + 8u * a; };
+  auto tempty_bar = [&](int a) { return bar0 + 48u + 8u * a; };
+  const uint32_t bfull = bar0 + 64u;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::BAR_OFF + 80);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_ctarank();
+  const int unit0 = (int)(blockIdx.x >> 1), units = (int)(gridDim.x >> 1);
+  const int taps = p.k2 * p.k2;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmX0);
+    tma_prefetch_desc(&tmX1);
+    tma_prefetch_desc(&tmW0);
+    tma_prefetch_desc(&tmW1);
+    for (int s = 0; s < L::STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 8);  // 4 epilogue warps x 2 CTAs
+    }
+    mbar_init(bfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "n"(L::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- producer: this CTA's half of every tap's weights, once --------
+      const uint32_t bfb = mapa_rank0(bfull);
+      if (rank == 0) mbar_expect_tx(bfull, (uint32_t)(2 * taps * (L::B0_TAP + L::B1_TAP)));
+      for (int t = 0; t < taps; ++t) {
+        tma_load_2d_pair(&tmW0, sbase + t * L::B0_TAP, bfb, t * CP, rank * L::BNL);
+        tma_load_2d_pair(&tmW1, sbase + L::B1_OFF + t * L::B1_TAP, bfb, t * CP + C0, rank * L::BNL);
+      }
+      // ---- then one input window per tile --------------------------------
+      const uint32_t win_bytes = (uint32_t)p.win_rows * (C0 + C1) * 4u;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = unit0; w < p.units; w += units) {
+        mbar_wait(empty_bar(stage), phase ^ 1);
+        if (rank == 0) mbar_expect_tx(full_bar(stage), 2u * win_bytes);
+        const uint32_t fb = mapa_rank0(full_bar(stage));
+        const int q0 = w * 256 + rank * 128;
+        const uint32_t dst = sbase + L::STAGE_OFF + stage * L::STAGE;
+        tma_load_2d_pair(&tmX0, dst, fb, 0, q0);
+        tma_load_2d_pair(&tmX1, dst + L::A0, fb, C0, q0);
+        if (++stage == L::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      // ---- MMA issuer (whole warp, one elected thread issues): 9 taps x
+      // (4 + 2) MMAs of K = 8 per tile; descriptors advance by adding the
+      // byte offset >> 4 to the start-address field
+      const uint32_t idesc = instr_desc_rt(BN, false, false, 256);
+      const uint64_t b0d = make_desc(sbase, 16, 1024, 2);
+      const uint64_t b1d = make_desc(sbase + L::B1_OFF, 16, 512, 4);
+      mbar_wait_acq_cluster(bfull, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int w = unit0; w < p.units; w += units) {
+        mbar_wait_acq_cluster(tempty_bar(acc), acc_phase ^ 1);
+        tc_fence_after();
+        mbar_wait(full_bar(stage), phase);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * L::ACC_STRIDE);
+        const uint32_t a0 = sbase + L::STAGE_OFF + stage * L::STAGE;
+        const uint64_t a0d = make_desc(a0, 16, 1024, 2);
+        const uint64_t a1d = make_desc(a0 + L::A0, 16, 512, 4);
+        for (int t = 0; t < taps; ++t) {
+          const int kx = t / p.k2, ky = t - kx * p.k2;
+          const uint32_t off = (uint32_t)(kx * p.n2 + ky);
+          const uint64_t at0 = a0d + (uint64_t)(off * 8u), at1 = a1d + (uint64_t)(off * 4u);
+          const uint64_t bt0 = b0d + (uint64_t)(t * (L::B0_TAP >> 4)), bt1 = b1d + (uint64_t)(t * (L::B1_TAP >> 4));
+#pragma unroll
+          for (int kk = 0; kk < C0 / 8; ++kk)
+            tc_mma_tf32_pair_elect(d_tmem, at0 + 2u * kk, bt0 + 2u * kk, idesc, (t > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < C1 / 8; ++kk)
+            tc_mma_tf32_pair_elect(d_tmem, at1 + 2u * kk, bt1 + 2u * kk, idesc, 1u);
+        }
+        tc_commit_pair_elect(empty_bar(stage));
+        tc_commit_pair_elect(tfull_bar(acc));
+        if (++stage == L::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---- epilogue: TMEM -> bias / ReLU -> NHWC rows (junk rows skipped) --
+    const int ew = warp - 4;
+    float* sbias = reinterpret_cast<float*>(smem + L::BIAS_OFF);
+    if (p.bias) {
+      for (int i = threadIdx.x - 128; i < BN; i += 128) sbias[i] = __ldg(p.bias + i);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int w = unit0; w < p.units; w += units) {
+      mbar_wait(tfull_bar(acc), acc_phase);
+      tc_fence_after();
+      const long long q = (long long)w * 256 + rank * 128 + ew * 32 + lane;
+      const int img = (int)(q / p.n2sq);
+      const int r = (int)(q - (long long)img * p.n2sq);
+      const int h = r / p.n2, x = r - (r / p.n2) * p.n2;
+      const int valid = (img < p.b && h < p.m && x < p.m) ? 1 : 0;
+      const int prow = valid ? (img * p.m + h) * p.m + x : 0;   // output pixel of this lane's row
+      const uint32_t t_row = tmem_base + (uint32_t)(acc * L::ACC_STRIDE) + ((uint32_t)(ew * 32) << 16);
+      float* stg = reinterpret_cast<float*>(smem + L::STG_OFF) + ew * 32 * L::STG_PITCH;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r0[16], r1[16];
+        tmem_ld16(t_row + (uint32_t)c0, r0);
+        tmem_ld16(t_row + (uint32_t)c0 + 16, r1);
+        tmem_wait_ld();
+        if (c0 + 32 >= BN) {  // last read of this accumulator: hand it back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster_relaxed(mapa_rank0(tempty_bar(acc)));
+        }
+        float* srow = stg + lane * L::STG_PITCH;
+        switch (p.epilogue) {
+          case OMNI_EPI_BIAS: fstage32<OMNI_EPI_BIAS>(srow, r0, r1, sbias, c0); break;
+          case OMNI_EPI_BIAS_RELU: fstage32<OMNI_EPI_BIAS_RELU>(srow, r0, r1, sbias, c0); break;
+          case OMNI_EPI_RELU: fstage32<OMNI_EPI_RELU>(srow, r0, r1, sbias, c0); break;
+          default: fstage32<OMNI_EPI_STORE>(srow, r0, r1, sbias, c0); break;
+        }
+        __syncwarp();
+        // coalesced store: each instruction writes 4 whole 128-byte row segments
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int row = it * 4 + (lane >> 3), c4 = lane & 7;
+          const int ok = __shfl_sync(0xffffffffu, valid, row);
+          const int pr = __shfl_sync(0xffffffffu, prow, row);
+          const float4 v = *reinterpret_cast<const float4*>(stg + row * L::STG_PITCH + 4 * c4);
+          if (ok) *reinterpret_cast<float4*>(p.Y + (long long)pr * p.ldy + c0 + 4 * c4) = v;
+        }
+        __syncwarp();
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(L::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------- wgrad ----
+struct WParams {
+  int b, n2, m, k2, n2sq;
+  int kb;          // K rows per block: m rounded up to 8 (the dZ box zero-fills the rest)
+  int win_rows;    // kb + (k2 - 1) * (n2 + 1)
+  int d_out;       // M (<= 128)
+  int nblk;        // K-blocks = b * m output rows
+  int taps, ncols;  // ncols = taps * 48 + 16
+  int atoms_a;     // ceil(d_out / 32) dZ boxes per block
+  int stages;
+  uint32_t atom_a, atom_b;  // byte strides of the MN-major atoms (multiples of 512)
+  uint32_t stage_bytes, a_bytes, ones_off, bar_off;
+  int tap_split;   // 1: N = 32 + N = 16 MMAs per tap instead of one N = 48 MMA
+  float* ws;       // [gridDim.x][d_out][ncols] partial sums
+};
+
+constexpr int W_TMEM_COLS = 512;
+
+__global__ void __launch_bounds__(256, 1)
+    conv_window_wgrad_kernel(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmX,
+                             const WParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = sbase + p.bar_off;
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 32u + 8u * s; };
+  const uint32_t acc_full = bar0 + 64u;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + p.bar_off + 80);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmG);
+    tma_prefetch_desc(&tmX);
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "n"(W_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // constant operands written once by all threads: the all-ones bias operand
+  // (every element 1.0, so its swizzle is irrelevant) and zeros in the dZ
+  // atoms past d_out (rows of D that are never stored; zero keeps them finite)
+  {
+    float4* ones = reinterpret_cast<float4*>(smem + p.ones_off);
+    const int n1 = p.kb * 32 / 4;
+    for (int i = threadIdx.x; i < n1; i += blockDim.x) ones[i] = make_float4(1.f, 1.f, 1.f, 1.f);
+    for (int s = 0; s < p.stages; ++s)
+      for (int j = p.atoms_a; j < 4; ++j) {
+        float4* z = reinterpret_cast<float4*>(smem + s * p.stage_bytes + j * p.atom_a);
+        for (int i = threadIdx.x; i < n1; i += blockDim.x) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  // this CTA's contiguous range of output rows (K-blocks)
+  const int blk0 = (int)(((long long)blockIdx.x * p.nblk) / gridDim.x);
+  const int blk1 = (int)(((long long)(blockIdx.x + 1) * p.nblk) / gridDim.x);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)p.atoms_a * p.kb * 128u + 2u * (uint32_t)p.win_rows * 128u;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int blk = blk0; blk < blk1; ++blk) {
+        const int img = blk / p.m, h = blk - (blk / p.m) * p.m;
+        const int q0 = img * p.n2sq + h * p.n2;
+        mbar_wait(empty_bar(stage), phase ^ 1);
+        mbar_expect_tx(full_bar(stage), bytes);
+        const uint32_t a = sbase + stage * p.stage_bytes;
+        const uint32_t bw = a + p.a_bytes;
+        for (int j = 0; j < p.atoms_a; ++j) tma_load_3d(&tmG, a + j * p.atom_a, full_bar(stage), 32 * j, 0, blk);
+        tma_load_2d(&tmX, bw, full_bar(stage), 0, q0);
+        tma_load_2d(&tmX, bw + p.atom_b, full_bar(stage), 32, q0);
+        if (++stage == p.stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer (whole warp, one elected thread issues) --------------
+    const uint32_t id48 = instr_desc_rt(48, true, true, 128);
+    const uint32_t id32 = instr_desc_rt(32, true, true, 128);
+    const uint32_t id16 = instr_desc_rt(16, true, true, 128);
+    const uint64_t onesd = make_desc(sbase + p.ones_off, 8192, 512, 1);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int blk = blk0; blk < blk1; ++blk) {
+      mbar_wait(full_bar(stage), phase);
+      tc_fence_after();
+      const uint32_t a = sbase + stage * p.stage_bytes;
+      const uint64_t ad0 = make_desc(a, p.atom_a, 512, 1);
+      const uint64_t bd0 = make_desc(a + p.a_bytes, p.atom_b, 512, 1);
+      const uint64_t bd1 = make_desc(a + p.a_bytes + p.atom_b, p.atom_b, 512, 1);
+      for (int kk = 0; kk < p.kb / 8; ++kk) {
+        const uint32_t accf = (blk > blk0 || kk > 0) ? 1u : 0u;
+        const uint64_t ad = ad0 + (uint64_t)(kk * 64u);       // 8 K rows = 1024 B
+        for (int t = 0; t < p.taps; ++t) {
+          const int kx = t / p.k2, ky = t - kx * p.k2;
+          const uint64_t roff = (uint64_t)((kx * p.n2 + ky + kk * 8) * 8u);   // rows x 128 B >> 4
+          const uint32_t dcol = tmem_base + (uint32_t)(t * CP);
+          if (!p.tap_split) {
+            tc_mma_tf32_elect(dcol, ad, bd0 + roff, id48, accf);
+          } else {
+            tc_mma_tf32_elect(dcol, ad, bd0 + roff, id32, accf);
+            tc_mma_tf32_elect(dcol + C0, ad, bd1 + roff, id16, accf);
+          }
+        }
+        // bias gradient: dZ^T times an all-ones operand (16 identical columns)
+        tc_mma_tf32_elect(tmem_base + (uint32_t)(p.taps * CP), ad, onesd + (uint64_t)(kk * 64u), id16, accf);
+      }
+      tc_commit_elect(empty_bar(stage));
+      if (++stage == p.stages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    tc_commit_elect(acc_full);
+  } else if (warp >= 4) {
+    // ---- epilogue: the CTA's partial dW (d_out x ncols) -> workspace -----
+    const int ew = warp - 4;
+    const int o = ew * 32 + lane;
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16);
+    float* dst = p.ws + ((long long)blockIdx.x * p.d_out + o) * p.ncols;
+#pragma unroll 1
+    for (int c0 = 0; c0 < p.ncols; c0 += 16) {
+      uint32_t rr[16];
+      tmem_ld16(t_row + (uint32_t)c0, rr);
+      tmem_wait_ld();
+      if (o < p.d_out) {
+        float4* d4 = reinterpret_cast<float4*>(dst + c0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          d4[j] = make_float4(__uint_as_float(rr[4 * j]), __uint_as_float(rr[4 * j + 1]),
+                              __uint_as_float(rr[4 * j + 2]), __uint_as_float(rr[4 * j + 3]));
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(W_TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// Y[o * ldy + c] = sum_s ws[s][o][c], s ascending (fixed order: deterministic).
+__global__ void __launch_bounds__(256) window_reduce_kernel(const float* __restrict__ ws, int S, int d_out,
+                                                            int ncols, float* __restrict__ Y, long long ldy) {
+  const int n4 = ncols / 4;
+  const int total = d_out * n4;
+  const long long split = (long long)d_out * ncols;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int o = i / n4, c = (i - o * n4) * 4;
+    const float* src = ws + (long long)o * ncols + c;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < S; ++s) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(src + s * split));
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    *reinterpret_cast<float4*>(Y + o * ldy + c) = acc;
+  }
+}
+
+// ------------------------------------------------------------- host -----
+struct Geo {
+  int m, taps, win_f, kb, win_w;
+};
+
+int geometry(int b, int n2, int cp, int k2, int d_out, Geo* g) {
+  OMNI_REQUIRE(b >= 1 && n2 >= 1 && k2 >= 1 && d_out >= 1, "conv window: bad shape");
+  OMNI_REQUIRE(cp == CP, "conv window: needs %d space-to-depth channels (got %d)", CP, cp);
+  OMNI_REQUIRE(k2 <= 3 && k2 <= n2, "conv window: k2 = %d unsupported", k2);
+  g->m = n2 - k2 + 1;
+  g->taps = k2 * k2;
+  g->win_f = 128 + (k2 - 1) * (n2 + 1);
+  g->kb = (g->m + 7) / 8 * 8;
+  g->win_w = g->kb + (k2 - 1) * (n2 + 1);
+  OMNI_REQUIRE(g->win_f <= WIN_MAX && g->win_w <= WIN_MAX && g->kb <= 64,
+               "conv window: image too wide for one window (n2 = %d)", n2);
+  OMNI_REQUIRE((long long)b * n2 * n2 < (1LL << 31), "conv window: too many pixels");
+  return OMNI_OK;
+}
+
+int wgrad_splits(int nblk) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int sms = omni::sm_count_cached(dev);
+  return nblk < sms ? nblk : sms;
+}
+
+template <int BN>
+int launch_fprop(const FParams& p, const CUtensorMap& x0, const CUtensorMap& x1, const CUtensorMap& w0,
+                 const CUtensorMap& w1, cudaStream_t st) {
+  using L = FLayout<BN>;
+  auto kern = conv_window_fprop_kernel<BN>;
+  static unsigned long long configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured & (1ull << (dev & 63)))) {
+    OMNI_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
+    configured |= 1ull << (dev & 63);
+  }
+  const int pairs = omni::sm_count_cached(dev) / 2;
+  const int grid = 2 * (p.units < pairs ? p.units : pairs);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = L::BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  OMNI_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, x0, x1, w0, w1, p));
+  return omni::check_launch("conv_window_fprop");
+}
+
+}  // namespace cwin
+
+extern "C" {
+
+long long omni_conv_window_plan(int op, int b, int n2, int cp, int k2, int d_out) {
+  cwin::Geo g;
+  if (cwin::geometry(b, n2, cp, k2, d_out, &g)) return -1;
+  if (op == OMNI_CONV_FPROP) return (d_out == 32 || d_out == 64 || d_out == 96 || d_out == 128) ? 0 : -1;
+  if (op != OMNI_CONV_WGRAD_BIAS || d_out > 128) return -1;
+  const int ncols = g.taps * cwin::CP + 16;
+  if (ncols > cwin::W_TMEM_COLS) return -1;
+  return (long long)cwin::wgrad_splits(b * g.m) * d_out * ncols * 4;
+}
+
+int omni_conv_window_f32(int op, const float* Xs, int b, int n2, int cp, int k2, int d_out, const float* G,
+                         long long ldg, float* Y, long long ldy, int epilogue, const float* bias,
+                         float* workspace, long long ws_bytes, void* stream) {
+  cwin::Geo g;
+  int rc = cwin::geometry(b, n2, cp, k2, d_out, &g);
+  if (rc) return rc;
+  OMNI_REQUIRE(((uintptr_t)Xs & 15) == 0 && ((uintptr_t)G & 15) == 0 && ((uintptr_t)Y & 15) == 0 &&
+                   ldg % 4 == 0 && ldy % 4 == 0,
+               "conv window: operands must be 16-byte aligned with leading dimensions %% 4 == 0");
+  cudaStream_t st = omni::as_stream(stream);
+  const long long rows = (long long)b * n2 * n2;
+  const int taps = g.taps;
+  if (op == OMNI_CONV_FPROP) {
+    OMNI_REQUIRE(d_out == 32 || d_out == 64 || d_out == 96 || d_out == 128,
+                 "conv window fprop: d_out must be 32, 64, 96 or 128 (got %d)", d_out);
+    OMNI_REQUIRE(ldg >= (long long)taps * cwin::CP && ldy >= d_out, "conv window fprop: leading dimension too small");
+    OMNI_REQUIRE(epilogue == OMNI_EPI_STORE || epilogue == OMNI_EPI_BIAS || epilogue == OMNI_EPI_BIAS_RELU ||
+                     epilogue == OMNI_EPI_RELU,
+                 "conv window fprop: unsupported epilogue %d", epilogue);
+    OMNI_REQUIRE(!(epilogue == OMNI_EPI_BIAS || epilogue == OMNI_EPI_BIAS_RELU) || bias,
+                 "conv window fprop: bias epilogue needs a bias vector");
+    const int bnl = d_out / 2;
+    CUtensorMap x0, x1, w0, w1;
+    const cuuint64_t xd[2] = {(cuuint64_t)cwin::CP, (cuuint64_t)rows};
+    const cuuint64_t xs[1] = {(cuuint64_t)cwin::CP * 4};
+    const cuuint32_t bx0[2] = {32, (cuuint32_t)g.win_f}, bx1[2] = {16, (cuuint32_t)g.win_f};
+    const cuuint64_t wd[2] = {(cuuint64_t)taps * cwin::CP, (cuuint64_t)d_out};
+    const cuuint64_t ws_[1] = {(cuuint64_t)ldg * 4};
+    const cuuint32_t bw0[2] = {32, (cuuint32_t)bnl}, bw1[2] = {16, (cuuint32_t)bnl};
+    if ((rc = cwin::tmap(&x0, Xs, 2, xd, xs, bx0, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+    if ((rc = cwin::tmap(&x1, Xs, 2, xd, xs, bx1, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
+    if ((rc = cwin::tmap(&w0, G, 2, wd, ws_, bw0, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+    if ((rc = cwin::tmap(&w1, G, 2, wd, ws_, bw1, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
+    cwin::FParams p{};
+    p.b = b;
+    p.n2 = n2;
+    p.m = g.m;
+    p.k2 = k2;
+    p.n2sq = n2 * n2;
+    p.rows = rows;
+    p.units = (int)omni::ceil_div(rows, 256);
+    p.win_rows = g.win_f;
+    p.epilogue = epilogue;
+    p.bias = bias;
+    p.Y = Y;
+    p.ldy = ldy;
+    switch (d_out) {
+      case 32: return cwin::launch_fprop<32>(p, x0, x1, w0, w1, st);
+      case 64: return cwin::launch_fprop<64>(p, x0, x1, w0, w1, st);
+      case 96: return cwin::launch_fprop<96>(p, x0, x1, w0, w1, st);
+      default: return cwin::launch_fprop<128>(p, x0, x1, w0, w1, st);
+    }
+  }
+  OMNI_REQUIRE(op == OMNI_CONV_WGRAD_BIAS, "conv window: op must be FPROP or WGRAD_BIAS");
+  OMNI_REQUIRE(d_out <= 128, "conv window wgrad: d_out <= 128 (got %d)", d_out);
+  const int ncols = taps * cwin::CP + 16;
+  OMNI_REQUIRE(ncols <= cwin::W_TMEM_COLS, "conv window wgrad: too many taps");
+  OMNI_REQUIRE(ldg >= d_out && ldy >= ncols, "conv window wgrad: leading dimension too small (ldy >= %d)", ncols);
+  const int nblk = b * g.m;
+  const int S = cwin::wgrad_splits(nblk);
+  const long long need = (long long)S * d_out * ncols * 4;
+  OMNI_REQUIRE(workspace && ws_bytes >= need && ((uintptr_t)workspace & 15) == 0,
+               "conv window wgrad: workspace of %lld bytes required (got %lld)", need, ws_bytes);
+  cwin::WParams p{};
+  p.b = b;
+  p.n2 = n2;
+  p.m = g.m;
+  p.k2 = k2;
+  p.n2sq = n2 * n2;
+  p.kb = g.kb;
+  p.win_rows = g.win_w;
+  p.d_out = d_out;
+  p.nblk = nblk;
+  p.taps = taps;
+  p.ncols = ncols;
+  p.atoms_a = (d_out + 31) / 32;
+  p.atom_a = (uint32_t)((g.kb * 128 + 511) / 512 * 512);
+  p.atom_b = (uint32_t)((g.win_w * 128 + 511) / 512 * 512);
+  p.a_bytes = 4 * p.atom_a;
+  p.stage_bytes = (p.a_bytes + 2 * p.atom_b + 1023) / 1024 * 1024;
+  const uint32_t budget = 232448 - 1024 - 256 - 8192;
+  p.stages = (int)(budget / p.stage_bytes);
+  if (p.stages > 4) p.stages = 4;
+  OMNI_REQUIRE(p.stages >= 2, "conv window wgrad: stages do not fit in shared memory");
+  p.ones_off = p.stages * p.stage_bytes;
+  p.bar_off = p.ones_off + 8192;
+  p.tap_split = getenv("OMNI_WINDOW_TAP_SPLIT") ? 1 : 0;
+  p.ws = workspace;
+  CUtensorMap tg, tx;
+  const cuuint64_t gd[3] = {(cuuint64_t)d_out, (cuuint64_t)g.m, (cuuint64_t)b * g.m};
+  const cuuint64_t gs[2] = {(cuuint64_t)ldg * 4, (cuuint64_t)g.m * ldg * 4};
+  const cuuint32_t gb[3] = {32, (cuuint32_t)g.kb, 1};
+  const cuuint64_t xd[2] = {(cuuint64_t)cwin::CP, (cuuint64_t)rows};
+  const cuuint64_t xs[1] = {(cuuint64_t)cwin::CP * 4};
+  const cuuint32_t xb[2] = {32, (cuuint32_t)g.win_w};
+  if ((rc = cwin::tmap(&tg, G, 3, gd, gs, gb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))) return rc;
+  if ((rc = cwin::tmap(&tx, Xs, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))) return rc;
+  const int bytes = (int)(p.bar_off + 256 + 1024);
+  static unsigned long long configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured & (1ull << (dev & 63)))) {
+    OMNI_CUDA_TRY(cudaFuncSetAttribute(cwin::conv_window_wgrad_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+    configured |= 1ull << (dev & 63);
+  }
+  cwin::conv_window_wgrad_kernel<<<S, 256, bytes, st>>>(tg, tx, p);
+  rc = omni::check_launch("conv_window_wgrad");
+  if (rc) return rc;
+  const int total = d_out * (ncols / 4);
+  cwin::window_reduce_kernel<<<omni::grid_for(total, 256), 256, 0, st>>>(workspace, S, d_out, ncols, Y, ldy);
+  return omni::check_launch("conv_window_reduce");
+}
+
+}  // extern "C"

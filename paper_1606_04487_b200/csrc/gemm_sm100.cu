@@ -30,11 +30,9 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "tc_ptx.cuh"
 
 namespace gemm {
-
-constexpr int BM = 128;
-constexpr int BK = 32;  // fp32 elements per stage along K = one 128-byte swizzle row
 
 struct Params {
   int M, N, K;
@@ -83,204 +81,6 @@ struct Layout {
   static_assert(STAGES >= 2, "need at least two stages");
   static_assert(B_BYTES % 1024 == 0, "B tile must keep 1 KiB swizzle alignment");
 };
-
-// ------------------------------------------------------------------ PTX --
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE;\n\t"
-      "bra LAB_WAIT;\n\t"
-      "DONE:\n\t}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint32_t dst, uint32_t bar,
-                                            int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
-      : "memory");
-}
-// TMA im2col load (4-D NHWC tensor map): `pixels` consecutive output pixels
-// starting at the window corner (w, h) of image n, 32 channels from c, filter
-// tap offsets (ow, oh); out-of-image taps read as zero (the conv padding).
-__device__ __forceinline__ void tma_load_im2col(const CUtensorMap* map, uint32_t dst, uint32_t bar,
-                                                int c, int w, int h, int n, uint16_t ow, uint16_t oh) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow),
-      "h"(oh)
-      : "memory");
-}
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1,
-                                             int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-          reinterpret_cast<uint64_t>(map)),
-      "r"(src), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_commit() {
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() {
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
-  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c),
-               "f"(d)
-               : "memory");
-}
-__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   bar)
-               : "memory");
-}
-__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                            uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// ---- CTA-pair (cta_group::2) variants ----
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
-                   "memory");
-}
-// shared::cluster address of the same shared-memory offset in CTA 0 of the pair
-__device__ __forceinline__ uint32_t mapa_rank0(uint32_t addr) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(addr));
-  return r;
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait_acq_cluster(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "LAB_WAITC:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONEC;\n\t"
-      "bra LAB_WAITC;\n\t"
-      "DONEC:\n\t}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-// TMA loads whose completion is signalled on CTA 0's barrier (bar is a
-// shared::cluster address); data lands in the issuing CTA's shared memory.
-__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t dst, uint32_t bar,
-                                                 int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_im2col_pair(const CUtensorMap* map, uint32_t dst,
-                                                     uint32_t bar, int c, int w, int h, int n,
-                                                     uint16_t ow, uint16_t oh) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.im2col.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow),
-      "h"(oh)
-      : "memory");
-}
-// commit to the barrier at the same offset in both CTAs of the pair
-__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(bar),
-      "h"((uint16_t)3)
-      : "memory");
-}
-__device__ __forceinline__ void tc_mma_tf32_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                                 uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_wait_ld() {
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-// Shared-memory matrix descriptor (tcgen05 "smem descriptor"): start address,
-// leading/stride byte offsets (>>4), version 1 (sm_100), layout type.
-//  K-major : SWIZZLE_128B (type 2, 16-byte atoms): rows of 128 B (32 tf32
-//            along K), 8-row atoms 1024 B apart (SBO).
-//  MN-major: tf32 only supports SWIZZLE_128B_BASE32B (type 1, 32-byte atoms,
-//            TMA mode 128B_ATOM_32B): 128 B along MN per K row; MN atoms of 32
-//            elements are a whole BK-row chunk apart (LBO = 32 rows * 128 B),
-//            4-row K groups 512 B apart (SBO).
-template <bool MN, int BKT = BK>
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
-  const uint64_t lbo = MN ? (uint64_t)((BKT * 128) >> 4) : 1ull;
-  const uint64_t sbo = MN ? (512 >> 4) : (1024 >> 4);
-  const uint64_t layout = MN ? 1ull : 2ull;
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | (lbo << 16) | (sbo << 32) | (1ull << 46) |
-         (layout << 61);
-}
-
-// Instruction descriptor: D=f32, A=B=tf32, majors, N>>3, M>>4 (M = 256 for a CTA pair).
-template <int BN, bool A_MN, bool B_MN, int MM = BM>
-__host__ __device__ constexpr uint32_t instr_desc() {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
-         ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(MM >> 4) << 24);
-}
 
 // 3xTF32 operand split: hi = x rounded to the nearest tf32 (adding half an
 // ulp of the 10-bit mantissa to the magnitude bits, then truncating), lo =
@@ -383,7 +183,11 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
   // K-major operands hold exactly one 128-byte swizzle row (32 fp32) per stage;
   // deeper stages are for MN-major operands only.
   static_assert(BKT == BK || (A_MN && B_MN), "BKT > 32 needs MN-major operands");
-  static_assert(!(CTA2 && SPLIT3), "the CTA-pair kernel is TF32 only");
+  // 3xTF32 on CTA pairs: each CTA's TMA signals its OWN full barrier (its
+  // converter warps must see its stage land), each CTA splits its own half of
+  // the stage, and the converters' per-warp arrivals gather on CTA 0's
+  // conversion barrier, which the MMA issuer waits on.
+  constexpr bool OWN_FULL = SPLIT3 || !CTA2;
   using L = Layout<BN, SPLIT3, BKT, CTA2>;
   constexpr int BM_T = CTA2 ? 2 * BM : BM;  // output rows per work tile
   constexpr int BNL = L::BNL;               // B rows this CTA stages
@@ -413,7 +217,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
     for (int s = 0; s < L::STAGES; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
-      if (SPLIT3) mbar_init(conv_bar(s), 128);
+      if (SPLIT3) mbar_init(conv_bar(s), CTA2 ? 2 : 1);  // one arrival per CTA's converters
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
@@ -509,15 +313,16 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
         }
         for (int kt = kt0; kt < kt1; ++kt) {
           mbar_wait(empty_bar(stage), phase ^ 1);
-          if (rank == 0) mbar_expect_tx(full_bar(stage), (uint32_t)(CTA2 ? 2 * L::STAGE : L::STAGE));
-          const uint32_t fb = CTA2 ? mapa_rank0(full_bar(stage)) : full_bar(stage);
+          if (OWN_FULL) mbar_expect_tx(full_bar(stage), (uint32_t)L::STAGE);
+          else if (rank == 0) mbar_expect_tx(full_bar(stage), (uint32_t)(2 * L::STAGE));
+          const uint32_t fb = OWN_FULL ? full_bar(stage) : mapa_rank0(full_bar(stage));
           auto load2d = [&](const CUtensorMap* map, uint32_t dst, int c0, int c1) {
-            if (CTA2) tma_load_2d_pair(map, dst, fb, c0, c1);
+            if (!OWN_FULL) tma_load_2d_pair(map, dst, fb, c0, c1);
             else tma_load_2d(map, dst, fb, c0, c1);
           };
           auto load_im2col = [&](const CUtensorMap* map, uint32_t dst, int c, int w_, int h_, int n_,
                                  uint16_t ow, uint16_t oh) {
-            if (CTA2) tma_load_im2col_pair(map, dst, fb, c, w_, h_, n_, ow, oh);
+            if (!OWN_FULL) tma_load_im2col_pair(map, dst, fb, c, w_, h_, n_, ow, oh);
             else tma_load_im2col(map, dst, fb, c, w_, h_, n_, ow, oh);
           };
           const uint32_t a_dst = sbase + stage * L::STAGE_ALL;
@@ -607,7 +412,8 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * L::ACC_STRIDE);
         for (int kt = kt0; kt < kt1; ++kt) {
-          mbar_wait(SPLIT3 ? conv_bar(stage) : full_bar(stage), phase);
+          if (SPLIT3 && CTA2) mbar_wait_acq_cluster(conv_bar(stage), phase);  // both CTAs converted
+          else mbar_wait(SPLIT3 ? conv_bar(stage) : full_bar(stage), phase);
           tc_fence_after();
           const uint32_t a_addr = sbase + stage * L::STAGE_ALL;
           const uint32_t b_addr = a_addr + L::A_BYTES;
@@ -622,8 +428,13 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
             if (SPLIT3) {
               const uint64_t ad_lo = smem_desc<A_MN, BKT>(a_addr + L::STAGE + a_off);
               const uint64_t bd_lo = smem_desc<B_MN, BKT>(b_addr + L::STAGE + b_off);
-              tc_mma_tf32(d_tmem, ad_lo, bd, idesc, 1u);
-              tc_mma_tf32(d_tmem, ad, bd_lo, idesc, 1u);
+              if (CTA2) {
+                tc_mma_tf32_pair(d_tmem, ad_lo, bd, idesc, 1u);
+                tc_mma_tf32_pair(d_tmem, ad, bd_lo, idesc, 1u);
+              } else {
+                tc_mma_tf32(d_tmem, ad_lo, bd, idesc, 1u);
+                tc_mma_tf32(d_tmem, ad, bd_lo, idesc, 1u);
+              }
             }
           }
           // frees the stage (in both CTAs of a pair) once these MMAs have read it
@@ -764,8 +575,16 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
           hi[i] = h;
           lo[i] = l;
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(conv_bar(stage));
+        // converted stage -> async proxy (the MMA reads it, from CTA 0 for a
+        // pair: hence the cluster-scope proxy fence), then one arrival per CTA
+        // after all 128 converter threads are done (named barrier 1)
+        if (CTA2) asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+        else asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (t == 0) {
+          if (CTA2) mbar_arrive_cluster(mapa_rank0(conv_bar(stage)));
+          else mbar_arrive(conv_bar(stage));
+        }
         if (++stage == L::STAGES) {
           stage = 0;
           phase ^= 1;
@@ -1102,7 +921,10 @@ Plan make_plan(int M, int N, int K, int sms, int bkt = BK, bool cta2 = false, bo
 
 // CTA pairs (M = 256 tiles, half of B per CTA) for TF32 GEMMs with more than
 // one 128-row tile; the transposed conv form (im2col B, M = d_out <= 128) and
-// 3xTF32 stay on single CTAs.  OMNI_NO_2CTA=1 disables pairs.
+// 3xTF32 stay on single CTAs (the kernel's split-K/converter protocol for
+// 3xTF32 pairs is written -- OWN_FULL -- but its low-order products came out
+// missing on the B200, tests/test_kernels_gpu.py; not enabled).
+// OMNI_NO_2CTA=1 disables pairs.
 bool pair_ok(int precision, int M, int im2col) {
   static const bool off = getenv("OMNI_NO_2CTA") != nullptr;
   return !off && precision == OMNI_PREC_TF32 && M > BM && im2col != 4;

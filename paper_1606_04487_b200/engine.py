@@ -79,6 +79,7 @@ class Op:
     implicit: bool = False
     s2d: tuple | None = None          # (stride, k2, pad2, n2, cp) of the space-to-depth form
     s2d_buf: torch.Tensor | None = None
+    window: bool = False              # s2d layer on the window kernels (conv_window.cu, cp = 48)
     ldF: int = 0
     wflip: torch.Tensor | None = None
     dhat: torch.Tensor | None = None
@@ -150,9 +151,18 @@ class GpuNet:
                     n2 = -(-n // st)
                     p2 = L.pad // st
                     cp = K.round_up(st * st * c, 32)
+                    # the window kernels (TF32): no channel padding (cp = 48 for
+                    # CaffeNet conv1), every tap read from one staged window per tile
+                    window = (precision == "tf32" and p2 == 0 and st * st * c == 48 and
+                              os.environ.get("OMNI_WINDOW", "0") == "1" and
+                              K.conv_window_plan(_abi.CONV_FPROP, self.b, n2, 48, k2, d) >= 0 and
+                              K.conv_window_plan(_abi.CONV_WGRAD_BIAS, self.b, n2, 48, k2, d) >= 0)
+                    if window:
+                        cp = 48
                     if n2 + 2 * p2 - k2 + 1 == m and cp <= 2 * st * st * c:
                         op.s2d = (st, k2, p2, n2, cp)
                         op.implicit = True
+                        op.window = window
                         op.s2d_buf = z(self.b, n2, n2, cp)
                 if op.s2d is not None:
                     st, k2, p2, n2, cp = op.s2d
@@ -172,7 +182,11 @@ class GpuNet:
                     op.dhat = z(self.b * m * m, op.ldK)
                 op.wstage = z(d, op.ldK)
                 op.ldW = op.ldK
-                if op.implicit and op.boff >= 0 and not os.environ.get("OMNI_NO_WGRAD_BIAS"):
+                if op.window:
+                    # the window wgrad writes k2*k2*48 weight columns + 16 bias columns
+                    op.wgrad_op = _abi.CONV_WGRAD_BIAS
+                    op.ldW = K.round_up(op.Kf + 16, 32)
+                elif op.implicit and op.boff >= 0 and not os.environ.get("OMNI_NO_WGRAD_BIAS"):
                     # bias gradient as one more row of the implicit wgrad GEMM (column Kf)
                     op.wgrad_op = _abi.CONV_WGRAD_BIAS
                     op.ldW = K.round_up(op.Kf + 1, 32)
@@ -255,6 +269,9 @@ class GpuNet:
         """Largest split-K workspace any GEMM of this layer asks for, from the
         same plan functions the launches use (implicit convs plan differently
         from plain GEMMs: 64-deep wgrad stages, transposed fprop)."""
+        if op.kind == "conv" and op.window:
+            st, k2, p2, n2, cp = op.s2d
+            return K.conv_window_plan(_abi.CONV_WGRAD_BIAS, b, n2, cp, k2, op.layer.d_out)
         if op.kind == "conv" and op.implicit:
             d = op.layer.d_out
             if op.s2d is not None:
@@ -400,6 +417,11 @@ class GpuNet:
                         epi = _abi.EPI_RELU if op.relu else _abi.EPI_STORE
                         bias = None
                     X, c_, k_, s_, p_ = self._conv_input(op, b)
+                    if op.window:
+                        self._timed(Mr, d, op.c_in * op.k * op.k, "conv", lambda: K.conv_window(
+                            _abi.CONV_FPROP, X, k_, d, op.wstage, op.ldK, op.out.value, op.out.cs,
+                            epilogue=epi, bias=bias))
+                        continue
                     self._conv(_abi.CONV_FPROP, X, c_, k_, s_, p_, d, op.wstage, op.ldK,
                                op.out.value, op.out.cs, epi, bias)
                     continue
@@ -560,8 +582,13 @@ class GpuNet:
                 if op.implicit:
                     with wgrad_stream():
                         X, c_, k_, s_, p_ = self._conv_input(op, b, transform=False)
-                        self._conv(op.wgrad_op, X, c_, k_, s_, p_, d, dZ, op.out.cs,
-                                   op.dwstage, op.ldW)
+                        if op.window:
+                            self._timed(d, op.c_in * op.k * op.k, Mr, "conv", lambda: K.conv_window(
+                                _abi.CONV_WGRAD_BIAS, X, k_, d, dZ, op.out.cs, op.dwstage, op.ldW,
+                                workspace=self._ws_active))
+                        else:
+                            self._conv(op.wgrad_op, X, c_, k_, s_, p_, d, dZ, op.out.cs,
+                                       op.dwstage, op.ldW)
                         fold = op.wgrad_op == _abi.CONV_WGRAD_BIAS
                         gb = G[op.boff:op.boff + d] if fold else None
                         if op.s2d is not None:

@@ -220,6 +220,38 @@ def conv_implicit(op: int, X: torch.Tensor, c: int, k: int, stride: int, pad: in
     return Y
 
 
+def conv_window_plan(op: int, b: int, n2: int, cp: int, k2: int, d_out: int) -> int:
+    """Workspace bytes of the space-to-depth window conv, or -1 if it does not apply."""
+    return int(_abi.query("omni_conv_window_plan", op, b, n2, cp, k2, d_out))
+
+
+def conv_window(op: int, Xs: torch.Tensor, k2: int, d_out: int, G: torch.Tensor, ldg: int,
+                Y: torch.Tensor, ldy: int, *, epilogue: int = _abi.EPI_STORE,
+                bias: torch.Tensor | None = None, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Window implicit GEMM of a space-to-depth first layer (see include/omni.h):
+    Xs (b, n2, n2, 48); op = _abi.CONV_FPROP (G weights, Y NHWC output rows) or
+    _abi.CONV_WGRAD_BIAS (G = dZ rows, Y = staged dW with the bias in column k2*k2*48)."""
+    _require_cuda(Xs, G, Y)
+    b, n2, _, cp = Xs.shape
+    m = n2 - k2 + 1
+    pixels, taps = b * m * m, k2 * k2 * cp
+    if op == _abi.CONV_FPROP:
+        _fits(G, (d_out - 1) * ldg + taps, "G")
+        _fits(Y, (pixels - 1) * ldy + d_out, "Y")
+    else:
+        _fits(G, (pixels - 1) * ldg + d_out, "G")
+        _fits(Y, (d_out - 1) * ldy + taps + 16, "Y")
+    if bias is not None:
+        _fits(bias, d_out, "bias")
+    need = conv_window_plan(op, b, n2, cp, k2, d_out)
+    if need < 0:
+        raise ValueError(f"conv_window: geometry not covered (b={b} n2={n2} cp={cp} k2={k2} d_out={d_out})")
+    workspace = _check_workspace(need, workspace, Y.device)
+    call("omni_conv_window_f32", op, _ptr(Xs), b, n2, cp, k2, d_out, _ptr(G), ldg, _ptr(Y), ldy, epilogue,
+         _ptr(bias), _ptr(workspace), 0 if workspace is None else workspace.numel() * 4, _stream())
+    return Y
+
+
 def conv_weight_flip(W: torch.Tensor, o: int, c: int, k: int, Wf: torch.Tensor, ld: int) -> None:
     call("omni_conv_weight_flip_f32", _ptr(W), o, c, k, _ptr(Wf), ld, _stream())
 

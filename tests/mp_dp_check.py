@@ -1,13 +1,16 @@
 """Data-parallel DeviceSession (N ranks, per-layer async allreduce + layer-wise
-update inside the backward) == the synchronous update on the mean gradient.
+update inside the backward; or the peer-memory fused reduce + update; or
+merged FC) == the synchronous update on the mean gradient, replayed by the
+float64 CPU ORACLE.
 
-    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/dp_check.py
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tests/mp_dp_check.py [net] [p2p|merged]
 
-Every rank steps on its own batch; afterwards rank 0 recomputes each rank's
-gradient with the same engine (same kernels, same batches) step by step and
-applies V = mu V - eta (mean_r G_r + lam W); W += V in float64.  Prints the
-normwise difference of the final W (fp32 session vs fp64 replay of the same
-fp32 gradients).
+Every rank steps on its own batch; afterwards rank 0 replays the run on the
+host: each rank's batch gradient from oracle/refcnn.grad (float64, the
+reference's algorithm, problems.py:239-269) at the replayed W, the mean over
+ranks, and V = mu V - eta (mean_r G_r + lam W); W += V (sgd.py:92-101).  The
+fp32 session must match that replay (final W normwise <= 1e-4, the learned
+update W_T - W_0 and V_T <= 1e-3 in 3xTF32).
 """
 import os
 import sys
@@ -17,6 +20,7 @@ import torch
 import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import refcnn as R  # noqa: E402
 from paper_1606_04487_b200.problems import CNNProblem, DeviceBatch  # noqa: E402
 from paper_1606_04487_b200.sgd import Hyperparams, SGDState  # noqa: E402
 
@@ -49,32 +53,23 @@ def main():
     if p2p:                            # one owner computes each element: bit-identical W
         assert len(set(Ws)) == 1, Ws
     if rank == 0:
-        W = np.asarray(state.W, dtype=np.float64).copy()
-        V = np.zeros_like(W)
-        eng = prob.engine(b)
-        for t in range(steps):
-            Wd = torch.from_numpy(W.astype(np.float32)).to(dev)
-            G = np.zeros_like(W)
-            for r in range(world):
-                eng.gather_batch(prob.data, prob.data_labels, torch.from_numpy(idx[t][r]).to(dev))
-                _, g = eng.loss_and_grad(Wd, b)
-                G += g.double().cpu().numpy() / world
-            V = hp.mu * V - hp.eta * (G + hp.lam * W)
-            W = W + V
+        W0 = np.asarray(state.W, dtype=np.float32).astype(np.float64)
+        W, V = W0.copy(), np.zeros_like(W0)
+        images = prob.images.astype(np.float32).astype(np.float64)
+        L = prob.net.to_dicts()
+        with R.gemm_impl("blas"):
+            for t in range(steps):
+                G = np.zeros_like(W)
+                for r in range(world):
+                    ix = idx[t][r]
+                    G += R.grad(L, prob.net.in_channels, prob.net.in_size, W, images[ix], prob.labels[ix]) / world
+                W, V = R.sgd_step(W, V, G, W, hp.eta, hp.mu, hp.lam)
         rel = float(np.linalg.norm(W_dp - W) / np.linalg.norm(W))
+        reld = float(np.linalg.norm((W_dp - W0) - (W - W0)) / np.linalg.norm(W - W0))
         relv = float(np.linalg.norm(st.V - V) / np.linalg.norm(V))
-        print(f"{net}: N={world} data-parallel{' merged-FC' if merged else ' p2p' if p2p else ''} session vs replay: "
-              f"normwise {rel:.3e}, V {relv:.3e} (last loss {loss:.4f})")
-        worst = []
-        for op in eng.ops:
-            if op.kind in ("conv", "fc"):
-                hi = op.boff + op.layer.d_out if op.boff >= 0 else op.woff + op.wsz
-                for nm, lo, h in (("w", op.woff, op.woff + op.wsz), ("b", op.boff, hi)):
-                    if h > lo >= 0:
-                        e = float(np.linalg.norm(st.V[lo:h] - V[lo:h]) / max(np.linalg.norm(V[lo:h]), 1e-30))
-                        worst.append((e, f"{op.kind}@{op.woff}.{nm}[{h - lo}]"))
-        print("worst V slices:", sorted(worst, reverse=True)[:4])
-        assert rel < 1e-5 and relv < 1e-2, (rel, relv)
+        print(f"{net}: N={world} data-parallel{' merged-FC' if merged else ' p2p' if p2p else ''} session vs "
+              f"oracle replay: W normwise {rel:.3e}, W_T - W_0 {reld:.3e}, V {relv:.3e} (last loss {loss:.4f})")
+        assert rel < 1e-4 and reld < 1e-3 and relv < 1e-3, (rel, reld, relv)
     dist.destroy_process_group()
 
 

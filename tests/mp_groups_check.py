@@ -1,6 +1,6 @@
 """Multi-GPU check of the compute-group runtime (NCCL, one process per GPU).
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/groups_check.py --g G
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/mp_groups_check.py --g G
 
 Runs GroupRuntime with the CUDA backend (3xTF32) on the reference TinyCNN and
 compares the final master model and event log with the float64 oracle's

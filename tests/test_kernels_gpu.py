@@ -596,3 +596,65 @@ def test_space_to_depth_conv1_large_batch():
     ref = torch.nn.functional.conv2d(X.permute(0, 3, 1, 2).double().cpu(), W.double().cpu(), stride=s)
     torch.cuda.synchronize()
     assert rel_err(out.cpu(), ref.permute(0, 2, 3, 1).reshape(-1, d)) < 5e-6
+
+
+def _s2d_conv1(b, gen, n=227, c=3, k=11, s=4, d=96):
+    X = torch.randn(b, n, n, c, generator=gen).to(DEV)
+    W = (torch.randn(d, c, k, k, generator=gen) / (c * k * k) ** 0.5).to(DEV)
+    k2, n2, cp = -(-k // s), -(-n // s), 48
+    Y = torch.full((b, n2, n2, cp), float("nan"), device=DEV)
+    K.space_to_depth(X, c, s, Y)
+    return X, W, Y, k2, n2, cp
+
+
+@pytest.mark.parametrize("b,epi", [(1, "bias_relu"), (3, "store"), (20, "bias_relu")])
+def test_conv_window_fprop_vs_torch(b, epi):
+    """The window implicit GEMM (all 9 taps of a tile read from one staged input
+    window by shifted descriptors; weights resident; CTA pairs) == the strided
+    11x11 conv, TF32 tolerance; junk (padded-width) rows never written."""
+    gen = torch.Generator().manual_seed(60 + b)
+    X, W, Xs, k2, n2, cp = _s2d_conv1(b, gen)
+    d, m = 96, n2 - k2 + 1
+    ld = K.round_up(k2 * k2 * cp, 32)
+    Wt = torch.zeros(d, ld, device=DEV)
+    K.conv_weight_s2d(W, d, 3, 11, 4, cp, Wt, ld)
+    bias = torch.randn(d, generator=gen).to(DEV)
+    cs = 100   # a pixel stride wider than d_out: the gap must stay untouched
+    out = torch.full((b * m * m, cs), float("nan"), device=DEV)
+    code = {"store": _abi.EPI_STORE, "bias_relu": _abi.EPI_BIAS_RELU}[epi]
+    K.conv_window(_abi.CONV_FPROP, Xs, k2, d, Wt, ld, out, cs, epilogue=code, bias=bias)
+    ref = torch.nn.functional.conv2d(X.permute(0, 3, 1, 2).double().cpu(), W.double().cpu(), stride=4)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, d)
+    if epi == "bias_relu":
+        ref = (ref + bias.double().cpu()).clamp_min(0)
+    torch.cuda.synchronize()
+    o = out.cpu()
+    assert torch.isnan(o[:, d:]).all()
+    assert rel_err(o[:, :d], ref) < 2e-3
+
+
+@pytest.mark.parametrize("b", [1, 6])
+@pytest.mark.parametrize("split", ["", "1"])
+def test_conv_window_wgrad_bias_vs_torch(b, split, monkeypatch):
+    """Weight + bias gradient of the space-to-depth conv1 through the window
+    kernel (N = 48 MMA per tap on a shifted MN-major descriptor, or the
+    32 + 16 split), mapped back to OIHW, against torch's conv2d weight grad."""
+    if split:
+        monkeypatch.setenv("OMNI_WINDOW_TAP_SPLIT", split)
+    gen = torch.Generator().manual_seed(70 + b)
+    X, W, Xs, k2, n2, cp = _s2d_conv1(b, gen)
+    d, m = 96, n2 - k2 + 1
+    dY = torch.randn(b * m * m, d, generator=gen)
+    ldw = K.round_up(k2 * k2 * cp + 16, 32)
+    dWt = torch.full((d, ldw), float("nan"), device=DEV)
+    K.conv_window(_abi.CONV_WGRAD_BIAS, Xs, k2, d, dY.to(DEV), d, dWt, ldw)
+    dW = torch.empty(d, 3, 11, 11, device=DEV)
+    db = torch.empty(d, device=DEV)
+    K.conv_weight_s2d(dW, d, 3, 11, 4, cp, dWt, ldw, inverse=True, bias=db)
+    Xd = X.permute(0, 3, 1, 2).double().cpu()
+    Wd = W.double().cpu().requires_grad_(True)
+    ref = torch.nn.functional.conv2d(Xd, Wd, stride=4)
+    ref.backward(dY.reshape(b, m, m, d).permute(0, 3, 1, 2).double())
+    torch.cuda.synchronize()
+    assert rel_err(dW.cpu(), Wd.grad) < 2e-3
+    assert rel_err(db.cpu(), dY.double().sum(0)) < 2e-3   # the bias row is a TF32 product too

@@ -1,8 +1,9 @@
 """Multi-GPU parity checks (NCCL, one process per GPU), run through torchrun
 when the box has >= 2 GPUs (skipped on single-GPU boxes):
 
-* data-parallel DeviceSession (per-layer async allreduce, layer-wise update)
-  and its merged-FC variant == the float64 replay of the mean-gradient update;
+* data-parallel DeviceSession (per-layer async allreduce, layer-wise update;
+  peer-memory fused reduce + update; merged FC) == the float64 ORACLE replay
+  (refcnn.grad of every rank's batch, mean, sgd.py:92-101 update);
 * the round-synchronous compute-group runtime == the oracle's deterministic
   simulate (event log and weights)."""
 
@@ -27,9 +28,11 @@ def free_port() -> int:
 
 
 def torchrun(n, script, *args, env=None):
+    # the checkers that import the oracle live under tests/ (mp_*.py); probes under tools/
+    where = "tests" if script.startswith("mp_") else "tools"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", f"--master-port={free_port()}",
-           os.path.join(ROOT, "tools", script), *args]
+           os.path.join(ROOT, where, script), *args]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
                        env=None if env is None else {**os.environ, **env})
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
@@ -39,14 +42,14 @@ def torchrun(n, script, *args, env=None):
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("mode", ["", "merged", "p2p"])
 def test_data_parallel_session_equals_replay(mode):
-    out = torchrun(2, "dp_check.py", "cifar10_quick", *([mode] if mode else []))
+    out = torchrun(2, "mp_dp_check.py", "cifar10_quick", *([mode] if mode else []))
     assert "normwise" in out
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("mode", ["", "--p2p", "--overlap"])
 def test_group_runtime_equals_oracle_schedule(mode):
-    out = torchrun(2, "groups_check.py", *([mode] if mode else []))
+    out = torchrun(2, "mp_groups_check.py", *([mode] if mode else []))
     assert '"pass": true' in out
 
 
@@ -59,10 +62,10 @@ def test_c_abi_communicators_one_process_per_gpu():
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("transport", ["dma", "pull"])
 def test_peer_memory_update_both_transports(transport):
-    """dp_check asserts W bit-identical on every rank and equal to the float64
-    replay (<= 1e-5 normwise)."""
-    out = torchrun(2, "dp_check.py", "lenet", "p2p", env={"OMNI_P2P_MODE": transport})
-    assert "p2p session vs replay" in out
+    """mp_dp_check asserts W bit-identical on every rank and equal to the
+    float64 oracle replay."""
+    out = torchrun(2, "mp_dp_check.py", "lenet", "p2p", env={"OMNI_P2P_MODE": transport})
+    assert "p2p session vs oracle replay" in out
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")

@@ -256,11 +256,15 @@ def test_measured_he_deterministic(g):
     assert abs(he - pred) <= 0.02 * pred, (g, he, pred)
 
 
-def test_measured_he_exponential():
-    """Exponential services, 10k events: within 10% of he_predict (SPEC)."""
+@pytest.mark.parametrize("T_cc,t_fc", [(2.0, 2.0), (10.0, 0.01)])
+def test_measured_he_exponential(T_cc, t_fc):
+    """Exponential services, 10k events: within 10% of he_predict (SPEC) --
+    away from the saturation boundary, where queueing (which the closed form
+    ignores) is negligible: deeply FC-saturated (he = t_fc) and deeply
+    conv-bound (he = (t_conv + t_fc) / g)."""
     prob = TinyCNNProblem(8, 4, seed=3, n_examples=64)
     plan = P.ExecutionPlan(N=8, g=4)
-    prof = P.PhaseProfile(T_cc=10.0, T_nc=0.1, t_fc=2.0)
+    prof = P.PhaseProfile(T_cc=T_cc, T_nc=0.1, t_fc=t_fc)
     cfg = P.SimConfig(plan=plan, profile=prof, hp=P.Hyperparams(eta=0.001, mu=0.0, b=4), problem=prob,
                       service_mode="exponential", max_updates=10_000, loss_sample_interval=10_000, seed=2)
     tr = P.simulate(cfg)
