@@ -153,6 +153,36 @@ def tf32_peak_sustained(peaks: dict):
     return None
 
 
+def measure_tf32_peak(dev) -> dict:
+    """cuBLAS TF32 GEMM, 8192^3 (torch.matmul with TF32 enabled), best of 10
+    launches timed alone with CUDA events -- the measured TF32 counterpart of
+    MEASURED_PEAKS' cuBLAS bf16 burst figure (same method, same box, same run)."""
+    import torch
+
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        g = torch.Generator(device=dev).manual_seed(0)
+        a = torch.randn(n, n, device=dev, generator=g)
+        b = torch.randn(n, n, device=dev, generator=g)
+        for _ in range(3):
+            torch.matmul(a, b)
+        best = float("inf")
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        return {"tflops": 2.0 * n ** 3 / (best * 1e-3) / 1e12, "ms": best,
+                "how": "torch.matmul fp32 8192^3 with allow_tf32 (cuBLAS TF32), best of 10, CUDA events"}
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -409,7 +439,13 @@ def run_ours(args):
     conv_flops_step = net.conv_flops_per_image() * b
     achieved = conv_flops_step / (conv_ms * 1e-3) / 1e12 if conv_ms > 0 else 0.0
     peaks = measured_peaks()
-    peak, peak_src = tf32_peak(peaks)
+    bf16_half, bf16_src = tf32_peak(peaks)
+    tf32_meas = measure_tf32_peak(dev)
+    # roofline denominator: the TF32 GEMM peak measured here (cuBLAS, burst);
+    # 3xTF32 issues three tf32 MMAs per product, so its peak is a third of that
+    peak = tf32_meas["tflops"] / (3.0 if args.precision == "3xtf32" else 1.0)
+    peak_src = ("cuBLAS TF32 8192^3 measured in this run (burst), "
+                + ("/ 3 (3xTF32: three tf32 MMAs per product)" if args.precision == "3xtf32" else "of measured"))
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "r01_traffic_summary.json")
     if os.path.exists(tpath):
@@ -480,6 +516,10 @@ def run_ours(args):
             "dtype": args.precision, "data": "synthetic (Gaussian images, uniform labels, random-init weights)",
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per step",
+                         "peak_cublas_tf32_measured": tf32_meas,
+                         "peak_bf16_half": bf16_half, "frac_of_bf16_half": achieved / bf16_half,
+                         "bf16_half_source": bf16_src,
+                         "peak_nominal_tf32_dense": 1100.0, "frac_of_nominal": achieved / 1100.0,
                          "peak_sustained_tf32": tf32_peak_sustained(peaks),
                          "frac_of_sustained": (achieved / tf32_peak_sustained(peaks)
                                                if tf32_peak_sustained(peaks) else None),

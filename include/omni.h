@@ -111,16 +111,17 @@ int omni_gemm_f32(int precision, int M, int N, int K, const float* A, long long 
  * by TMA im2col from the NHWC activation X (b, n, n, cs): no lowered matrix in
  * HBM.  The GEMM
  * K index is (tap, channel) tap-major, i.e. the column order of
- * omni_lower_nhwc_f32.  Requires d_in = c multiple of 32.
- *   OMNI_CONV_FPROP: Y[pix, o] (op)= sum_{tap,ch} X(pix, tap, ch) G[o*ldg + tap*c + ch]
+ * omni_lower_nhwc_f32, with cp = round_up(c, 32) channels per tap (channels
+ * c..cp-1 of a partial 32-channel block read as zeros).
+ *   OMNI_CONV_FPROP: Y[pix, o] (op)= sum_{tap,ch} X(pix, tap, ch) G[o*ldg + tap*cp + ch]
  *                    (G = tap-major weights d_out x ldg; Y = b*m*m rows, ld ldy)
- *   OMNI_CONV_WGRAD: Y[o*ldy + tap*c + ch] = sum_pix G[pix*ldg + o] X(pix, tap, ch)
+ *   OMNI_CONV_WGRAD: Y[o*ldy + tap*cp + ch] = sum_pix G[pix*ldg + o] X(pix, tap, ch)
  *                    (G = output gradient dY, b*m*m rows, ld ldg)
  * The data gradient of a stride-1 conv is OMNI_CONV_FPROP on dY with pad
  * k-1-pad and the spatially flipped, transposed weights.                     */
 /*   OMNI_CONV_WGRAD_BIAS: as OMNI_CONV_WGRAD, plus the bias gradient
- *                    Y[o*ldy + k*k*c] = sum_pix G[pix*ldg + o] as one more GEMM row
- *                    (a ones operand chunk; needs ldy > k*k*c).  The workspace
+ *                    Y[o*ldy + k*k*cp] = sum_pix G[pix*ldg + o] as one more GEMM row
+ *                    (a ones operand chunk; needs ldy > k*k*cp).  The workspace
  *                    (size from omni_conv_implicit_plan) reserves room for that
  *                    ones tile; the library reads its own constant copy.  */
 #define OMNI_CONV_FPROP 0

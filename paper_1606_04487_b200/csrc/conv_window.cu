@@ -45,7 +45,8 @@ using namespace gemm;
 constexpr int CP = 48;        // space-to-depth channels (4 x 4 x 3)
 constexpr int C0 = 32;        // channels in the 128-byte swizzled box
 constexpr int C1 = CP - C0;   // channels in the 64-byte swizzled box
-constexpr int MAX_TAPS = 9;   // k2 <= 3
+constexpr int K2 = 3;         // taps per dimension of the space-to-depth conv (11/4 -> 3)
+constexpr int MAX_TAPS = K2 * K2;
 constexpr int WIN_MAX = 256;  // TMA box rows
 
 PFN_cuTensorMapEncodeTiled_v12000 encode() {
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(256, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = (int)cluster_ctarank();
   const int unit0 = (int)(blockIdx.x >> 1), units = (int)(gridDim.x >> 1);
-  const int taps = p.k2 * p.k2;
+  constexpr int taps = MAX_TAPS;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmX0);
@@ -241,9 +242,9 @@ __global__ void __launch_bounds__(256, 1)
         const uint32_t a0 = sbase + L::STAGE_OFF + stage * L::STAGE;
         const uint64_t a0d = make_desc(a0, 16, 1024, 2);
         const uint64_t a1d = make_desc(a0 + L::A0, 16, 512, 4);
+#pragma unroll
         for (int t = 0; t < taps; ++t) {
-          const int kx = t / p.k2, ky = t - kx * p.k2;
-          const uint32_t off = (uint32_t)(kx * p.n2 + ky);
+          const uint32_t off = (uint32_t)((t / K2) * p.n2 + t % K2);   // t is a compile-time constant
           const uint64_t at0 = a0d + (uint64_t)(off * 8u), at1 = a1d + (uint64_t)(off * 4u);
           const uint64_t bt0 = b0d + (uint64_t)(t * (L::B0_TAP >> 4)), bt1 = b1d + (uint64_t)(t * (L::B1_TAP >> 4));
 #pragma unroll
@@ -284,17 +285,19 @@ __global__ void __launch_bounds__(256, 1)
       const int prow = valid ? (img * p.m + h) * p.m + x : 0;   // output pixel of this lane's row
       const uint32_t t_row = tmem_base + (uint32_t)(acc * L::ACC_STRIDE) + ((uint32_t)(ew * 32) << 16);
       float* stg = reinterpret_cast<float*>(smem + L::STG_OFF) + ew * 32 * L::STG_PITCH;
-#pragma unroll 1
+      // all of this row's accumulator columns in one batch of TMEM loads,
+      // then the accumulator goes straight back to the MMA warp
+      uint32_t racc[BN / 16][16];
+#pragma unroll
+      for (int j = 0; j < BN / 16; ++j) tmem_ld16(t_row + (uint32_t)(16 * j), racc[j]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster_relaxed(mapa_rank0(tempty_bar(acc)));
+#pragma unroll
       for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r0[16], r1[16];
-        tmem_ld16(t_row + (uint32_t)c0, r0);
-        tmem_ld16(t_row + (uint32_t)c0 + 16, r1);
-        tmem_wait_ld();
-        if (c0 + 32 >= BN) {  // last read of this accumulator: hand it back to the MMA warp
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster_relaxed(mapa_rank0(tempty_bar(acc)));
-        }
+        const uint32_t(&r0)[16] = racc[c0 / 16];
+        const uint32_t(&r1)[16] = racc[c0 / 16 + 1];
         float* srow = stg + lane * L::STG_PITCH;
         switch (p.epilogue) {
           case OMNI_EPI_BIAS: fstage32<OMNI_EPI_BIAS>(srow, r0, r1, sbias, c0); break;
@@ -440,9 +443,9 @@ __global__ void __launch_bounds__(256, 1)
       for (int kk = 0; kk < p.kb / 8; ++kk) {
         const uint32_t accf = (blk > blk0 || kk > 0) ? 1u : 0u;
         const uint64_t ad = ad0 + (uint64_t)(kk * 64u);       // 8 K rows = 1024 B
-        for (int t = 0; t < p.taps; ++t) {
-          const int kx = t / p.k2, ky = t - kx * p.k2;
-          const uint64_t roff = (uint64_t)((kx * p.n2 + ky + kk * 8) * 8u);   // rows x 128 B >> 4
+#pragma unroll
+        for (int t = 0; t < MAX_TAPS; ++t) {
+          const uint64_t roff = (uint64_t)(((t / K2) * p.n2 + t % K2 + kk * 8) * 8u);   // rows x 128 B >> 4
           const uint32_t dcol = tmem_base + (uint32_t)(t * CP);
           if (!p.tap_split) {
             tc_mma_tf32_elect(dcol, ad, bd0 + roff, id48, accf);
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
         // bias gradient: dZ^T times an all-ones operand (16 identical columns)
-        tc_mma_tf32_elect(tmem_base + (uint32_t)(p.taps * CP), ad, onesd + (uint64_t)(kk * 64u), id16, accf);
+        tc_mma_tf32_elect(tmem_base + (uint32_t)(MAX_TAPS * CP), ad, onesd + (uint64_t)(kk * 64u), id16, accf);
       }
       tc_commit_elect(empty_bar(stage));
       if (++stage == p.stages) {
@@ -522,7 +525,7 @@ struct Geo {
 int geometry(int b, int n2, int cp, int k2, int d_out, Geo* g) {
   OMNI_REQUIRE(b >= 1 && n2 >= 1 && k2 >= 1 && d_out >= 1, "conv window: bad shape");
   OMNI_REQUIRE(cp == CP, "conv window: needs %d space-to-depth channels (got %d)", CP, cp);
-  OMNI_REQUIRE(k2 <= 3 && k2 <= n2, "conv window: k2 = %d unsupported", k2);
+  OMNI_REQUIRE(k2 == K2 && k2 <= n2, "conv window: k2 = %d unsupported (the kernels are built for %d)", k2, K2);
   g->m = n2 - k2 + 1;
   g->taps = k2 * k2;
   g->win_f = 128 + (k2 - 1) * (n2 + 1);

@@ -1125,7 +1125,7 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
     p.conv_s = cg->s;
     p.conv_pad = cg->pad;
     p.conv_k = cg->k;
-    p.conv_cblocks = cg->c / 32;
+    p.conv_cblocks = (cg->c + 31) / 32;
     p.px_dh = bkt / cg->m;
     p.px_dw = bkt - p.px_dh * cg->m;
   }
@@ -1256,7 +1256,12 @@ static int conv_shape(int op, int b, int n, int c, int k, int stride, int pad, i
                "conv: unknown op %d", op);
   OMNI_REQUIRE(b >= 1 && n >= 1 && k >= 1 && stride >= 1 && pad >= 0 && d_out >= 1,
                "n, k, d_in, d_out, stride must be positive");
-  OMNI_REQUIRE(c % 32 == 0, "implicit conv needs d_in %% 32 == 0 (got %d)", c);
+  OMNI_REQUIRE(c >= 1, "implicit conv needs d_in >= 1");
+  // channels run in 32-wide im2col blocks: a partial last block reads the
+  // missing channels as zeros (TMA out-of-bounds fill), so the GEMM's K index
+  // per filter tap -- and the weight / weight-gradient rows -- are
+  // round_up(d_in, 32) wide
+  const int cpad = (c + 31) / 32 * 32;
   OMNI_REQUIRE(k <= n + 2 * pad && (n + 2 * pad - k) % stride == 0, "conv: bad geometry");
   OMNI_REQUIRE(pad <= 127 && k - 1 - pad <= 128, "conv: padding outside the im2col box range");
   *m = (n + 2 * pad - k) / stride + 1;
@@ -1265,10 +1270,10 @@ static int conv_shape(int op, int b, int n, int c, int k, int stride, int pad, i
   if (op == OMNI_CONV_FPROP) {
     *M = (int)pix;
     *N = d_out;
-    *K = k * k * c;
+    *K = k * k * cpad;
   } else {
     *M = d_out;
-    *N = k * k * c;
+    *N = k * k * cpad;
     *K = (int)pix;
   }
   return OMNI_OK;

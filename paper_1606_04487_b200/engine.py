@@ -154,7 +154,7 @@ class GpuNet:
                     # the window kernels (TF32): no channel padding (cp = 48 for
                     # CaffeNet conv1), every tap read from one staged window per tile
                     window = (precision == "tf32" and p2 == 0 and st * st * c == 48 and
-                              os.environ.get("OMNI_WINDOW", "0") == "1" and
+                              not os.environ.get("OMNI_NO_WINDOW") and
                               K.conv_window_plan(_abi.CONV_FPROP, self.b, n2, 48, k2, d) >= 0 and
                               K.conv_window_plan(_abi.CONV_WGRAD_BIAS, self.b, n2, 48, k2, d) >= 0)
                     if window:
@@ -183,9 +183,12 @@ class GpuNet:
                 op.wstage = z(d, op.ldK)
                 op.ldW = op.ldK
                 if op.window:
-                    # the window wgrad writes k2*k2*48 weight columns + 16 bias columns
+                    # weight gradient on the generic implicit GEMM over the same
+                    # 48-channel image: 64-wide channel blocks per tap (16 zero-read),
+                    # the bias as the folded extra row
+                    st, k2, p2, n2, cp = op.s2d
                     op.wgrad_op = _abi.CONV_WGRAD_BIAS
-                    op.ldW = K.round_up(op.Kf + 16, 32)
+                    op.ldW = K.round_up(k2 * k2 * 64 + 1, 32)
                 elif op.implicit and op.boff >= 0 and not os.environ.get("OMNI_NO_WGRAD_BIAS"):
                     # bias gradient as one more row of the implicit wgrad GEMM (column Kf)
                     op.wgrad_op = _abi.CONV_WGRAD_BIAS
@@ -269,9 +272,6 @@ class GpuNet:
         """Largest split-K workspace any GEMM of this layer asks for, from the
         same plan functions the launches use (implicit convs plan differently
         from plain GEMMs: 64-deep wgrad stages, transposed fprop)."""
-        if op.kind == "conv" and op.window:
-            st, k2, p2, n2, cp = op.s2d
-            return K.conv_window_plan(_abi.CONV_WGRAD_BIAS, b, n2, cp, k2, op.layer.d_out)
         if op.kind == "conv" and op.implicit:
             d = op.layer.d_out
             if op.s2d is not None:
@@ -582,19 +582,15 @@ class GpuNet:
                 if op.implicit:
                     with wgrad_stream():
                         X, c_, k_, s_, p_ = self._conv_input(op, b, transform=False)
-                        if op.window:
-                            self._timed(d, op.c_in * op.k * op.k, Mr, "conv", lambda: K.conv_window(
-                                _abi.CONV_WGRAD_BIAS, X, k_, d, dZ, op.out.cs, op.dwstage, op.ldW,
-                                workspace=self._ws_active))
-                        else:
-                            self._conv(op.wgrad_op, X, c_, k_, s_, p_, d, dZ, op.out.cs,
-                                       op.dwstage, op.ldW)
+                        self._conv(op.wgrad_op, X, c_, k_, s_, p_, d, dZ, op.out.cs,
+                                   op.dwstage, op.ldW)
                         fold = op.wgrad_op == _abi.CONV_WGRAD_BIAS
                         gb = G[op.boff:op.boff + d] if fold else None
                         if op.s2d is not None:
+                            # wgrad rows are round_up(cp, 32) wide per tap (64 for the window form)
                             K.conv_weight_s2d(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k,
-                                              op.s2d[0], op.s2d[4], op.dwstage, op.ldW, inverse=True,
-                                              bias=gb)
+                                              op.s2d[0], K.round_up(op.s2d[4], 32), op.dwstage, op.ldW,
+                                              inverse=True, bias=gb)
                         else:
                             K.conv_weight_to_tap(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k,
                                                  op.dwstage, op.ldW, inverse=True, bias=gb)

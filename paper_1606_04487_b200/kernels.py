@@ -200,7 +200,7 @@ def conv_implicit(op: int, X: torch.Tensor, c: int, k: int, stride: int, pad: in
     _require_cuda(X, G, Y)
     b, n, _, cs = X.shape
     m = (n + 2 * pad - k) // stride + 1
-    pixels, taps = b * m * m, k * k * c
+    pixels, taps = b * m * m, k * k * round_up(c, 32)   # cp = round_up(c, 32) per tap
     _fits(X, (b * n * n - 1) * cs + c, "X")
     if op == _abi.CONV_FPROP:   # G: d_out x ldg (tap-major weights), Y: pixels x ldy
         _fits(G, (d_out - 1) * ldg + taps, "G")

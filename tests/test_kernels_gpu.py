@@ -658,3 +658,35 @@ def test_conv_window_wgrad_bias_vs_torch(b, split, monkeypatch):
     torch.cuda.synchronize()
     assert rel_err(dW.cpu(), Wd.grad) < 2e-3
     assert rel_err(db.cpu(), dY.double().sum(0)) < 2e-3   # the bias row is a TF32 product too
+
+
+@pytest.mark.parametrize("prec", ["tf32", "3xtf32"])
+def test_conv_implicit_partial_channel_block(prec):
+    """d_in = 48 (the window path's space-to-depth image): the generic implicit
+    GEMM runs 64-wide per-tap channel blocks whose last 16 channels read as
+    zeros (TMA out-of-bounds fill), fprop and wgrad + bias row, vs torch."""
+    gen = torch.Generator().manual_seed(81)
+    X, W, Xs, k2, n2, cp = _s2d_conv1(3, gen)
+    d, m = 96, n2 - k2 + 1
+    ld = K.round_up(k2 * k2 * 64 + 1, 32)
+    Wt = torch.zeros(d, ld, device=DEV)
+    K.conv_weight_s2d(W, d, 3, 11, 4, 64, Wt, ld)          # 64 weight columns per tap
+    pc = {"tf32": _abi.PREC_TF32, "3xtf32": _abi.PREC_3XTF32}[prec]
+    tol = 2e-3 if prec == "tf32" else 1e-5
+    out = torch.empty(3 * m * m, d, device=DEV)
+    K.conv_implicit(_abi.CONV_FPROP, Xs, cp, k2, 1, 0, d, Wt, ld, out, d, precision=pc)
+    Xd = X.permute(0, 3, 1, 2).double().cpu()
+    Wd = W.double().cpu().requires_grad_(True)
+    ref = torch.nn.functional.conv2d(Xd, Wd, stride=4)
+    torch.cuda.synchronize()
+    assert rel_err(out.cpu(), ref.permute(0, 2, 3, 1).reshape(-1, d)) < tol
+    dY = torch.randn(3 * m * m, d, generator=gen)
+    ref.backward(dY.reshape(3, m, m, d).permute(0, 3, 1, 2).double())
+    dWt = torch.full((d, ld), float("nan"), device=DEV)
+    K.conv_implicit(_abi.CONV_WGRAD_BIAS, Xs, cp, k2, 1, 0, d, dY.to(DEV), d, dWt, ld, precision=pc)
+    dW = torch.empty(d, 3, 11, 11, device=DEV)
+    db = torch.empty(d, device=DEV)
+    K.conv_weight_s2d(dW, d, 3, 11, 4, 64, dWt, ld, inverse=True, bias=db)
+    torch.cuda.synchronize()
+    assert rel_err(dW.cpu(), Wd.grad) < tol
+    assert rel_err(db.cpu(), dY.double().sum(0)) < max(tol, 1e-5)
