@@ -15,7 +15,7 @@ $(BUILD)/%.o: $(SRC_DIR)/%.cu $(SRC_DIR)/common.cuh $(SRC_DIR)/tc_ptx.cuh includ
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/$*.ptxas.log || (cat $(BUILD)/$*.ptxas.log; exit 1)
 
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl -lrt
 
 clean:
 	rm -rf $(BUILD) $(LIB)

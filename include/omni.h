@@ -30,6 +30,7 @@ extern "C" {
 #define OMNI_EINVAL -1       /* bad argument: maps to ValueError           */
 #define OMNI_ECUDA -2        /* CUDA runtime / driver failure: RuntimeError */
 #define OMNI_EUNSUPPORTED -3 /* shape/layout outside what a kernel handles  */
+#define OMNI_ETIMEOUT -4     /* a wait gave up (a peer process stalled or died) */
 
 const char* omni_last_error(void);
 int omni_version(void);
@@ -189,6 +190,23 @@ long long omni_conv_window_plan(int op, int b, int n2, int cp, int k2, int d_out
 int omni_conv_window_f32(int op, const float* Xs, int b, int n2, int cp, int k2, int d_out, const float* G,
                          long long ldg, float* Y, long long ldy, int epilogue, const float* bias,
                          float* workspace, long long ws_bytes, void* stream);
+/* Mailbox of the free-running compute groups (async_groups.py, mailbox.cu):
+ * a POSIX shared-memory page of lock-free atomics through which the update
+ * server (co-located on rank 0) and the group leaders hand over gradients and
+ * snapshots; the payloads move GPU to GPU by DMA (omni_copy_async on
+ * IPC-mapped buffers).  post: a leader whose gradient has landed takes a
+ * ticket; next: the server takes the next ticket's group (FIFO by arrival,
+ * simulator.py:3-7); snap_post / snap_wait: per-group snapshot sequence
+ * (-1 = stop).  Waits return OMNI_ETIMEOUT after timeout_ms.                */
+long long omni_mailbox_bytes(void);
+int omni_mailbox_create(const char* name, int ngroups, void** box);
+int omni_mailbox_open(const char* name, void** box, int timeout_ms);
+int omni_mailbox_close(void* box, const char* unlink_name);
+int omni_mailbox_post(void* box, int group, long long* ticket);
+int omni_mailbox_next(void* box, int* group, int timeout_ms);
+int omni_mailbox_snap_post(void* box, int group, long long seq);
+int omni_mailbox_snap_wait(void* box, int group, long long last, long long* seq, int timeout_ms);
+
 /* K8 fused momentum SGD (sgd.py:92-101): V = mu*V - eta*(g + lam*w_read);
  * W = W + V.  w_read may alias W (synchronous step).                         */
 int omni_sgd_momentum_f32(float* W, float* V, const float* g, const float* w_read, float eta,
@@ -270,6 +288,9 @@ int omni_comm_size_rank(void* comm, int* size, int* rank);
 /* In-place sum over the communicator (a group's gradient), on the stream. */
 int omni_allreduce_sum_f32(void* comm, float* buf, size_t n, void* stream);
 /* Point to point (snapshot / gradient exchange with the update server).   */
+/* In-place broadcast of buf from communicator rank `root` (a compute group's
+ * new snapshot from its leader to the other members).                        */
+int omni_broadcast_f32(void* comm, float* buf, size_t n, int root, void* stream);
 int omni_send_f32(void* comm, const float* buf, size_t n, int peer, void* stream);
 int omni_recv_f32(void* comm, float* buf, size_t n, int peer, void* stream);
 /* Bracket several send/recv calls so NCCL fuses them (no deadlock on

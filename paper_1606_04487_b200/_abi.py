@@ -19,6 +19,7 @@ OMNI_OK = 0
 OMNI_EINVAL = -1
 OMNI_ECUDA = -2
 OMNI_EUNSUPPORTED = -3
+OMNI_ETIMEOUT = -4
 
 PREC_TF32 = 0
 PREC_3XTF32 = 1
@@ -98,6 +99,7 @@ SIGNATURES: dict[str, tuple] = {
     "omni_comm_destroy": (_I, [_P]),
     "omni_comm_size_rank": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "omni_allreduce_sum_f32": (_I, [_P, _P, ctypes.c_size_t, _P]),
+    "omni_broadcast_f32": (_I, [_P, _P, ctypes.c_size_t, _I, _P]),
     "omni_send_f32": (_I, [_P, _P, ctypes.c_size_t, _I, _P]),
     "omni_recv_f32": (_I, [_P, _P, ctypes.c_size_t, _I, _P]),
     "omni_comm_group_start": (_I, []),
@@ -107,6 +109,14 @@ SIGNATURES: dict[str, tuple] = {
     "omni_p2p_wait": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _P]),
     "omni_p2p_reduce_sgd_f32": (_I, [_P, _P, _I, _I, _L, _L, _P, _P, _F, _F, _F, _P]),
     "omni_copy_async": (_I, [_P, _P, _L, _P]),
+    "omni_mailbox_bytes": (_L, []),
+    "omni_mailbox_create": (_I, [ctypes.c_char_p, _I, ctypes.POINTER(_P)]),
+    "omni_mailbox_open": (_I, [ctypes.c_char_p, ctypes.POINTER(_P), _I]),
+    "omni_mailbox_close": (_I, [_P, ctypes.c_char_p]),
+    "omni_mailbox_post": (_I, [_P, _I, ctypes.POINTER(_L)]),
+    "omni_mailbox_next": (_I, [_P, ctypes.POINTER(_I), _I]),
+    "omni_mailbox_snap_post": (_I, [_P, _I, _L]),
+    "omni_mailbox_snap_wait": (_I, [_P, _I, _L, ctypes.POINTER(_L), _I]),
     "omni_ipc_handle": (_I, [_P, _P, ctypes.POINTER(_L)]),
     "omni_ipc_open": (_I, [_P, ctypes.POINTER(_P)]),
     "omni_ipc_close": (_I, [_P]),

@@ -102,6 +102,10 @@ class Communicator:
         _abi.call("omni_allreduce_sum_f32", self._h, _buf(t), t.numel(), _stream(stream, t))
         return t
 
+    def broadcast(self, t: torch.Tensor, root: int, stream=None) -> torch.Tensor:
+        _abi.call("omni_broadcast_f32", self._h, _buf(t), t.numel(), root, _stream(stream, t))
+        return t
+
     def send(self, t: torch.Tensor, peer: int, stream=None) -> None:
         _abi.call("omni_send_f32", self._h, _buf(t), t.numel(), peer, _stream(stream, t))
 

@@ -33,6 +33,8 @@ struct Nccl {
   ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
@@ -65,7 +67,7 @@ void load_nccl() {
             sym(h, "ncclCommInitAll", n.CommInitAll) && sym(h, "ncclCommSplit", n.CommSplit) &&
             sym(h, "ncclCommDestroy", n.CommDestroy) && sym(h, "ncclCommCount", n.CommCount) &&
             sym(h, "ncclCommUserRank", n.CommUserRank) && sym(h, "ncclAllReduce", n.AllReduce) &&
-            sym(h, "ncclSend", n.Send) && sym(h, "ncclRecv", n.Recv) &&
+            sym(h, "ncclBroadcast", n.Broadcast) && sym(h, "ncclSend", n.Send) && sym(h, "ncclRecv", n.Recv) &&
             sym(h, "ncclGroupStart", n.GroupStart) && sym(h, "ncclGroupEnd", n.GroupEnd);
   n.ok = ok;
   g_nccl = n;
@@ -172,6 +174,15 @@ int omni_allreduce_sum_f32(void* comm, float* buf, size_t n, void* stream) {
   OMNI_REQUIRE(n == 0 || buf != nullptr, "omni_allreduce_sum_f32: buf is NULL");
   if (n == 0) return OMNI_OK;
   OMNI_NCCL_TRY(g_nccl.AllReduce(buf, buf, n, ncclFloat32, ncclSum, static_cast<ncclComm_t>(comm),
+                                 omni::as_stream(stream)));
+  return OMNI_OK;
+}
+
+int omni_broadcast_f32(void* comm, float* buf, size_t n, int root, void* stream) {
+  OMNI_NEED_NCCL();
+  OMNI_REQUIRE(comm != nullptr && (n == 0 || buf != nullptr), "omni_broadcast_f32: NULL argument");
+  if (n == 0) return OMNI_OK;
+  OMNI_NCCL_TRY(g_nccl.Broadcast(buf, buf, n, ncclFloat32, root, static_cast<ncclComm_t>(comm),
                                  omni::as_stream(stream)));
   return OMNI_OK;
 }

@@ -99,3 +99,30 @@ def async_worker(rank, world, port, g, max_updates, hp_tuple, out_dir):
             A.run_worker(plan, JitterBackend(1000 + rank), hp, W0, N_EX, seed=11)
     finally:
         dist.destroy_process_group()
+
+
+def colocated_worker(rank, world, port, g, max_updates, hp_tuple, out_dir):
+    """paper_1606_04487_b200.colocated: every rank computes, rank 0 also serves
+    (host shared-memory payload store, gloo group collectives)."""
+    from paper_1606_04487_b200 import async_groups as A
+    from paper_1606_04487_b200 import colocated as C
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        eta, mu, lam, b = hp_tuple
+        hp = Hyperparams(eta=eta, mu=mu, lam=lam, b=b)
+        plan = ExecutionPlan(world, g)
+        W0 = torch.from_numpy(initial_weights())
+        res = C.run_colocated(plan, JitterBackend(1000 + rank), hp, W0, N_EX, seed=11,
+                              max_updates=max_updates, store="shm")
+        if rank == 0:
+            Wr, _ = A.replay(res.events, plan, OracleBackend(), hp, W0, N_EX, seed=11)
+            np.save(os.path.join(out_dir, "W.npy"), res.W.numpy())
+            np.save(os.path.join(out_dir, "Wreplay.npy"), Wr.numpy())
+            np.save(os.path.join(out_dir, "ev.npy"),
+                    np.array([[e.group_id, e.read_step, e.write_step, e.staleness, e.batch_index]
+                              for e in res.events]))
+    finally:
+        dist.destroy_process_group()

@@ -72,3 +72,19 @@ def test_peer_memory_update_both_transports(transport):
 def test_peer_update_probe_exact():
     out = torchrun(2, "p2p_probe.py")
     assert '"W_identical_on_all_ranks": true' in out
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("g", [1, 2])
+def test_colocated_async_groups_two_gpus(g):
+    """Free-running groups, server co-located on rank 0 (no extra GPU):
+    valid schedule, bit-exact replay, float64 oracle replay <= 1e-4."""
+    out = torchrun(2, "mp_async_check.py", "cifar10_quick", str(g), "16")
+    assert '"pass": true' in out
+
+
+@pytest.mark.skipif(NGPU < 4, reason="needs >= 4 GPUs")
+@pytest.mark.parametrize("g", [2, 4])
+def test_colocated_async_groups_four_gpus(g):
+    out = torchrun(4, "mp_async_check.py", "cifar10_quick", str(g), "16")
+    assert '"pass": true' in out
