@@ -147,13 +147,22 @@ class PeerStore:
         return self._opened[h] + off
 
     def lane(self, gi: int) -> torch.Tensor:
+        if gi == 0 and self.local_grad is not None:
+            return self.local_grad
         return self.lanes[gi]
 
+    local_grad = None   # rank 0's own group: the server reads its gradient buffer in place
+
     def push_grad(self, G: torch.Tensor) -> None:
-        """Leader: G -> its lane on rank 0; returns once the copy has landed."""
+        """Leader: G -> its lane on rank 0; returns once the copy has landed.
+        On rank 0 itself the lane is G (zero copy: G stays untouched until
+        this group's next snapshot has arrived)."""
         s = torch.cuda.current_stream(self.dev)
-        _abi.call("omni_copy_async", ctypes.c_void_p(self.lane_ptr), ctypes.c_void_p(G.data_ptr()),
-                  self.n * self.esz, ctypes.c_void_p(s.cuda_stream))
+        if self.lanes is not None:   # rank 0, group 0
+            self.local_grad = G
+        else:
+            _abi.call("omni_copy_async", ctypes.c_void_p(self.lane_ptr), ctypes.c_void_p(G.data_ptr()),
+                      self.n * self.esz, ctypes.c_void_p(s.cuda_stream))
         s.synchronize()
 
     def push_snap(self, gi: int, W: torch.Tensor) -> None:
@@ -335,11 +344,20 @@ def _work(plan, backend, hp, W0, st, box, grp, gi, member, n_examples, seed) -> 
     rng = batch_stream(seed, gi)
     W = st.model if member == 0 else W0.clone()
     last, n = 0, 0
+    hooked = plan.k > 1 and isinstance(grp, _OmniGroup) and hasattr(backend, "grad_hooked")
     while True:
         idx = rng.integers(0, n_examples, size=hp.b)
-        G = backend.grad(W, idx[member * per:(member + 1) * per])
-        if plan.k > 1:
-            grp.allreduce_sum(G)                       # sum of the k slice means
+        mine = idx[member * per:(member + 1) * per]
+        if hooked:
+            # each layer's slice of the group allreduce is issued on the weight-
+            # gradient stream as soon as the layer is done, overlapping the rest
+            # of the backward (the sum of the k slice means lands in engine.grad)
+            G = backend.engine.grad
+            backend.grad_hooked(W, mine, lambda lo, hi: grp.allreduce_sum(G[lo:hi]))
+        else:
+            G = backend.grad(W, mine)
+            if plan.k > 1:
+                grp.allreduce_sum(G)                   # sum of the k slice means
         if member == 0:
             st.push_grad(G)                            # landed in the server lane
             box.post(gi)
