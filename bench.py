@@ -359,7 +359,7 @@ def run_ours(args):
     sess = prob.device_session(SGDState.fresh(np.zeros(1)), hp,
                                process_group=dist.group.WORLD if world > 1 else None,
                                merged_fc=args.merged_fc and world > 1,
-                               p2p=args.p2p and world > 1)
+                               p2p=args.p2p and world > 1 and not args.merged_fc)
     gw = torch.Generator(device=dev)
     gw.manual_seed(args.seed)                     # identical initial model on every rank
     sess.W = 0.01 * torch.randn(net.dim, generator=gw, device=dev)

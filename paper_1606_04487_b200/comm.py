@@ -317,3 +317,92 @@ class PeerUpdate:
         for base in self._opened.values():
             _abi.call("omni_ipc_close", ctypes.c_void_p(base))
         self._opened.clear()
+
+
+class _Done:
+    """Completion handle of an allreduce issued on a communicator stream:
+    ``wait()`` makes the caller's current stream wait for it (no host block)."""
+
+    def __init__(self, stream):
+        self._ev = torch.cuda.Event()
+        self._ev.record(stream)
+
+    def wait(self) -> None:
+        torch.cuda.current_stream().wait_event(self._ev)
+
+
+class SessionComm:
+    """The data-parallel session's collectives on the library's own NCCL
+    communicator (C-ABI), one per process group: torch.distributed only
+    bootstraps it (the unique id) and names the ranks.
+
+    * ``allreduce_async(t)``: issued on a dedicated communicator stream after
+      the work already queued on the caller's stream (a layer's weight
+      gradient), so it overlaps the rest of the backward; returns a handle
+      whose ``wait()`` orders the caller's stream after it;
+    * ``gather_to_root`` / ``scatter_from_root`` / ``broadcast``: the merged-FC
+      exchanges (pool5 activations and labels to rank 0, their gradients
+      back), as grouped point-to-point calls on the caller's stream."""
+
+    def __init__(self, process_group, device: torch.device):
+        import torch.distributed as dist
+
+        self.pg = process_group
+        self.rank = dist.get_rank(process_group)
+        self.world = dist.get_world_size(process_group)
+        uid = [unique_id() if self.rank == 0 else None]
+        root = dist.get_global_rank(process_group, 0) if process_group is not dist.group.WORLD else 0
+        dist.broadcast_object_list(uid, src=root, group=process_group)
+        self.comm = Communicator.init_rank(self.world, uid[0], self.rank, device.index)
+        self.stream = torch.cuda.Stream(device=device)
+
+    def allreduce_async(self, t: torch.Tensor) -> "_Done":
+        cur = torch.cuda.current_stream(t.device)
+        self.stream.wait_stream(cur)
+        self.comm.allreduce_sum(t, stream=self.stream)
+        return _Done(self.stream)
+
+    def allreduce(self, t: torch.Tensor) -> torch.Tensor:
+        return self.comm.allreduce_sum(t)
+
+    def broadcast(self, t: torch.Tensor, root: int = 0) -> torch.Tensor:
+        return self.comm.broadcast(_f32(t), root) if t.dtype == torch.float32 else self._bcast_bits(t, root)
+
+    def _bcast_bits(self, t, root):
+        self.comm.broadcast(t.view(torch.float32), root)
+        return t
+
+    def gather_to_root(self, src: torch.Tensor, dst_parts: list | None) -> None:
+        """Rank r's ``src`` -> ``dst_parts[r]`` on rank 0 (int32 moves as its bits)."""
+        with group():
+            if self.rank == 0:
+                for r in range(self.world):
+                    if r == 0:
+                        dst_parts[0].copy_(src)
+                    else:
+                        self.comm.recv(_f32(dst_parts[r]), r)
+            else:
+                self.comm.send(_f32(src), 0)
+
+    def scatter_from_root(self, dst: torch.Tensor, src_parts: list | None) -> None:
+        with group():
+            if self.rank == 0:
+                for r in range(self.world):
+                    if r == 0:
+                        dst.copy_(src_parts[0])
+                    else:
+                        self.comm.send(_f32(src_parts[r]), r)
+            else:
+                self.comm.recv(_f32(dst), 0)
+
+    def close(self) -> None:
+        self.comm.destroy()
+
+
+def _f32(t: torch.Tensor) -> torch.Tensor:
+    """A contiguous float32 view of the same bytes (int32 labels travel as bits)."""
+    if t.dtype == torch.float32:
+        return t
+    if t.element_size() != 4:
+        raise ValueError("only 4-byte element types travel through the float32 communicator calls")
+    return t.view(torch.float32)

@@ -186,13 +186,21 @@ class DeviceSession:
                 self.p2p, self.use_p2p = None, False
         return self.p2p
 
-    def _allreduce_hook(self, works):
-        import torch.distributed as dist
+    def _comm(self):
+        """The library's own NCCL communicator over the process group
+        (comm.SessionComm; torch.distributed only bootstraps it)."""
+        if getattr(self, "_scomm", None) is None:
+            from .comm import SessionComm
 
+            self._scomm = SessionComm(self.pg, self.problem.device)
+        return self._scomm
+
+    def _allreduce_hook(self, works):
         G = self.engine.grad
+        sc = self._comm()
 
         def hook(lo, hi):
-            w = dist.all_reduce(G[lo:hi], group=self.pg, async_op=True)
+            w = sc.allreduce_async(G[lo:hi])
             works.append(w)
             return w
 
@@ -227,22 +235,20 @@ class DeviceSession:
 
     # ------------------------------------------------------------ steps --
     def _compute_merged(self, wr: torch.Tensor, b: int) -> None:
-        import torch.distributed as dist
-
-        hp, eng, pg = self.hp, self.engine, self.pg
+        hp, eng = self.hp, self.engine
+        sc = self._comm()
         f = eng.first_fc
         eng.forward(wr, b, stop=f)                          # conv part, data parallel
         act, dact = eng.ops[f].inp.value[:b], eng.ops[f].inp.grad[:b]
         labels = eng.labels[:b]
         head = self.head
-        root = dist.get_global_rank(pg, 0) if pg is not dist.group.WORLD else 0
         if self.rank == 0:
             gx = [head.input.value[r * b:(r + 1) * b] for r in range(self.world)]
             gy = [head.labels[r * b:(r + 1) * b] for r in range(self.world)]
         else:
             gx = gy = None
-        dist.gather(act.contiguous(), gx, dst=root, group=pg)
-        dist.gather(labels.contiguous(), gy, dst=root, group=pg)
+        sc.gather_to_root(act.contiguous(), gx)
+        sc.gather_to_root(labels.contiguous(), gy)
         nb = self.world * b
         if self.rank == 0:                                  # FC head on the whole global batch
             Wfc = wr[self.fc_off:]
@@ -256,11 +262,11 @@ class DeviceSession:
             sx = [head.input.grad[r * b:(r + 1) * b] for r in range(self.world)]
         else:
             sx = None
-        dist.scatter(dact, sx, src=root, group=pg)
+        sc.scatter_from_root(dact, sx)
         works = []
 
         def hook(lo, hi):   # conv gradients only; the head's 1/(N b) makes SUM the mean
-            w = dist.all_reduce(eng.grad[lo:hi], group=pg, async_op=True)
+            w = sc.allreduce_async(eng.grad[lo:hi])
             works.append(w)
             return w
 
@@ -386,11 +392,8 @@ class DeviceSession:
         Merged FC: the global-batch loss, computed on rank 0 and broadcast
         (a collective: every rank calls it)."""
         if self.merged_fc:
-            import torch.distributed as dist
-
             buf = (self.head.loss_buf if self.rank == 0 else torch.zeros(1, device=self.W.device))
-            root = dist.get_global_rank(self.pg, 0) if self.pg is not dist.group.WORLD else 0
-            dist.broadcast(buf, src=root, group=self.pg)
+            self._comm().broadcast(buf, 0)
             return float(buf.item())
         return float(self.engine.loss_buf.item())
 
@@ -410,11 +413,9 @@ class DeviceSession:
         (the other ranks never update them).  A collective."""
         if not self.merged_fc:
             return
-        import torch.distributed as dist
-
-        root = dist.get_global_rank(self.pg, 0) if self.pg is not dist.group.WORLD else 0
-        dist.broadcast(self.W[self.fc_off:].contiguous(), src=root, group=self.pg)
-        dist.broadcast(self.V[self.fc_off:].contiguous(), src=root, group=self.pg)
+        sc = self._comm()
+        sc.broadcast(self.W[self.fc_off:], 0)
+        sc.broadcast(self.V[self.fc_off:], 0)
 
     def sync_momentum(self) -> None:
         """Peer-memory mode: each rank holds V only for the parts it updates;
