@@ -32,6 +32,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -90,6 +91,8 @@ struct FParams {
   const float* bias;
   float* Y;
   long long ldy;
+  int debug;          // OMNI_WINDOW_DEBUG (timing probes only): 1 no stores, 2 no window
+                      // reloads after the first STAGES tiles, 4 no MMAs
 };
 
 template <int BN>
@@ -206,8 +209,17 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t win_bytes = (uint32_t)p.win_rows * (C0 + C1) * 4u;
       int stage = 0;
       uint32_t phase = 0;
-      for (int w = unit0; w < p.units; w += units) {
+      int it = 0;
+      for (int w = unit0; w < p.units; w += units, ++it) {
         mbar_wait(empty_bar(stage), phase ^ 1);
+        if ((p.debug & 2) && it >= L::STAGES) {    // probe: reuse the staged window
+          if (rank == 0) mbar_arrive(full_bar(stage));
+          if (++stage == L::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+          continue;
+        }
         if (rank == 0) mbar_expect_tx(full_bar(stage), 2u * win_bytes);
         const uint32_t fb = mapa_rank0(full_bar(stage));
         const int q0 = w * 256 + rank * 128;
@@ -313,7 +325,7 @@ __global__ void __launch_bounds__(256, 1)
           const int ok = __shfl_sync(0xffffffffu, valid, row);
           const int pr = __shfl_sync(0xffffffffu, prow, row);
           const float4 v = *reinterpret_cast<const float4*>(stg + row * L::STG_PITCH + 4 * c4);
-          if (ok) *reinterpret_cast<float4*>(p.Y + (long long)pr * p.ldy + c0 + 4 * c4) = v;
+          if (ok && !(p.debug & 1)) *reinterpret_cast<float4*>(p.Y + (long long)pr * p.ldy + c0 + 4 * c4) = v;
         }
         __syncwarp();
       }
@@ -634,6 +646,7 @@ int omni_conv_window_f32(int op, const float* Xs, int b, int n2, int cp, int k2,
     p.bias = bias;
     p.Y = Y;
     p.ldy = ldy;
+    p.debug = getenv("OMNI_WINDOW_DEBUG") ? atoi(getenv("OMNI_WINDOW_DEBUG")) : 0;
     switch (d_out) {
       case 32: return cwin::launch_fprop<32>(p, x0, x1, w0, w1, st);
       case 64: return cwin::launch_fprop<64>(p, x0, x1, w0, w1, st);
