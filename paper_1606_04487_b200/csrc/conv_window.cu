@@ -112,8 +112,12 @@ struct FLayout {
   static constexpr int STG_PITCH = 36;               // floats per staged row (32 + 4: conflict-free)
   static constexpr int STG_OFF = BIAS_OFF + 512;     // 4 warps x 32 rows x STG_PITCH floats
   static constexpr int BYTES = STG_OFF + 4 * 32 * STG_PITCH * 4 + 1024;
-  static constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : 256);
-  static constexpr int ACC_STRIDE = TMEM_COLS / 2;
+  // a ring of NACC accumulators: tiles are short (54 MMAs), so the MMA warp
+  // runs up to NACC - 1 tiles ahead of the epilogue and the cross-CTA
+  // handoffs (commit -> epilogue -> release) overlap instead of pacing tiles
+  static constexpr int NACC = 4;
+  static constexpr int ACC_STRIDE = BN <= 32 ? 32 : (BN <= 64 ? 64 : 128);
+  static constexpr int TMEM_COLS = NACC * ACC_STRIDE <= 128 ? 128 : (NACC * ACC_STRIDE <= 256 ? 256 : 512);
   static_assert(BYTES <= 232448, "fprop window layout exceeds shared memory");
   static_assert(B0_TAP % 1024 == 0 && B1_TAP % 512 == 0 && B1_OFF % 1024 == 0, "swizzle alignment");
 };
@@ -157,10 +161,10 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t bar0 = sbase + L::BAR_OFF;
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 16u + 8u * s; };
-  auto tfull_bar = [&](int a) { return bar0 + 32u + 8u * a; };
-  auto tempty_bar = [&](int a) { return bar0 + 48u + 8u * a; };
-  const uint32_t bfull = bar0 + 64u;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::BAR_OFF + 80);
+  auto tfull_bar = [&](int a) { return bar0 + 32u + 8u * a; };    // a < NACC <= 4
+  auto tempty_bar = [&](int a) { return bar0 + 64u + 8u * a; };
+  const uint32_t bfull = bar0 + 96u;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + L::BAR_OFF + 104);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = (int)cluster_ctarank();
@@ -176,7 +180,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < L::NACC; ++a) {
       mbar_init(tfull_bar(a), 1);
       mbar_init(tempty_bar(a), 8);  // 4 epilogue warps x 2 CTAs
     }
@@ -272,8 +276,10 @@ __global__ void __launch_bounds__(256, 1)
           stage = 0;
           phase ^= 1;
         }
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if (++acc == L::NACC) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
       }
     }
   } else if (warp >= 4) {
@@ -329,8 +335,10 @@ __global__ void __launch_bounds__(256, 1)
         }
         __syncwarp();
       }
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (++acc == L::NACC) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
     }
   }
 

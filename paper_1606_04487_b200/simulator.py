@@ -39,6 +39,10 @@ class SimConfig:
     init: Optional[SGDState] = None
     loss_sample_interval: int = 1
     record_models: bool = False
+    # (extension, not in the reference) stop once the mean of the last
+    # `target_window` sampled losses is <= target_loss -- time-to-target sweeps
+    target_loss: Optional[float] = None
+    target_window: int = 50
 
     def __post_init__(self) -> None:
         if self.service_mode not in ("deterministic", "exponential"):
@@ -221,6 +225,9 @@ def _simulate(cfg: SimConfig, on_write=None) -> SimTrace:
             loss_values.append(loss)
             if not np.isfinite(loss) or loss > bound:
                 diverged = True
+            elif cfg.target_loss is not None and \
+                    float(np.mean(loss_values[-cfg.target_window:])) <= cfg.target_loss:
+                break
         if diverged:
             break
         cd, nfs = draw(i)
