@@ -447,7 +447,7 @@ def run_ours(args):
     peak_src = ("cuBLAS TF32 8192^3 measured in this run (burst), "
                 + ("/ 3 (3xTF32: three tf32 MMAs per product)" if args.precision == "3xtf32" else "of measured"))
     traffic, traffic_src = None, None
-    tpath = os.path.join(ROOT, "profiles", "r01_traffic_summary.json")
+    tpath = os.path.join(ROOT, "profiles", "r02_traffic_summary.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
             ts = json.load(f)

@@ -109,9 +109,15 @@ struct FLayout {
   static constexpr int STAGE_OFF = B_ALLOC;
   static constexpr int BAR_OFF = STAGE_OFF + STAGES * STAGE;
   static constexpr int BIAS_OFF = BAR_OFF + 256;    // BN floats
-  static constexpr int STG_PITCH = 36;               // floats per staged row (32 + 4: conflict-free)
-  static constexpr int STG_OFF = BIAS_OFF + 512;     // 4 warps x 32 rows x STG_PITCH floats
-  static constexpr int BYTES = STG_OFF + 4 * 32 * STG_PITCH * 4 + 1024;
+  // epilogue: EPI sets of 4 warps, set e drains accumulator columns
+  // [e*CS, (e+1)*CS) of the 128 TMEM lanes (tiles are short: one set of four
+  // warps cannot drain 96 columns as fast as the MMA warp fills them)
+  static constexpr int EPI = BN <= 96 ? 2 : 1;
+  static constexpr int CS = BN / EPI;
+  static constexpr int THREADS = 128 + 128 * EPI;
+  static constexpr int STG_PITCH = 20;               // floats per staged row (16 + 4: conflict-free)
+  static constexpr int STG_OFF = BIAS_OFF + 512;     // 4*EPI warps x 32 rows x STG_PITCH floats
+  static constexpr int BYTES = STG_OFF + 4 * EPI * 32 * STG_PITCH * 4 + 1024;
   // a ring of NACC accumulators: tiles are short (54 MMAs), so the MMA warp
   // runs up to NACC - 1 tiles ahead of the epilogue and the cross-CTA
   // handoffs (commit -> epilogue -> release) overlap instead of pacing tiles
@@ -130,26 +136,23 @@ __device__ __forceinline__ float fepi(float acc, const float* bias, int col) {  
   return acc;
 }
 
-// Apply the epilogue to one lane's 32 accumulator columns and stage them as
-// that lane's row of the warp's 32 x 32 staging tile (pitch 36 floats).
+// Apply the epilogue to one lane's 16 accumulator columns and stage them as
+// that lane's row of the warp's 32 x 16 staging tile (pitch 20 floats).
 template <int MODE>
-__device__ __forceinline__ void fstage32(float* srow, const uint32_t (&r0)[16], const uint32_t (&r1)[16],
-                                         const float* bias, int c0) {
+__device__ __forceinline__ void fstage16(float* srow, const uint32_t (&r)[16], const float* bias, int c0) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t* r = j < 4 ? r0 : r1;
-    const int k = (j & 3) * 4;
+  for (int j = 0; j < 4; ++j) {
     float4 v;
-    v.x = fepi<MODE>(__uint_as_float(r[k]), bias, c0 + 4 * j);
-    v.y = fepi<MODE>(__uint_as_float(r[k + 1]), bias, c0 + 4 * j + 1);
-    v.z = fepi<MODE>(__uint_as_float(r[k + 2]), bias, c0 + 4 * j + 2);
-    v.w = fepi<MODE>(__uint_as_float(r[k + 3]), bias, c0 + 4 * j + 3);
+    v.x = fepi<MODE>(__uint_as_float(r[4 * j]), bias, c0 + 4 * j);
+    v.y = fepi<MODE>(__uint_as_float(r[4 * j + 1]), bias, c0 + 4 * j + 1);
+    v.z = fepi<MODE>(__uint_as_float(r[4 * j + 2]), bias, c0 + 4 * j + 2);
+    v.w = fepi<MODE>(__uint_as_float(r[4 * j + 3]), bias, c0 + 4 * j + 3);
     *reinterpret_cast<float4*>(srow + 4 * j) = v;
   }
 }
 
 template <int BN>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(FLayout<BN>::THREADS, 1)
     conv_window_fprop_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ CUtensorMap tmX1,
                              const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW1,
                              const FParams p) {
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < L::NACC; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(tempty_bar(a), 8 * L::EPI);  // 4 * EPI epilogue warps x 2 CTAs
     }
     mbar_init(bfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -284,12 +287,14 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ---- epilogue: TMEM -> bias / ReLU -> NHWC rows (junk rows skipped) --
-    const int ew = warp - 4;
+    const int ew = warp & 3;                 // TMEM lane quarter (rows ew*32 ..)
+    const int es = (warp - 4) >> 2;          // column set
     float* sbias = reinterpret_cast<float*>(smem + L::BIAS_OFF);
     if (p.bias) {
-      for (int i = threadIdx.x - 128; i < BN; i += 128) sbias[i] = __ldg(p.bias + i);
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      for (int i = threadIdx.x - 128; i < BN; i += 128 * L::EPI) sbias[i] = __ldg(p.bias + i);
+      asm volatile("bar.sync 1, %0;" ::"n"(128 * L::EPI) : "memory");
     }
+    float* stg = reinterpret_cast<float*>(smem + L::STG_OFF) + (warp - 4) * 32 * L::STG_PITCH;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int w = unit0; w < p.units; w += units) {
@@ -301,37 +306,37 @@ __global__ void __launch_bounds__(256, 1)
       const int h = r / p.n2, x = r - (r / p.n2) * p.n2;
       const int valid = (img < p.b && h < p.m && x < p.m) ? 1 : 0;
       const int prow = valid ? (img * p.m + h) * p.m + x : 0;   // output pixel of this lane's row
-      const uint32_t t_row = tmem_base + (uint32_t)(acc * L::ACC_STRIDE) + ((uint32_t)(ew * 32) << 16);
-      float* stg = reinterpret_cast<float*>(smem + L::STG_OFF) + ew * 32 * L::STG_PITCH;
-      // all of this row's accumulator columns in one batch of TMEM loads,
-      // then the accumulator goes straight back to the MMA warp
-      uint32_t racc[BN / 16][16];
+      const uint32_t t_row = tmem_base + (uint32_t)(acc * L::ACC_STRIDE + es * L::CS) + ((uint32_t)(ew * 32) << 16);
+      // this set's accumulator columns in one batch of TMEM loads, then the
+      // accumulator goes straight back to the MMA warp
+      uint32_t racc[L::CS / 16][16];
 #pragma unroll
-      for (int j = 0; j < BN / 16; ++j) tmem_ld16(t_row + (uint32_t)(16 * j), racc[j]);
+      for (int j = 0; j < L::CS / 16; ++j) tmem_ld16(t_row + (uint32_t)(16 * j), racc[j]);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster_relaxed(mapa_rank0(tempty_bar(acc)));
+      float* srow = stg + lane * L::STG_PITCH;
+      const float* yb = p.Y + es * L::CS;
 #pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        const uint32_t(&r0)[16] = racc[c0 / 16];
-        const uint32_t(&r1)[16] = racc[c0 / 16 + 1];
-        float* srow = stg + lane * L::STG_PITCH;
+      for (int j = 0; j < L::CS / 16; ++j) {
+        const int c0 = es * L::CS + 16 * j;   // accumulator / output column
         switch (p.epilogue) {
-          case OMNI_EPI_BIAS: fstage32<OMNI_EPI_BIAS>(srow, r0, r1, sbias, c0); break;
-          case OMNI_EPI_BIAS_RELU: fstage32<OMNI_EPI_BIAS_RELU>(srow, r0, r1, sbias, c0); break;
-          case OMNI_EPI_RELU: fstage32<OMNI_EPI_RELU>(srow, r0, r1, sbias, c0); break;
-          default: fstage32<OMNI_EPI_STORE>(srow, r0, r1, sbias, c0); break;
+          case OMNI_EPI_BIAS: fstage16<OMNI_EPI_BIAS>(srow, racc[j], sbias, c0); break;
+          case OMNI_EPI_BIAS_RELU: fstage16<OMNI_EPI_BIAS_RELU>(srow, racc[j], sbias, c0); break;
+          case OMNI_EPI_RELU: fstage16<OMNI_EPI_RELU>(srow, racc[j], sbias, c0); break;
+          default: fstage16<OMNI_EPI_STORE>(srow, racc[j], sbias, c0); break;
         }
         __syncwarp();
-        // coalesced store: each instruction writes 4 whole 128-byte row segments
+        // coalesced store: each instruction writes 8 whole 64-byte row segments
 #pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int row = it * 4 + (lane >> 3), c4 = lane & 7;
+        for (int it = 0; it < 4; ++it) {
+          const int row = it * 8 + (lane >> 2), c4 = lane & 3;
           const int ok = __shfl_sync(0xffffffffu, valid, row);
           const int pr = __shfl_sync(0xffffffffu, prow, row);
           const float4 v = *reinterpret_cast<const float4*>(stg + row * L::STG_PITCH + 4 * c4);
-          if (ok && !(p.debug & 1)) *reinterpret_cast<float4*>(p.Y + (long long)pr * p.ldy + c0 + 4 * c4) = v;
+          if (ok && !(p.debug & 1))
+            *reinterpret_cast<float4*>(const_cast<float*>(yb) + (long long)pr * p.ldy + 16 * j + 4 * c4) = v;
         }
         __syncwarp();
       }
@@ -580,7 +585,7 @@ int launch_fprop(const FParams& p, const CUtensorMap& x0, const CUtensorMap& x1,
   const int grid = 2 * (p.units < pairs ? p.units : pairs);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(L::THREADS);
   cfg.dynamicSmemBytes = L::BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
