@@ -112,7 +112,7 @@ struct FLayout {
   // epilogue: EPI sets of 4 warps, set e drains accumulator columns
   // [e*CS, (e+1)*CS) of the 128 TMEM lanes (tiles are short: one set of four
   // warps cannot drain 96 columns as fast as the MMA warp fills them)
-  static constexpr int EPI = BN <= 96 ? 2 : 1;
+  static constexpr int EPI = 2;
   static constexpr int CS = BN / EPI;
   static constexpr int THREADS = 128 + 128 * EPI;
   static constexpr int STG_PITCH = 20;               // floats per staged row (16 + 4: conflict-free)
@@ -129,24 +129,25 @@ struct FLayout {
 };
 
 template <int MODE>
-__device__ __forceinline__ float fepi(float acc, const float* bias, int col) {   // bias: shared memory
+__device__ __forceinline__ float fepi(float acc, const float* bias, int col) {
   if (MODE == OMNI_EPI_BIAS) return acc + bias[col];
   if (MODE == OMNI_EPI_BIAS_RELU) return fmaxf(acc + bias[col], 0.f);
   if (MODE == OMNI_EPI_RELU) return fmaxf(acc, 0.f);
   return acc;
 }
 
-// Apply the epilogue to one lane's 16 accumulator columns and stage them as
-// that lane's row of the warp's 32 x 16 staging tile (pitch 20 floats).
+// Apply the epilogue to one lane's 16 accumulator columns (bias: the 16
+// matching values, in registers) and stage them as that lane's row of the
+// warp's 32 x 16 staging tile (pitch 20 floats).
 template <int MODE>
-__device__ __forceinline__ void fstage16(float* srow, const uint32_t (&r)[16], const float* bias, int c0) {
+__device__ __forceinline__ void fstage16(float* srow, const uint32_t (&r)[16], const float* b16) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     float4 v;
-    v.x = fepi<MODE>(__uint_as_float(r[4 * j]), bias, c0 + 4 * j);
-    v.y = fepi<MODE>(__uint_as_float(r[4 * j + 1]), bias, c0 + 4 * j + 1);
-    v.z = fepi<MODE>(__uint_as_float(r[4 * j + 2]), bias, c0 + 4 * j + 2);
-    v.w = fepi<MODE>(__uint_as_float(r[4 * j + 3]), bias, c0 + 4 * j + 3);
+    v.x = fepi<MODE>(__uint_as_float(r[4 * j]), b16, 4 * j);
+    v.y = fepi<MODE>(__uint_as_float(r[4 * j + 1]), b16, 4 * j + 1);
+    v.z = fepi<MODE>(__uint_as_float(r[4 * j + 2]), b16, 4 * j + 2);
+    v.w = fepi<MODE>(__uint_as_float(r[4 * j + 3]), b16, 4 * j + 3);
     *reinterpret_cast<float4*>(srow + 4 * j) = v;
   }
 }
@@ -289,11 +290,11 @@ __global__ void __launch_bounds__(FLayout<BN>::THREADS, 1)
     // ---- epilogue: TMEM -> bias / ReLU -> NHWC rows (junk rows skipped) --
     const int ew = warp & 3;                 // TMEM lane quarter (rows ew*32 ..)
     const int es = (warp - 4) >> 2;          // column set
-    float* sbias = reinterpret_cast<float*>(smem + L::BIAS_OFF);
-    if (p.bias) {
-      for (int i = threadIdx.x - 128; i < BN; i += 128 * L::EPI) sbias[i] = __ldg(p.bias + i);
-      asm volatile("bar.sync 1, %0;" ::"n"(128 * L::EPI) : "memory");
-    }
+    // this set's bias values live in registers for the whole launch (a
+    // shared-memory operand per element made the epilogue instruction-bound)
+    float breg[L::CS];
+#pragma unroll
+    for (int j = 0; j < L::CS; ++j) breg[j] = p.bias ? __ldg(p.bias + es * L::CS + j) : 0.f;
     float* stg = reinterpret_cast<float*>(smem + L::STG_OFF) + (warp - 4) * 32 * L::STG_PITCH;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -320,12 +321,11 @@ __global__ void __launch_bounds__(FLayout<BN>::THREADS, 1)
       const float* yb = p.Y + es * L::CS;
 #pragma unroll
       for (int j = 0; j < L::CS / 16; ++j) {
-        const int c0 = es * L::CS + 16 * j;   // accumulator / output column
         switch (p.epilogue) {
-          case OMNI_EPI_BIAS: fstage16<OMNI_EPI_BIAS>(srow, racc[j], sbias, c0); break;
-          case OMNI_EPI_BIAS_RELU: fstage16<OMNI_EPI_BIAS_RELU>(srow, racc[j], sbias, c0); break;
-          case OMNI_EPI_RELU: fstage16<OMNI_EPI_RELU>(srow, racc[j], sbias, c0); break;
-          default: fstage16<OMNI_EPI_STORE>(srow, racc[j], sbias, c0); break;
+          case OMNI_EPI_BIAS: fstage16<OMNI_EPI_BIAS>(srow, racc[j], breg + 16 * j); break;
+          case OMNI_EPI_BIAS_RELU: fstage16<OMNI_EPI_BIAS_RELU>(srow, racc[j], breg + 16 * j); break;
+          case OMNI_EPI_RELU: fstage16<OMNI_EPI_RELU>(srow, racc[j], breg + 16 * j); break;
+          default: fstage16<OMNI_EPI_STORE>(srow, racc[j], breg + 16 * j); break;
         }
         __syncwarp();
         // coalesced store: each instruction writes 8 whole 64-byte row segments
