@@ -503,6 +503,14 @@ def run_ours(args):
                        "stream overlapping step(); every step's loss read on the host via "
                        "loss_future() (async D2H, read one step later)"}
 
+    # the reference's own call shapes through the drop-in API (float64 NCHW
+    # host batches; reported beside e2e, not the headline): run_sync
+    # (sgd.py:210-256, device session, full-dataset loss sampled every 5 steps)
+    # and the TrainingProblem.grad + sgd_step pair a user's loop calls
+    dropin = None
+    if rank == 0 and world == 1 and not args.no_e2e:
+        dropin = measure_dropin(net, b, args, prob, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(net, b, args.seed)
@@ -531,6 +539,7 @@ def run_ours(args):
                          "conv_gemm_share_of_step": conv_ms / (ms / args.steps)},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "dropin_api": dropin,
             "gpu_launches": launches_per_step * args.steps,
             "gpu_launches_source": "omni_launch_count() delta over one eager step x steps "
                                    "(graph replays launch the same kernels)",
@@ -540,6 +549,41 @@ def run_ours(args):
         emit(line)
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_dropin(net, b, args, prob, dev) -> dict:
+    """images/s through the reference-shaped API: (1) run_sync for 10 steps
+    (device session; full-dataset loss every 5 steps, the reference's
+    sampling option), (2) problem.grad(W, (X, y)) with X a float64 NCHW host
+    array + sgd_step on float64 host state -- the per-call host<->device
+    traffic of the drop-in boundary included."""
+    import torch
+
+    from paper_1606_04487_b200.sgd import Hyperparams, SGDState, StopRule, run_sync, sgd_step
+
+    hp = Hyperparams(eta=args.eta, mu=args.mu, lam=args.lam, b=b)
+    state = SGDState.fresh(0.01 * np.random.default_rng(args.seed).standard_normal(net.dim))
+    torch.cuda.synchronize()
+    run_sync(prob, hp, state, StopRule(max_steps=2), seed=args.seed, sample_interval=2)   # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    run_sync(prob, hp, state, StopRule(max_steps=10), seed=args.seed, sample_interval=5)
+    torch.cuda.synchronize()
+    rs = 10 * b / (time.perf_counter() - t0)
+    rng = np.random.default_rng(args.seed)
+    X = rng.standard_normal((b, net.in_channels, net.in_size, net.in_size))
+    y = rng.integers(0, net.classes, size=b)
+    st = state
+    g = prob.grad(st.W, (X, y))                     # warm-up
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        g = prob.grad(st.W, (X, y))
+        st = sgd_step(st, hp, g, st.W)
+    ga = reps * b / (time.perf_counter() - t0)
+    return {"run_sync_images_per_s": rs, "grad_sgd_step_images_per_s": ga,
+            "path": "run_sync(CNNProblem, ...) 10 steps (device session, full loss every 5); "
+                    "problem.grad(W_f64, (X_f64 NCHW, y)) + sgd_step(float64 state) on host arrays"}
 
 
 def run_groups(args, net, dev, world, rank, local):

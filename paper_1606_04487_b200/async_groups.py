@@ -276,7 +276,13 @@ def run_server_merged(plan: ExecutionPlan, head, hp: Hyperparams, W0: torch.Tens
     events = []
     t = fc_t = 0
     t0 = time.perf_counter()
-    Wfc, Vfc = W[fc_off:], V[fc_off:]
+    # the head stages its weights from a 16-byte aligned vector (TMA): when the
+    # FC parameters do not start on a 4-float boundary (LeNet: fc_off % 4 = 2)
+    # the server keeps them in their own aligned buffers and writes them back
+    # into W / V when it returns
+    aligned = fc_off % 4 == 0
+    Wfc = W[fc_off:] if aligned else W[fc_off:].clone()
+    Vfc = V[fc_off:] if aligned else V[fc_off:].clone()
     while t < max_updates:
         i = None
         while i is None:
@@ -336,6 +342,9 @@ def run_server_merged(plan: ExecutionPlan, head, hp: Hyperparams, W0: torch.Tens
                 continue
             dist.send(stop, dst=leaders[i], group=pair[i])
             break
+    if not aligned:
+        W[fc_off:].copy_(Wfc)
+        V[fc_off:].copy_(Vfc)
     return events, W, V, seconds
 
 
@@ -379,7 +388,9 @@ def replay_merged(events: list, plan: ExecutionPlan, eng, head, problem, hp: Hyp
     b = hp.b
     W = W0.clone()
     V = torch.zeros_like(W)
-    Wfc, Vfc = W[fc_off:], V[fc_off:]
+    aligned = fc_off % 4 == 0                        # (see run_server_merged)
+    Wfc = W[fc_off:] if aligned else W[fc_off:].clone()
+    Vfc = V[fc_off:] if aligned else V[fc_off:].clone()
     rngs = [batch_stream(seed, i) for i in range(plan.g)]
     snaps = [W0.clone() for _ in range(plan.g)]      # full-size vectors; conv part used
     idx_of = {}
@@ -406,4 +417,7 @@ def replay_merged(events: list, plan: ExecutionPlan, eng, head, problem, hp: Hyp
             K.sgd_momentum(W[:fc_off], V[:fc_off], eng.grad[:fc_off], snaps[i][:fc_off],
                            hp.eta, hp.mu, hp.lam)
             snaps[i][:fc_off].copy_(W[:fc_off])
+    if not aligned:
+        W[fc_off:].copy_(Wfc)
+        V[fc_off:].copy_(Vfc)
     return W, V

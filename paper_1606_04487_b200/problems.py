@@ -336,7 +336,13 @@ class DeviceSession:
 
     def step(self, batch: Any, w_read: torch.Tensor | None = None) -> None:
         """V = mu V - eta (grad(w_read) + lam w_read); W += V, with w_read = W when
-        synchronous (sgd.py:104-112).
+        synchronous (sgd.py:104-112).  Runs on the problem's device (its current
+        stream), whichever device the caller has current."""
+        with torch.cuda.device(self.problem.device):
+            self._step(batch, w_read)
+
+    def _step(self, batch: Any, w_read: torch.Tensor | None = None) -> None:
+        """(step's body)
 
         Single-GPU steps on full device batches or prefetched host batches are
         captured in a CUDA graph on their second occurrence and replayed after."""
@@ -522,17 +528,29 @@ class CNNProblem(TrainingProblem):
         return batch.size if isinstance(batch, (Batch, HostBatch, DeviceBatch)) else len(batch[1])
 
     def loss(self, W, batch) -> float:
+        with torch.cuda.device(self.device):
+            return self._loss(W, batch)
+
+    def _loss(self, W, batch) -> float:
         e = self.engine(self._batch_size(batch))
         b = self.load_batch(e, batch)
         return float(e.forward(self._w(W), b, need_grad=False).item())
 
     def grad(self, W, batch) -> np.ndarray:
+        with torch.cuda.device(self.device):   # launches go to this problem's device / stream
+            return self._grad(W, batch)
+
+    def _grad(self, W, batch) -> np.ndarray:
         e = self.engine(self._batch_size(batch))
         b = self.load_batch(e, batch)
         _, G = e.loss_and_grad(self._w(W), b)
         return G.double().cpu().numpy()
 
     def full_loss_device(self, Wd: torch.Tensor, chunk: int = 256) -> float:
+        with torch.cuda.device(self.device):
+            return self._full_loss_device(Wd, chunk)
+
+    def _full_loss_device(self, Wd: torch.Tensor, chunk: int = 256) -> float:
         n = self._n
         e = self.engine(min(n, chunk))
         tot = torch.zeros(1, dtype=torch.float64, device=self.device)
@@ -551,6 +569,10 @@ class CNNProblem(TrainingProblem):
 
     def full_grad_device(self, Wd: torch.Tensor, chunk: int = 256) -> torch.Tensor:
         """Mean gradient over the whole dataset at device weights (float64, on device)."""
+        with torch.cuda.device(self.device):
+            return self._full_grad_device(Wd, chunk)
+
+    def _full_grad_device(self, Wd: torch.Tensor, chunk: int = 256) -> torch.Tensor:
         n = self._n
         e = self.engine(min(n, chunk))
         acc = torch.zeros(self.dim, dtype=torch.float64, device=self.device)
