@@ -182,7 +182,13 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
                      const __grid_constant__ CUtensorMap tmO, const Params p) {
   // K-major operands hold exactly one 128-byte swizzle row (32 fp32) per stage;
   // deeper stages are for MN-major operands only.
-  static_assert(BKT == BK || (A_MN && B_MN), "BKT > 32 needs MN-major operands");
+  // BKT = K per pipeline stage.  MN-major operands stage BKT K-rows directly;
+  // K-major operands stage KSUB = BKT / 32 sub-tiles of one 128-byte swizzle
+  // row each (64-deep stages halve the stages, barriers and TMA issues per
+  // byte -- the per-stage cost bounds the short-tile conv / FC GEMMs).
+  static_assert(BKT == BK || BKT == 2 * BK, "BKT must be 32 or 64");
+  static_assert(IM2COL != 4 || BKT == BK, "the transposed im2col form stages 32-deep");
+  constexpr int KSUB = BKT / BK;
   // 3xTF32 on CTA pairs: each CTA's TMA signals its OWN full barrier (its
   // converter warps must see its stage land), each CTA splits its own half of
   // the stage, and the converters' per-warp arrivals gather on CTA 0's
@@ -306,8 +312,9 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
         // IM2COL 1/4: (channel block, tap) cursor of k-tile kt, tap-major K
         int t_cb = 0, t_kx = 0, t_ky = 0;
         if (IM2COL == 1 || IM2COL == 4) {
-          const int tap = kt0 / p.conv_cblocks;
-          t_cb = kt0 - tap * p.conv_cblocks;
+          const int blk0 = kt0 * KSUB;   // first 32-wide K block of this work unit
+          const int tap = blk0 / p.conv_cblocks;
+          t_cb = blk0 - tap * p.conv_cblocks;
           t_kx = tap / p.conv_k;
           t_ky = tap - t_kx * p.conv_k;
         }
@@ -330,8 +337,22 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
           const int kc = kt * BKT;
           const int px_h0 = px_oh * p.conv_s - p.conv_pad, px_w0 = px_ow * p.conv_s - p.conv_pad;
           if (IM2COL == 1) {
-            // K index = (tap, channel): tap-major, 32-channel blocks
-            load_im2col(&tmA, a_dst, t_cb * 32, a_w0, a_h0, a_img, (uint16_t)t_ky, (uint16_t)t_kx);
+            // K index = (tap, channel): tap-major, 32-channel blocks, KSUB per stage
+#pragma unroll
+            for (int sub = 0; sub < KSUB; ++sub) {
+              // past the last block (odd block count): reload the last one, the MMA skips it
+              const bool past = t_kx >= p.conv_k;
+              load_im2col(&tmA, a_dst + sub * (BM * 128), (past ? p.conv_cblocks - 1 : t_cb) * 32, a_w0,
+                          a_h0, a_img, (uint16_t)(past ? p.conv_k - 1 : t_ky),
+                          (uint16_t)(past ? p.conv_k - 1 : t_kx));
+              if (++t_cb == p.conv_cblocks) {
+                t_cb = 0;
+                if (++t_ky == p.conv_k) {
+                  t_ky = 0;
+                  ++t_kx;
+                }
+              }
+            }
           } else if (IM2COL == 3) {
             // A(i = (tap, ch), r = pixel): BKT output pixels x 32 channels per 32-row chunk
 #pragma unroll
@@ -343,7 +364,8 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
                             (uint16_t)ch_ky[j], (uint16_t)ch_kx[j]);
             }
           } else if (!A_MN) {
-            load2d(&tmA, a_dst, kc, arow);
+#pragma unroll
+            for (int sub = 0; sub < KSUB; ++sub) load2d(&tmA, a_dst + sub * (BM * 128), kc + 32 * sub, arow);
           } else {
 #pragma unroll
             for (int j = 0; j < BM / 32; ++j)
@@ -359,14 +381,15 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
               load_im2col(&tmB, b_dst + j * (BKT * 128), ch_c[j], px_w0, px_h0, px_img,
                           (uint16_t)ch_ky[j], (uint16_t)ch_kx[j]);
           } else if (!B_MN) {
-            load2d(&tmB, b_dst, kc, bcol);
+#pragma unroll
+            for (int sub = 0; sub < KSUB; ++sub) load2d(&tmB, b_dst + sub * (BNL * 128), kc + 32 * sub, bcol);
           } else {
 #pragma unroll
             for (int j = 0; j < BNL / 32; ++j)
               load2d(&tmB, b_dst + j * (BKT * 128), bcol + 32 * j, kc);
           }
-          // advance the K cursors by one k-tile
-          if (IM2COL == 1 || IM2COL == 4) {
+          // advance the K cursors by one k-tile (IM2COL 1 advanced per sub-tile above)
+          if (IM2COL == 4) {
             if (++t_cb == p.conv_cblocks) {
               t_cb = 0;
               if (++t_ky == p.conv_k) {
@@ -419,8 +442,10 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
           const uint32_t b_addr = a_addr + L::A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BKT / 8; ++kk) {
-            const uint32_t a_off = A_MN ? kk * 1024u : kk * 32u;
-            const uint32_t b_off = B_MN ? kk * 1024u : kk * 32u;
+            // an odd number of 32-wide K blocks: the last stage's second sub-tile is past K
+            if (KSUB > 1 && kk > 0 && (kk & 3) == 0 && kt * BKT + kk * 8 >= p.K) break;
+            const uint32_t a_off = A_MN ? kk * 1024u : (uint32_t)(kk >> 2) * (BM * 128u) + (kk & 3) * 32u;
+            const uint32_t b_off = B_MN ? kk * 1024u : (uint32_t)(kk >> 2) * (BNL * 128u) + (kk & 3) * 32u;
             const uint64_t ad = smem_desc<A_MN, BKT>(a_addr + a_off);
             const uint64_t bd = smem_desc<B_MN, BKT>(b_addr + b_off);
             if (CTA2) tc_mma_tf32_pair(d_tmem, ad, bd, idesc, (kt > kt0 || kk > 0) ? 1u : 0u);
@@ -463,7 +488,7 @@ __global__ void __launch_bounds__(Layout<BN, SPLIT3, BKT, CTA2>::THREADS, 1)
       tc_fence_before();
       if (CTA2) {
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(mapa_rank0(tempty_bar(a)));
+        if (lane == 0) mbar_arrive_cluster_relaxed(mapa_rank0(tempty_bar(a)));  // TMEM reads only: no store drain
       } else {
         mbar_arrive(tempty_bar(a));
       }
@@ -845,6 +870,16 @@ int wgrad_bkt(int precision) {
   return (precision == OMNI_PREC_TF32 && env == 64) ? 64 : BK;
 }
 
+// Stage depth of every launch: 64-deep for TF32 plain GEMMs (FC) and implicit
+// forward / data-gradient convs (OMNI_KMAJOR_BKT=32 for the 32-deep variant);
+// the transposed im2col form and 3xTF32 (hi/lo copies double the stage) 32.
+int stage_bkt(int precision, int im2col) {
+  static const int env = getenv("OMNI_KMAJOR_BKT") ? atoi(getenv("OMNI_KMAJOR_BKT")) : 64;
+  if (im2col == 3) return wgrad_bkt(precision);
+  if ((im2col == 0 || im2col == 1) && precision == OMNI_PREC_TF32 && env == 64) return 64;
+  return BK;
+}
+
 Plan make_plan(int M, int N, int K, int sms, int bkt = BK, bool cta2 = false, bool b_mn = false) {
   Plan pl{};
   pl.cta2 = cta2;
@@ -934,7 +969,7 @@ bool pair_ok(int precision, int M, int im2col) {
 Plan plan_for(int precision, int M, int N, int K, bool b_mn, int im2col) {
   int dev = 0;
   cudaGetDevice(&dev);
-  const int bkt = im2col == 3 ? wgrad_bkt(precision) : BK;
+  const int bkt = stage_bkt(precision, im2col);
   const bool b_mn_eff = b_mn || im2col == 2 || im2col == 3;
   // SMs left free for concurrent communication kernels (data parallel: the
   // persistent GEMM grids would otherwise hold every SM and delay NCCL)
@@ -1083,13 +1118,13 @@ int dispatch_bn(const Plan& pl, const float* A, long long lda, const float* B, l
   return dispatch_bn_t<A_MN, B_MN, SPLIT3, IM2COL, BKT, false>(pl, A, lda, B, ldb, p, st, cg, ones);
 }
 
-template <bool SPLIT3>
+template <bool SPLIT3, int BKT = BK>
 int dispatch_major(const Plan& pl, int a_mn, int b_mn, const float* A, long long lda,
                    const float* B, long long ldb, const Params& p, cudaStream_t st) {
-  if (!a_mn && !b_mn) return dispatch_bn<false, false, SPLIT3, 0>(pl, A, lda, B, ldb, p, st);
-  if (!a_mn && b_mn) return dispatch_bn<false, true, SPLIT3, 0>(pl, A, lda, B, ldb, p, st);
-  if (a_mn && !b_mn) return dispatch_bn<true, false, SPLIT3, 0>(pl, A, lda, B, ldb, p, st);
-  return dispatch_bn<true, true, SPLIT3, 0>(pl, A, lda, B, ldb, p, st);
+  if (!a_mn && !b_mn) return dispatch_bn<false, false, SPLIT3, 0, BKT>(pl, A, lda, B, ldb, p, st);
+  if (!a_mn && b_mn) return dispatch_bn<false, true, SPLIT3, 0, BKT>(pl, A, lda, B, ldb, p, st);
+  if (a_mn && !b_mn) return dispatch_bn<true, false, SPLIT3, 0, BKT>(pl, A, lda, B, ldb, p, st);
+  return dispatch_bn<true, true, SPLIT3, 0, BKT>(pl, A, lda, B, ldb, p, st);
 }
 
 // Shared tail of omni_gemm_f32 / omni_conv_implicit_f32: plan, workspace,
@@ -1111,7 +1146,7 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
   p.vec_aux = aux && ld_aux % 4 == 0 && ((uintptr_t)aux & 15) == 0;
   // The implicit weight gradient (im2col A, both operands MN-major) runs 64-deep
   // K stages in TF32 mode: half the TMA ops per byte, 64-pixel im2col boxes.
-  const int bkt = im2col == 3 ? wgrad_bkt(precision) : BK;
+  const int bkt = stage_bkt(precision, im2col);
   const Plan pl = plan_for(precision, M, N, K, b_mn != 0, im2col);
   p.m_tiles = pl.m_tiles;
   p.n_tiles = pl.n_tiles;
@@ -1155,7 +1190,8 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
   const bool s3 = precision == OMNI_PREC_3XTF32;
   if (im2col == 1)
     rc = s3 ? dispatch_bn<false, false, true, 1>(pl, A, lda, B, ldb, p, st, cg)
-            : dispatch_bn<false, false, false, 1>(pl, A, lda, B, ldb, p, st, cg);
+       : bkt == 64 ? dispatch_bn<false, false, false, 1, 64>(pl, A, lda, B, ldb, p, st, cg)
+                   : dispatch_bn<false, false, false, 1>(pl, A, lda, B, ldb, p, st, cg);
   else if (im2col == 3)
     rc = s3 ? dispatch_bn<true, true, true, 3>(pl, A, lda, B, ldb, p, st, cg, ones)
        : bkt == 64 ? dispatch_bn<true, true, false, 3, 64>(pl, A, lda, B, ldb, p, st, cg, ones)
@@ -1165,7 +1201,8 @@ int run_gemm(int precision, int M, int N, int K, const float* A, long long lda, 
             : dispatch_bn<false, false, false, 4>(pl, A, lda, B, ldb, p, st, cg);
   else
     rc = s3 ? dispatch_major<true>(pl, a_mn, b_mn ? 1 : 0, A, lda, B, ldb, p, st)
-            : dispatch_major<false>(pl, a_mn, b_mn ? 1 : 0, A, lda, B, ldb, p, st);
+       : bkt == 64 ? dispatch_major<false, 64>(pl, a_mn, b_mn ? 1 : 0, A, lda, B, ldb, p, st)
+                   : dispatch_major<false>(pl, a_mn, b_mn ? 1 : 0, A, lda, B, ldb, p, st);
   if (rc) return rc;
   if (pl.splits > 1) {
     Params q = p;
