@@ -211,6 +211,15 @@ int omni_mailbox_snap_wait(void* box, int group, long long last, long long* seq,
  * W = W + V.  w_read may alias W (synchronous step).                         */
 int omni_sgd_momentum_f32(float* W, float* V, const float* g, const float* w_read, float eta,
                           float mu, float lam, long long n, void* stream);
+/* The g ordered updates of one compute-group round on a shard (groups.py,
+ * simulator.py:123-213 deterministic schedule): rows is nrows x n (pitch ld),
+ * row m = rank m's gradient shard; for i = 0..g-1 in order, group i's gradient
+ * is the sum of rows members[i*k .. i*k+k) in that order, the K8 update
+ * V = mu*V - eta*(G_i + lam*snaps[i]); W += V is applied, and snaps[i] = W
+ * (group i's next snapshot).  members / snaps are host arrays (g*k <= 64).   */
+int omni_group_updates_f32(const float* rows, int nrows, long long ld, const int* members, int g,
+                           int k, float* W, float* V, float* const* snaps, long long n, float eta,
+                           float mu, float lam, void* stream);
 /* K8 in float64 for the drop-in host API (SGDState keeps float64, sgd.py:72-101):
  * same update, the reference's evaluation order, no FMA contraction, so it
  * is bit-identical to the NumPy expression.                                  */
@@ -293,6 +302,15 @@ int omni_allreduce_sum_f32(void* comm, float* buf, size_t n, void* stream);
 int omni_broadcast_f32(void* comm, float* buf, size_t n, int root, void* stream);
 int omni_send_f32(void* comm, const float* buf, size_t n, int peer, void* stream);
 int omni_recv_f32(void* comm, float* buf, size_t n, int peer, void* stream);
+/* recv[r*n .. (r+1)*n) = rank r's send (n floats), every rank (the sharded
+ * group runtime's master-model assembly).                                    */
+int omni_allgather_f32(void* comm, const float* send, float* recv, size_t n, void* stream);
+/* Personalised all-to-all: parts[m] (a host array of nranks device pointers,
+ * n floats each) goes to rank m; rank m's part for this rank lands at
+ * recv + m*n.  The sharded group round's gradient-shard and snapshot-shard
+ * exchanges (groups.py), without staging the parts contiguously.            */
+int omni_all_to_all_f32(void* comm, const float* const* parts, float* recv, size_t n,
+                        void* stream);
 /* Bracket several send/recv calls so NCCL fuses them (no deadlock on
  * simultaneous exchanges).                                                 */
 int omni_comm_group_start(void);

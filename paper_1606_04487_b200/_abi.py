@@ -83,6 +83,7 @@ SIGNATURES: dict[str, tuple] = {
     "omni_bias_grad_f32": (_I, [_P, _L, _I, _I, _P, _P, _P]),
     "omni_sgd_momentum_f32": (_I, [_P, _P, _P, _P, _F, _F, _F, _L, _P]),
     "omni_sgd_momentum_f64": (_I, [_P, _P, _P, _P, _D, _D, _D, _L, _P]),
+    "omni_group_updates_f32": (_I, [_P, _I, _L, _P, _I, _I, _P, _P, _P, _L, _F, _F, _F, _P]),
     "omni_gather_rows_f32": (_I, [_P, _L, _P, _I, _P, _P]),
     "omni_gather_i32": (_I, [_P, _P, _I, _P, _P]),
     "omni_conv_weight_to_tap_f32": (_I, [_P, _I, _I, _I, _P, _L, _I, _P, _P]),
@@ -102,6 +103,8 @@ SIGNATURES: dict[str, tuple] = {
     "omni_broadcast_f32": (_I, [_P, _P, ctypes.c_size_t, _I, _P]),
     "omni_send_f32": (_I, [_P, _P, ctypes.c_size_t, _I, _P]),
     "omni_recv_f32": (_I, [_P, _P, ctypes.c_size_t, _I, _P]),
+    "omni_allgather_f32": (_I, [_P, _P, _P, ctypes.c_size_t, _P]),
+    "omni_all_to_all_f32": (_I, [_P, _P, _P, ctypes.c_size_t, _P]),
     "omni_comm_group_start": (_I, []),
     "omni_comm_group_end": (_I, []),
     "omni_p2p_step": (_I, [_P, _P]),

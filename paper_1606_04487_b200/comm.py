@@ -113,6 +113,25 @@ class Communicator:
         _abi.call("omni_recv_f32", self._h, _buf(t), t.numel(), peer, _stream(stream, t))
         return t
 
+    def allgather(self, t: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+        """out[r*n:(r+1)*n] = rank r's t (n = t.numel())."""
+        if out.numel() < t.numel() * self.size or not out.is_contiguous():
+            raise ValueError("allgather: out must be contiguous with nranks * t.numel() elements")
+        _abi.call("omni_allgather_f32", self._h, _buf(t), _buf(out), t.numel(), _stream(stream, t))
+        return out
+
+    def all_to_all(self, parts: list, recv: torch.Tensor, stream=None) -> torch.Tensor:
+        """parts[m] (n floats each, anywhere in device memory) -> rank m;
+        rank m's part for this rank -> recv[m*n:(m+1)*n]."""
+        n = parts[0].numel()
+        if len(parts) != self.size or any(p.numel() != n or not p.is_contiguous() for p in parts):
+            raise ValueError("all_to_all: one contiguous part of equal length per rank")
+        if recv.numel() < n * len(parts) or not recv.is_contiguous():
+            raise ValueError("all_to_all: recv must be contiguous with nranks * n elements")
+        ptrs = (ctypes.c_void_p * len(parts))(*[p.data_ptr() for p in parts])
+        _abi.call("omni_all_to_all_f32", self._h, ptrs, _buf(recv), n, _stream(stream, recv))
+        return recv
+
     def destroy(self) -> None:
         if self._h.value:
             _abi.call("omni_comm_destroy", self._h)
@@ -397,6 +416,53 @@ class SessionComm:
 
     def close(self) -> None:
         self.comm.destroy()
+
+
+class GroupExchange:
+    """The collectives of groups.GroupRuntime on the library's own NCCL
+    communicators (C-ABI): the world communicator, its split into the g
+    compute groups (color = group, key = member) and into the k cross-group
+    sets (color = member, key = group).  torch.distributed only bootstraps
+    the unique id.  Calls run on the caller's (torch current) stream except
+    ``all_to_all_async``, which runs on a dedicated stream ordered after the
+    caller's work and returns a handle whose ``wait()`` orders the caller
+    after it (the per-layer exchanges overlapping the backward)."""
+
+    def __init__(self, plan, device: torch.device):
+        import torch.distributed as dist
+
+        self.rank = dist.get_rank()
+        uid = [unique_id() if self.rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        self.world = Communicator.init_rank(plan.N, uid[0], self.rank, device.index)
+        self.group = self.world.split(plan.group_of(self.rank), plan.member_of(self.rank))
+        self.cross = self.world.split(plan.member_of(self.rank), plan.group_of(self.rank))
+        self.stream = torch.cuda.Stream(device=device)
+
+    def group_allreduce(self, t: torch.Tensor) -> None:
+        self.group.allreduce_sum(t)
+
+    def cross_allgather(self, t: torch.Tensor, out: torch.Tensor) -> None:
+        """out row i = group i's t (this rank's member index in every group)."""
+        self.cross.allgather(t, out)
+
+    def world_allreduce(self, t: torch.Tensor) -> None:
+        self.world.allreduce_sum(t)
+
+    def world_allgather(self, t: torch.Tensor, out: torch.Tensor) -> None:
+        self.world.allgather(t, out)
+
+    def all_to_all(self, parts: list, recv: torch.Tensor) -> None:
+        self.world.all_to_all(parts, recv)
+
+    def all_to_all_async(self, parts: list, recv: torch.Tensor) -> "_Done":
+        self.stream.wait_stream(torch.cuda.current_stream(recv.device))
+        self.world.all_to_all(parts, recv, stream=self.stream)
+        return _Done(self.stream)
+
+    def close(self) -> None:
+        for c in (self.cross, self.group, self.world):
+            c.destroy()
 
 
 def _f32(t: torch.Tensor) -> torch.Tensor:

@@ -37,6 +37,8 @@ struct Nccl {
                             cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
 };
@@ -68,6 +70,7 @@ void load_nccl() {
             sym(h, "ncclCommDestroy", n.CommDestroy) && sym(h, "ncclCommCount", n.CommCount) &&
             sym(h, "ncclCommUserRank", n.CommUserRank) && sym(h, "ncclAllReduce", n.AllReduce) &&
             sym(h, "ncclBroadcast", n.Broadcast) && sym(h, "ncclSend", n.Send) && sym(h, "ncclRecv", n.Recv) &&
+            sym(h, "ncclAllGather", n.AllGather) &&
             sym(h, "ncclGroupStart", n.GroupStart) && sym(h, "ncclGroupEnd", n.GroupEnd);
   n.ok = ok;
   g_nccl = n;
@@ -200,6 +203,49 @@ int omni_recv_f32(void* comm, float* buf, size_t n, int peer, void* stream) {
   OMNI_REQUIRE(comm != nullptr && (n == 0 || buf != nullptr), "omni_recv_f32: NULL argument");
   OMNI_NCCL_TRY(g_nccl.Recv(buf, n, ncclFloat32, peer, static_cast<ncclComm_t>(comm),
                             omni::as_stream(stream)));
+  return OMNI_OK;
+}
+
+int omni_allgather_f32(void* comm, const float* send, float* recv, size_t n, void* stream) {
+  OMNI_NEED_NCCL();
+  OMNI_REQUIRE(comm != nullptr && (n == 0 || (send != nullptr && recv != nullptr)),
+               "omni_allgather_f32: NULL argument");
+  if (n == 0) return OMNI_OK;
+  OMNI_NCCL_TRY(g_nccl.AllGather(send, recv, n, ncclFloat32, static_cast<ncclComm_t>(comm),
+                                 omni::as_stream(stream)));
+  return OMNI_OK;
+}
+
+// Personalised all-to-all: parts[m] (n floats, any addresses) goes to rank m,
+// rank m's part for this rank lands at recv + m*n.  One NCCL group of
+// 2*(nranks-1) point-to-point calls; the self part is a device copy.
+int omni_all_to_all_f32(void* comm, const float* const* parts, float* recv, size_t n,
+                        void* stream) {
+  OMNI_NEED_NCCL();
+  OMNI_REQUIRE(comm != nullptr && parts != nullptr && (n == 0 || recv != nullptr),
+               "omni_all_to_all_f32: NULL argument");
+  if (n == 0) return OMNI_OK;
+  ncclComm_t c = static_cast<ncclComm_t>(comm);
+  int size = 0, me = 0;
+  OMNI_NCCL_TRY(g_nccl.CommCount(c, &size));
+  OMNI_NCCL_TRY(g_nccl.CommUserRank(c, &me));
+  for (int m = 0; m < size; ++m)
+    OMNI_REQUIRE(parts[m] != nullptr, "omni_all_to_all_f32: NULL part");
+  cudaStream_t st = omni::as_stream(stream);
+  OMNI_CUDA_TRY(cudaMemcpyAsync(recv + (size_t)me * n, parts[me], n * sizeof(float),
+                                cudaMemcpyDeviceToDevice, st));
+  OMNI_NCCL_TRY(g_nccl.GroupStart());
+  for (int m = 0; m < size; ++m) {
+    if (m == me) continue;
+    ncclResult_t r = g_nccl.Send(parts[m], n, ncclFloat32, m, c, st);
+    if (r == ncclSuccess) r = g_nccl.Recv(recv + (size_t)m * n, n, ncclFloat32, m, c, st);
+    if (r != ncclSuccess) {
+      g_nccl.GroupEnd();
+      omni::set_error("omni_all_to_all_f32: %s", g_nccl.GetErrorString(r));
+      return OMNI_ECUDA;
+    }
+  }
+  OMNI_NCCL_TRY(g_nccl.GroupEnd());
   return OMNI_OK;
 }
 

@@ -486,6 +486,71 @@ __global__ void __launch_bounds__(kThreads) sgd_kernel_scalar(float* W, float* V
   }
 }
 
+// The g ordered updates of one compute-group round on a shard (groups.py):
+// row m of `rows` is rank m's gradient shard; group i's gradient is the sum of
+// its k members' rows in member order, applied with the group's snapshot as
+// the regulariser's w_read (sgd.py:104-112), and W after update i becomes
+// group i's next snapshot.  One pass over the shard instead of g*(k+2) eager
+// launches; the per-element arithmetic is sgd_kernel's.
+constexpr int kMaxGroupRanks = 64;
+struct GroupUpdates {
+  const float* rows;
+  long long ld;
+  float* W;
+  float* V;
+  float* snaps[kMaxGroupRanks];
+  int members[kMaxGroupRanks];
+  int g, k;
+  float eta, mu, lam;
+};
+
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
+__global__ void __launch_bounds__(kThreads) group_updates_kernel(const __grid_constant__ GroupUpdates p,
+                                                                 long long n, int vec) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const float eta = p.eta, mu = p.mu, lam = p.lam;
+  if (vec) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += stride) {
+      float4 w = reinterpret_cast<const float4*>(p.W)[i];
+      float4 v = reinterpret_cast<const float4*>(p.V)[i];
+      for (int gi = 0; gi < p.g; ++gi) {
+        const int* mem = p.members + gi * p.k;
+        float4 gv = reinterpret_cast<const float4*>(p.rows + mem[0] * p.ld)[i];
+        for (int j = 1; j < p.k; ++j)
+          gv = f4add(gv, reinterpret_cast<const float4*>(p.rows + mem[j] * p.ld)[i]);
+        float4* sp = reinterpret_cast<float4*>(p.snaps[gi]) + i;
+        const float4 wr = *sp;
+        v.x = mu * v.x - eta * (gv.x + lam * wr.x);
+        v.y = mu * v.y - eta * (gv.y + lam * wr.y);
+        v.z = mu * v.z - eta * (gv.z + lam * wr.z);
+        v.w = mu * v.w - eta * (gv.w + lam * wr.w);
+        w.x += v.x; w.y += v.y; w.z += v.z; w.w += v.w;
+        *sp = w;
+      }
+      reinterpret_cast<float4*>(p.V)[i] = v;
+      reinterpret_cast<float4*>(p.W)[i] = w;
+    }
+    return;
+  }
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float w = p.W[i], v = p.V[i];
+    for (int gi = 0; gi < p.g; ++gi) {
+      const int* mem = p.members + gi * p.k;
+      float gv = p.rows[mem[0] * p.ld + i];
+      for (int j = 1; j < p.k; ++j) gv = gv + p.rows[mem[j] * p.ld + i];
+      const float wr = p.snaps[gi][i];
+      v = mu * v - eta * (gv + lam * wr);
+      w = w + v;
+      p.snaps[gi][i] = w;
+    }
+    p.V[i] = v;
+    p.W[i] = w;
+  }
+}
+
 // float64 K8 for the drop-in host API (sgd.py:92-101 keeps W, V in float64):
 // the reference's NumPy expression evaluated in its exact order, one rounding
 // per operation and no FMA contraction (the _rn intrinsics), so the result is
@@ -685,6 +750,40 @@ int omni_sgd_momentum_f32(float* W, float* V, const float* g, const float* w_rea
     sgd_kernel_scalar<<<omni::grid_for(n, kThreads), kThreads, 0, st>>>(W, V, g, w_read, eta, mu,
                                                                        lam, n);
   return omni::check_launch("sgd_momentum");
+}
+
+int omni_group_updates_f32(const float* rows, int nrows, long long ld, const int* members, int g, int k,
+                           float* W, float* V, float* const* snaps, long long n, float eta,
+                           float mu, float lam, void* stream) {
+  OMNI_REQUIRE(n >= 0 && g >= 1 && k >= 1 && g * k <= kMaxGroupRanks,
+               "group_updates: need n >= 0, 1 <= g*k <= 64");
+  OMNI_REQUIRE(rows && members && W && V && snaps, "group_updates: NULL argument");
+  OMNI_REQUIRE(ld >= n, "group_updates: row pitch ld < n");
+  if (n == 0) return OMNI_OK;
+  GroupUpdates p{};
+  p.rows = rows;
+  p.ld = ld;
+  p.W = W;
+  p.V = V;
+  p.g = g;
+  p.k = k;
+  p.eta = eta;
+  p.mu = mu;
+  p.lam = lam;
+  bool vec = aligned16(rows) && aligned16(W) && aligned16(V) && ld % 4 == 0 && n % 4 == 0;
+  for (int i = 0; i < g * k; ++i) {
+    OMNI_REQUIRE(members[i] >= 0 && members[i] < nrows, "group_updates: member row out of range");
+    p.members[i] = members[i];
+  }
+  for (int i = 0; i < g; ++i) {
+    OMNI_REQUIRE(snaps[i] != nullptr, "group_updates: NULL snapshot");
+    p.snaps[i] = snaps[i];
+    vec = vec && aligned16(snaps[i]);
+  }
+  const long long work = vec ? n / 4 : n;
+  group_updates_kernel<<<omni::grid_for(work, kThreads), kThreads, 0, omni::as_stream(stream)>>>(
+      p, n, vec ? 1 : 0);
+  return omni::check_launch("group_updates");
 }
 
 int omni_sgd_momentum_f64(double* W, double* V, const double* g, const double* w_read, double eta,

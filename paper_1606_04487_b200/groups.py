@@ -50,6 +50,15 @@ class Backend(Protocol):
             hp: Hyperparams) -> None:
         """In place: V = mu V - eta (G + lam w_read); W += V."""
 
+    def group_updates(self, rows: torch.Tensor, members: list, W: torch.Tensor, V: torch.Tensor,
+                      snaps: list, hp: Hyperparams) -> None:
+        """The g ordered updates of a round on one shard: for i in order, G_i =
+        sum of rows[members[i]] (in that order), sgd(W, V, G_i, snaps[i]),
+        then snaps[i] = W."""
+
+    def exchange(self, plan: ExecutionPlan):
+        """The runtime's collectives (comm.GroupExchange's methods)."""
+
 
 class CudaBackend:
     """B200 engine: device gather + fused forward/backward + K8 update."""
@@ -70,6 +79,16 @@ class CudaBackend:
         from . import kernels as K
 
         K.sgd_momentum(W, V, G, w_read, hp.eta, hp.mu, hp.lam)
+
+    def group_updates(self, rows, members, W, V, snaps, hp):
+        from . import kernels as K
+
+        K.group_updates(rows, members, W, V, snaps, hp.eta, hp.mu, hp.lam)
+
+    def exchange(self, plan):
+        from .comm import GroupExchange
+
+        return GroupExchange(plan, self.device)
 
     def layer_ranges(self) -> list:
         """Parameter ranges [lo, hi) of the layers, in backward order (the
@@ -126,9 +145,7 @@ class GroupRuntime:
         self.group = plan.group_of(rank)
         self.member = plan.member_of(rank)
         self.n_examples = n_examples
-        # every rank creates every subgroup, in the same order (torch.distributed rule)
-        self.group_pgs = [dist.new_group(plan.group_ranks(i)) for i in range(plan.g)]
-        self.cross_pgs = [dist.new_group([i * plan.k + j for i in range(plan.g)]) for j in range(plan.k)]
+        self._x = None                       # collectives (backend.exchange), made on first use
         self.sharded = bool(sharded)
         self._layered = False
         self.snap_step = [0] * plan.g
@@ -151,7 +168,9 @@ class GroupRuntime:
             self._V = torch.zeros_like(self._W)
             self._snapsh = [self._W.clone() for _ in range(plan.g)]
             self._snap_own = W0.clone()              # this rank's group snapshot, full length
-            self._pad = torch.zeros(N * S - self.dim, dtype=W0.dtype, device=W0.device)
+            self._Gpad = torch.zeros(N * S, dtype=W0.dtype, device=W0.device)
+            self._rows = torch.empty(N, S, dtype=W0.dtype, device=W0.device)
+            self._back = torch.empty(N * S, dtype=W0.dtype, device=W0.device)
             self._layered = bool(overlap) and hasattr(backend, "grad_hooked")
             if self._layered:
                 self._init_layered(W0)
@@ -159,10 +178,29 @@ class GroupRuntime:
             self._W = W0.clone()
             self._V = torch.zeros_like(self._W)
             self.snaps = [self._W.clone() for _ in range(plan.g)]
-            self._gather = [torch.empty_like(self._W) for _ in range(plan.g)]
+            self._gather = torch.empty(plan.g, self.dim, dtype=W0.dtype, device=W0.device)
         # gradients arrive as the SUM of k slice means; fold the 1/k into the fused
         # update: eta (G/k + lam w) = (eta/k) (G + k lam w)
         self._hp_sum = hp.replace(eta=hp.eta / plan.k, lam=hp.lam * plan.k)
+
+    @property
+    def x(self):
+        """The collectives (the backend's exchange: the library's NCCL
+        communicators on the CUDA backend).  Made on first use -- every rank
+        reaches it in the same round -- so a peer-memory runtime that never
+        assembles the master model opens no communicator."""
+        if self._x is None:
+            self._x = self.backend.exchange(self.plan)
+        return self._x
+
+    def _members(self) -> list:
+        return [list(self.plan.group_ranks(i)) for i in range(self.plan.g)]
+
+    def _log_round(self) -> None:
+        for i in range(self.plan.g):
+            self.t += 1
+            self.events.append(GroupEvent(i, self.snap_step[i], self.t, self.t - 1 - self.snap_step[i]))
+            self.snap_step[i] = self.t
 
     def _init_p2p(self, W0: torch.Tensor) -> None:
         """Peer-memory rounds (comm.PeerUpdate, copy-engine DMA): rank r owns
@@ -246,7 +284,7 @@ class GroupRuntime:
         for lo, hi in self._layers:
             a, b = owned_part(lo, hi, self.plan.N, self.rank)
             out[a:b] = full[a:b]
-        dist.all_reduce(out)
+        self.x.world_allreduce(out)
         return out
 
     def _init_layered(self, W0: torch.Tensor) -> None:
@@ -279,13 +317,14 @@ class GroupRuntime:
         self._snapsh = [sh.clone() for _ in range(self.plan.g)]
         self._send = {lo: torch.zeros(N * q, dtype=W0.dtype, device=dev) for lo, hi, q, o in self._layers}
         self._recv = {lo: torch.empty(N * q, dtype=W0.dtype, device=dev) for lo, hi, q, o in self._layers}
+        self._back = torch.empty(N * S, dtype=W0.dtype, device=dev)
 
     def _full(self, shard: torch.Tensor) -> torch.Tensor:
-        parts = [torch.empty_like(shard) for _ in range(self.plan.N)]
-        dist.all_gather(parts, shard)
+        out = torch.empty(self.plan.N * shard.numel(), dtype=shard.dtype, device=shard.device)
+        self.x.world_allgather(shard, out)
         if getattr(self, "_layered", False):
-            return torch.cat(parts)[self._gidx]
-        return torch.cat(parts)[:self.dim]
+            return out[self._gidx]
+        return out[:self.dim]
 
     @property
     def W(self) -> torch.Tensor:
@@ -319,25 +358,24 @@ class GroupRuntime:
         idx = self.rng.integers(0, self.n_examples, size=self.hp.b)
         G = self.backend.grad(self.snaps[self.group], self._my_slice(idx))
         if plan.k > 1:
-            dist.all_reduce(G, group=self.group_pgs[self.group])   # sum of k slice means
+            self.x.group_allreduce(G)                       # sum of k slice means
         if plan.g > 1:
-            dist.all_gather(self._gather, G, group=self.cross_pgs[self.member])
-            grads = self._gather
+            self.x.cross_allgather(G, self._gather)         # row i = group i's gradient
+            rows = self._gather
         else:
-            grads = [G]
-        for i in range(plan.g):
-            self.backend.sgd(self._W, self._V, grads[i], self.snaps[i], self._hp_sum)
-            self.t += 1
-            self.events.append(GroupEvent(i, self.snap_step[i], self.t, self.t - 1 - self.snap_step[i]))
-            self.snaps[i].copy_(self._W)      # group i reads W(t) next round
-            self.snap_step[i] = self.t
+            rows = G.view(1, -1)
+        # the g ordered updates; snaps[i] <- W after update i (group i reads it next round)
+        self.backend.group_updates(rows, [[i] for i in range(plan.g)], self._W, self._V, self.snaps,
+                                   self._hp_sum)
+        self._log_round()
 
     def _round_layered(self) -> None:
         """_round_sharded with layer-aligned shards: each layer's gradient
-        all-to-all is issued from the backward's on_grad hook, overlapping the
-        rest of the backward; group sums, the g ordered updates and the
-        snapshot exchange are as in _round_sharded."""
-        plan, N, S = self.plan, self.plan.N, self._S
+        all-to-all is issued from the backward's on_grad hook on the exchange's
+        own stream, overlapping the rest of the backward; the g ordered
+        updates of each layer's shard (one kernel per layer) and the snapshot
+        exchange are as in _round_sharded."""
+        plan, N = self.plan, self.plan.N
         idx = self.rng.integers(0, self.n_examples, size=self.hp.b)
         works = []
         G = self.backend.engine.grad
@@ -346,57 +384,35 @@ class GroupRuntime:
         def hook(lo, hi):
             send = self._send[lo]
             send[:lens[lo]].copy_(G[lo:hi])                    # (on the gradient's stream)
-            works.append(dist.all_to_all_single(self._recv[lo], send, async_op=True))
+            works.append(self.x.all_to_all_async(list(send.view(N, -1)), self._recv[lo]))
 
         self.backend.grad_hooked(self._snap_own, self._my_slice(idx), hook)
         for w in works:
             w.wait()
-        grads = [torch.empty(S, dtype=self._W.dtype, device=self._W.device) for _ in range(plan.g)]
+        members = self._members()
         for lo, hi, q, o in self._layers:
-            rows = self._recv[lo].view(N, q)
-            for i in range(plan.g):
-                ranks = plan.group_ranks(i)
-                gi = grads[i][o:o + q]
-                gi.copy_(rows[ranks[0]])
-                for m in ranks[1:]:
-                    gi.add_(rows[m])
-        for i in range(plan.g):
-            self.backend.sgd(self._W, self._V, grads[i], self._snapsh[i], self._hp_sum)
-            self.t += 1
-            self.events.append(GroupEvent(i, self.snap_step[i], self.t, self.t - 1 - self.snap_step[i]))
-            self._snapsh[i].copy_(self._W)
-            self.snap_step[i] = self.t
-        out = torch.stack([self._snapsh[plan.group_of(m)] for m in range(N)])
-        back = torch.empty_like(out)
-        dist.all_to_all_single(back, out)
-        self._snap_own = back.view(-1)[self._gidx]
+            self.backend.group_updates(self._recv[lo].view(N, q), members, self._W[o:o + q],
+                                       self._V[o:o + q], [s[o:o + q] for s in self._snapsh],
+                                       self._hp_sum)
+        self._log_round()
+        self.x.all_to_all([self._snapsh[plan.group_of(m)] for m in range(N)], self._back)
+        self._snap_own = self._back[self._gidx]
 
     def _round_sharded(self) -> None:
         """The same round with the update work partitioned: one all-to-all gives
-        every rank its shard of each group's gradient (summed over the group's
-        members in member order), each rank applies the g ordered updates to its
-        shard of W, V and of the g snapshots, and a second all-to-all returns to
-        every rank its own group's next snapshot.  Per-rank traffic ~2 models
-        per round (vs a group allreduce plus g models gathered), update work g/N
-        models (vs g)."""
+        every rank its shard of each group's gradient, one kernel applies the g
+        ordered updates to this rank's shard of W, V and of the g snapshots
+        (group i's gradient = the sum of its members' rows in member order),
+        and a second all-to-all returns to every rank its own group's next
+        snapshot.  Per-rank traffic ~2 models per round (vs a group allreduce
+        plus g models gathered), update work g/N models (vs g)."""
         plan, N, S = self.plan, self.plan.N, self._S
         idx = self.rng.integers(0, self.n_examples, size=self.hp.b)
         G = self.backend.grad(self._snap_own, self._my_slice(idx))
-        send = torch.cat([G, self._pad]) if self._pad.numel() else G
-        recv = torch.empty_like(send)
-        dist.all_to_all_single(recv, send)              # row m of recv = rank m's gradient, my shard
-        rows = recv.view(N, S)
-        for i in range(plan.g):
-            ranks = plan.group_ranks(i)
-            Gi = rows[ranks[0]].clone()
-            for m in ranks[1:]:
-                Gi.add_(rows[m])                          # sum of the group's k slice means
-            self.backend.sgd(self._W, self._V, Gi, self._snapsh[i], self._hp_sum)
-            self.t += 1
-            self.events.append(GroupEvent(i, self.snap_step[i], self.t, self.t - 1 - self.snap_step[i]))
-            self._snapsh[i].copy_(self._W)
-            self.snap_step[i] = self.t
-        out = torch.stack([self._snapsh[plan.group_of(m)] for m in range(N)])   # row m -> rank m
-        back = torch.empty_like(out)
-        dist.all_to_all_single(back, out)                # row j = shard j of my group's snapshot
-        self._snap_own = back.view(-1)[:self.dim].clone()
+        self._Gpad[:self.dim].copy_(G)
+        rows = self._rows
+        self.x.all_to_all(list(self._Gpad.view(N, S)), rows.view(-1))   # row m = rank m's gradient, my shard
+        self.backend.group_updates(rows, self._members(), self._W, self._V, self._snapsh, self._hp_sum)
+        self._log_round()
+        self.x.all_to_all([self._snapsh[plan.group_of(m)] for m in range(N)], self._back)
+        self._snap_own = self._back[:self.dim]            # my group's next snapshot (a view)

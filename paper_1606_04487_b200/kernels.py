@@ -7,6 +7,8 @@ Strides ("ld") are in elements, as in include/omni.h.
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 
 from . import _abi
@@ -320,6 +322,27 @@ def sgd_momentum_f64(W: torch.Tensor, V: torch.Tensor, g: torch.Tensor, w_read: 
             raise ValueError("sgd_momentum_f64 takes float64 tensors")
     call("omni_sgd_momentum_f64", _ptr(W), _ptr(V), _ptr(g), _ptr(w_read), eta, mu, lam,
          W.numel(), _stream())
+
+
+def group_updates(rows: torch.Tensor, members: list, W: torch.Tensor, V: torch.Tensor,
+                  snaps: list, eta: float, mu: float, lam: float) -> None:
+    """The g ordered updates of a compute-group round on one shard (one
+    kernel): rows is (nrows, >= n) with unit inner stride, row m = rank m's
+    gradient shard; members[i] lists group i's rows in summation order;
+    snaps[i] is group i's snapshot (the regulariser's w_read, overwritten
+    with W after update i)."""
+    n = W.numel()
+    if rows.dim() != 2 or rows.stride(1) != 1 or rows.shape[1] < n:
+        raise ValueError("group_updates: rows must be (nrows, >= n) with unit inner stride")
+    g, k = len(members), len(members[0])
+    if len(snaps) != g or any(len(m) != k for m in members):
+        raise ValueError("group_updates: one snapshot and k members per group")
+    if any(t.numel() != n or not t.is_contiguous() for t in (V, *snaps)) or not W.is_contiguous():
+        raise ValueError("group_updates: W, V and the snapshots must be contiguous shards of equal length")
+    mem = (ctypes.c_int * (g * k))(*[m for ms in members for m in ms])
+    sp = (ctypes.c_void_p * g)(*[t.data_ptr() for t in snaps])
+    call("omni_group_updates_f32", _ptr(rows), rows.shape[0], rows.stride(0), mem, g, k, _ptr(W),
+         _ptr(V), sp, n, eta, mu, lam, _stream())
 
 
 def gather_rows(src: torch.Tensor, idx: torch.Tensor, dst: torch.Tensor) -> None:

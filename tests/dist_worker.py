@@ -37,13 +37,55 @@ class OracleBackend:
         V.mul_(hp.mu).sub_(hp.eta * (G + hp.lam * w_read))
         W.add_(V)
 
+    def group_updates(self, rows, members, W, V, snaps, hp):
+        for i, ms in enumerate(members):
+            Gi = rows[ms[0]].clone()[:W.numel()]
+            for m in ms[1:]:
+                Gi.add_(rows[m][:W.numel()])
+            self.sgd(W, V, Gi, snaps[i], hp)
+            snaps[i].copy_(W)
+
+    def exchange(self, plan):
+        return TorchExchange(plan)
+
+
+class TorchExchange:
+    """groups.GroupRuntime's collectives over torch.distributed (gloo): the
+    CPU test double of comm.GroupExchange, method for method."""
+
+    def __init__(self, plan):
+        self.plan = plan
+        self.rank = dist.get_rank()
+        # every rank creates every subgroup, in the same order
+        self.groups = [dist.new_group(plan.group_ranks(i)) for i in range(plan.g)]
+        self.crosses = [dist.new_group([i * plan.k + j for i in range(plan.g)]) for j in range(plan.k)]
+
+    def group_allreduce(self, t):
+        dist.all_reduce(t, group=self.groups[self.plan.group_of(self.rank)])
+
+    def cross_allgather(self, t, out):
+        dist.all_gather(list(out.view(self.plan.g, -1)), t,
+                        group=self.crosses[self.plan.member_of(self.rank)])
+
+    def world_allreduce(self, t):
+        dist.all_reduce(t)
+
+    def world_allgather(self, t, out):
+        dist.all_gather(list(out.view(self.plan.N, -1)), t)
+
+    def all_to_all(self, parts, recv):
+        dist.all_to_all_single(recv, torch.cat(parts))
+
+    def all_to_all_async(self, parts, recv):
+        return dist.all_to_all_single(recv, torch.cat(parts), async_op=True)
+
 
 def initial_weights():
     layers = R.tiny_cnn_layers(SIZE, CLASSES)
     return 0.01 * R.problem_rng(SEED, 1).standard_normal(R.param_count(layers, 1, SIZE))
 
 
-def worker(rank, world, port, g, rounds, hp_tuple, out_dir):
+def worker(rank, world, port, g, rounds, hp_tuple, out_dir, sharded=True):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -51,7 +93,7 @@ def worker(rank, world, port, g, rounds, hp_tuple, out_dir):
         eta, mu, lam, b = hp_tuple
         hp = Hyperparams(eta=eta, mu=mu, lam=lam, b=b)
         rt = GroupRuntime(ExecutionPlan(world, g), OracleBackend(), hp,
-                          torch.from_numpy(initial_weights()), N_EX, seed=11)
+                          torch.from_numpy(initial_weights()), N_EX, seed=11, sharded=sharded)
         rt.run(rounds)
         np.save(os.path.join(out_dir, f"W{rank}.npy"), rt.W.numpy())
         np.save(os.path.join(out_dir, f"ev{rank}.npy"),

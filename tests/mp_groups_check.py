@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=4)
     ap.add_argument("--overlap", action="store_true", help="layer-aligned shards, per-layer exchange")
     ap.add_argument("--p2p", action="store_true", help="exchanges over NVLink peer memory (DMA)")
+    ap.add_argument("--replicated", action="store_true", help="unsharded: every rank holds W, V, snapshots")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -42,7 +43,8 @@ def main():
     prob = TinyCNNProblem(8, 4, seed=3, n_examples=64, precision="3xtf32", device=dev)
     W0 = torch.from_numpy(prob.initial_weights().astype(np.float32)).to(dev)
     rt = GroupRuntime(plan, CudaBackend(prob, hp.b // plan.k), hp, W0, prob.n_examples, seed=11,
-                      overlap=args.overlap, p2p=args.p2p)
+                      overlap=args.overlap, p2p=args.p2p,
+                      sharded=not args.replicated)
     rt.run(args.rounds)
     torch.cuda.synchronize()
     W_master = rt.W                      # (sharded runtime: a collective, every rank)

@@ -24,8 +24,9 @@ def free_port() -> int:
         return s.getsockname()[1]
 
 
-def run(world, g, rounds, tmp_path):
-    mp.spawn(DW.worker, args=(world, free_port(), g, rounds, HP, str(tmp_path)), nprocs=world, join=True)
+def run(world, g, rounds, tmp_path, sharded=True):
+    mp.spawn(DW.worker, args=(world, free_port(), g, rounds, HP, str(tmp_path), sharded), nprocs=world,
+             join=True)
     Ws = [np.load(tmp_path / f"W{r}.npy") for r in range(world)]
     evs = [np.load(tmp_path / f"ev{r}.npy") for r in range(world)]
     for r in range(1, world):   # every rank holds the same master model and log
@@ -66,6 +67,15 @@ def test_g1_k2_equals_run_sync(tmp_path):
 
 def test_g2_k1_equals_deterministic_simulate(tmp_path):
     W, ev = run(2, 2, 4, tmp_path)
+    Wr, evr = oracle_simulate(2, 8)
+    assert np.array_equal(ev, evr)
+    assert nrel(W, Wr) < 1e-12
+
+
+def test_g2_k1_replicated_equals_deterministic_simulate(tmp_path):
+    # sharded=False: every rank holds W, V and all g snapshots; group allreduce
+    # + cross-group all-gather + the g ordered updates in one group_updates call
+    W, ev = run(2, 2, 4, tmp_path, sharded=False)
     Wr, evr = oracle_simulate(2, 8)
     assert np.array_equal(ev, evr)
     assert nrel(W, Wr) < 1e-12

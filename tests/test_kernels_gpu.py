@@ -317,6 +317,33 @@ def test_bias_grad_sgd_gather_transpose():
     assert torch.equal(out.cpu(), T.transpose(1, 2))
 
 
+@pytest.mark.parametrize("g,k,n,off", [(1, 2, 4096, 0), (2, 2, 1003, 0), (4, 1, 4096, 1), (2, 4, 777, 3)])
+def test_group_updates_equals_eager_rounds(g, k, n, off):
+    """One group_updates kernel == the eager round (clone + add_ of the members'
+    rows in order, K8, snapshot copy), bit for bit, on vector and scalar paths
+    (off > 0: shards at unaligned offsets, as the layer-aligned runtime slices)."""
+    gen = torch.Generator().manual_seed(7 + g * k)
+    N = g * k
+    rows = torch.randn(N, (n + off + 7) // 4 * 4, generator=gen).to(DEV)     # pitch % 4 == 0
+    W0, V0 = (torch.randn(n + off, generator=gen).to(DEV) for _ in range(2))
+    S0 = [torch.randn(n + off, generator=gen).to(DEV) for _ in range(g)]
+    members = [list(range(i * k, i * k + k))[::-1] for i in range(g)]       # any order: summed as listed
+    eta, mu, lam = 0.05, 0.9, 1e-3
+    W, V, S = W0.clone(), V0.clone(), [s.clone() for s in S0]
+    K.group_updates(rows[:, off:], members, W[off:], V[off:], [s[off:] for s in S], eta, mu, lam)
+    We, Ve, Se = W0.clone()[off:], V0.clone()[off:], [s.clone()[off:] for s in S0]
+    for i in range(g):
+        Gi = rows[members[i][0], off:off + n].clone()
+        for m in members[i][1:]:
+            Gi.add_(rows[m, off:off + n])
+        K.sgd_momentum(We, Ve, Gi.contiguous(), Se[i], eta, mu, lam)
+        Se[i].copy_(We)
+    torch.cuda.synchronize()
+    assert torch.equal(W[off:], We) and torch.equal(V[off:], Ve)
+    assert all(torch.equal(s[off:], e) for s, e in zip(S, Se))
+    assert torch.equal(W[:off], W0[:off])
+
+
 @pytest.mark.parametrize("o,c,k", [(7, 3, 5), (96, 3, 11), (256, 96, 5), (384, 256, 3), (512, 512, 3),
                                    (50, 20, 5)])
 def test_conv_weight_tap_roundtrip(o, c, k):

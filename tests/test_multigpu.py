@@ -47,7 +47,7 @@ def test_data_parallel_session_equals_replay(mode):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("mode", ["", "--p2p", "--overlap"])
+@pytest.mark.parametrize("mode", ["", "--p2p", "--overlap", "--replicated"])
 def test_group_runtime_equals_oracle_schedule(mode):
     out = torchrun(2, "mp_groups_check.py", *([mode] if mode else []))
     assert '"pass": true' in out

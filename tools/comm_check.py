@@ -1,8 +1,9 @@
 """One process per GPU through the C-ABI communicators (no torch NCCL on the
 data path): rank 0 makes the NCCL id, the torch store ships it, every rank
 calls omni_comm_init_rank; then a CaffeNet-sized gradient allreduce (exact on
-integer data, timed), a split into the compute groups of ExecutionPlan(N, g)
-and a server <-> leader snapshot exchange.
+integer data, timed), a split into the compute groups of ExecutionPlan(N, g),
+a server <-> leader snapshot exchange, an all-gather and a personalised
+all-to-all (the sharded group runtime's exchanges).
 
     torchrun --nproc-per-node 4 --master-addr 127.0.0.1 tools/comm_check.py
 """
@@ -63,6 +64,20 @@ def main():
             c.send(grad, 0)
         torch.cuda.synchronize()
         assert bool(torch.all(snap == 7.0).item())
+    # all-gather and the personalised all-to-all (parts from scattered addresses)
+    m = 1000
+    ag = torch.empty(world * m, device="cuda")
+    c.allgather(torch.full((m,), float(rank), device="cuda"), ag)
+    pool = torch.arange(world * 2 * m, dtype=torch.float32, device="cuda") + 1e4 * rank
+    parts = [pool[(2 * d + 1) * m:(2 * d + 2) * m] for d in range(world)]   # non-adjacent parts
+    recv = torch.empty(world * m, device="cuda")
+    c.all_to_all(parts, recv)
+    torch.cuda.synchronize()
+    want_ag = torch.arange(world, device="cuda").float().repeat_interleave(m)
+    out["allgather_exact"] = bool(torch.equal(ag, want_ag))
+    want = torch.cat([torch.arange((2 * rank + 1) * m, (2 * rank + 2) * m, device="cuda").float() + 1e4 * src
+                      for src in range(world)])
+    out["all_to_all_exact"] = bool(torch.equal(recv, want))
     for groups in [d for d in (1, 2, 4, 8) if world % d == 0]:
         k = ExecutionPlan(world, groups).k
         s = c.split(rank // k, rank % k)
