@@ -35,7 +35,10 @@ def torchrun(n, script, *args, env=None):
            os.path.join(ROOT, where, script), *args]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
                        env=None if env is None else {**os.environ, **env})
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    if r.returncode != 0:
+        # the failing rank's traceback sits before torchrun's own summary
+        tb = [ln for ln in r.stderr.splitlines() if not ln.startswith(("E1", "W1", "I1"))]
+        raise AssertionError(r.stdout[-3000:] + "\n".join(tb)[-8000:])
     return r.stdout
 
 
