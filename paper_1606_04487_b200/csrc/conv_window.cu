@@ -21,14 +21,12 @@
 //    swizzled box, 32-47 as a 64-byte swizzled box (K = 432, not 576).
 //    A tile costs 244 rows x 192 B of L2->SM traffic instead of 9 x 128 rows
 //    x 256 B plus the weights.
-//  * wgrad  (dW[o, tap, ch] = sum_pix dZ[pix, o] X[q(pix) + off(tap), ch]):
-//    M = d_out (<= 128), N = taps x 48 + 16 (the bias: a resident all-ones
-//    operand) <= 512 TMEM columns, K = pixels, one K-block per output row
-//    (m pixels, padded to a multiple of 8 by the dZ box's zero fill).  The
-//    window is the MN-major B operand; every tap is one N = 48 MMA whose
-//    descriptor starts off(tap) rows into it.  Each CTA reduces a contiguous
-//    range of output rows; a fixed-order reduction sums the per-CTA partials
-//    (deterministic, no atomics).
+//  * wgrad  (dW[o, kx, ky, ch] = sum_pix dZ[pix, o] X[q(pix) + kx*n2 + ky, ch]):
+//    M = (kx, ky*48 + ch) -- for a fixed kx the three ky taps' channels are
+//    one contiguous 144-float run of the image -- in 32-channel MN-major
+//    atoms, N = d_out, K = pixels, one output row per stage; the s2d rows stay
+//    resident in a ring across the three output rows that read them (see the
+//    wgrad section below).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -358,22 +356,35 @@ __global__ void __launch_bounds__(FLayout<BN>::THREADS, 1)
 }
 
 // ------------------------------------------------------------- wgrad ----
-struct WParams {
-  int b, n2, m, k2, n2sq;
-  int kb;          // K rows per block: m rounded up to 8 (the dZ box zero-fills the rest)
-  int win_rows;    // kb + (k2 - 1) * (n2 + 1)
-  int d_out;       // M (<= 128)
-  int nblk;        // K-blocks = b * m output rows
-  int taps, ncols;  // ncols = taps * 48 + 16
-  int atoms_a;     // ceil(d_out / 32) dZ boxes per block
-  int stages;
-  uint32_t atom_a, atom_b;  // byte strides of the MN-major atoms (multiples of 512)
-  uint32_t stage_bytes, a_bytes, ones_off, bar_off;
-  int tap_split;   // 1: N = 32 + N = 16 MMAs per tap instead of one N = 48 MMA
-  float* ws;       // [gridDim.x][d_out][ncols] partial sums
-};
-
+// dW[o, kx, J] = sum_pix dZ[pix, o] X[q(pix) + kx*n2, J], J = ky*48 + ch in
+// [0, 144): for a fixed kx the three ky taps' channels are ONE contiguous run
+// of 144 floats of the flattened s2d image (pixel pitch 48), so with the image
+// viewed as overlapping 160-float rows at a 192-byte pitch, M = (kx, J) is
+// 3 x 4.5 MN-major 32-channel atoms -- no 48 -> 64 channel padding:
+//   tiles 0-2 (M = 128): kx = t, J in [0, 128)   (atoms a0-a3 of s2d row h+t)
+//   tile  3   (M = 128): J in [128, 160) of kx = 0, 1, 2 (16 real rows each)
+//                        + a resident all-ones atom: rows 96-127 = the bias
+//                        gradient (dZ column sums) at no extra MMA
+// N = d_out, K = pixels: one output row (img, h) per stage, m = 55 pixels
+// padded to 56 by the dZ box's zero fill.  The s2d rows' atoms a0-a3 sit in a
+// 4-slot ring: output row h+1 reuses rows h+1 and h+2 of row h and loads only
+// row h+3 (the A traffic of the 128-pixel im2col tiles drops 3x); the a4 atoms
+// of the three rows and the dZ row are per-stage loads.  Each CTA reduces a
+// contiguous range of output rows into TMEM (4 x d_out columns); a fixed-order
+// reduction sums the per-CTA partials.
 constexpr int W_TMEM_COLS = 512;
+constexpr int W_RING = 4;            // s2d-row slots (rows h .. h+2 in use + 1 loading)
+constexpr int W_STAGES = 2;          // per-output-row stages (a4 atoms + dZ)
+constexpr int W_KB = 56;             // K rows per stage: one output row, 55 -> 56
+constexpr uint32_t W_ATOM = W_KB * 128;   // 7168 B: one 32-float x 56-row MN-major atom
+constexpr int W_COLS = 436;          // workspace row: 432 (kx, J) columns + bias + 3 pad
+struct WParams {
+  int n2, m;
+  int units;        // output rows b * m
+  int d_out;        // N (32, 64 or 96)
+  uint32_t ring_off, stage_off, bar_off;
+  float* ws;        // [gridDim.x][d_out][W_COLS] partial sums
+};
 
 __global__ void __launch_bounds__(256, 1)
     conv_window_wgrad_kernel(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmX,
@@ -388,11 +399,15 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t acc_full = bar0 + 64u;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + p.bar_off + 80);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ring = sbase + p.ring_off;
+  const uint32_t stg0 = sbase + p.stage_off;
+  constexpr uint32_t STAGE_BYTES = 7 * W_ATOM;   // a4 x 3, ones, dZ x 3
+  const int natoms_z = p.d_out / 32;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmG);
     tma_prefetch_desc(&tmX);
-    for (int s = 0; s < p.stages; ++s) {
+    for (int s = 0; s < W_STAGES; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
@@ -406,18 +421,12 @@ __global__ void __launch_bounds__(256, 1)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  // constant operands written once by all threads: the all-ones bias operand
-  // (every element 1.0, so its swizzle is irrelevant) and zeros in the dZ
-  // atoms past d_out (rows of D that are never stored; zero keeps them finite)
-  {
-    float4* ones = reinterpret_cast<float4*>(smem + p.ones_off);
-    const int n1 = p.kb * 32 / 4;
-    for (int i = threadIdx.x; i < n1; i += blockDim.x) ones[i] = make_float4(1.f, 1.f, 1.f, 1.f);
-    for (int s = 0; s < p.stages; ++s)
-      for (int j = p.atoms_a; j < 4; ++j) {
-        float4* z = reinterpret_cast<float4*>(smem + s * p.stage_bytes + j * p.atom_a);
-        for (int i = threadIdx.x; i < n1; i += blockDim.x) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+  {  // each stage's all-ones atom (tile 3's rows 96-127; every element 1.0, so
+     // its swizzle is irrelevant; TMA never writes it)
+    for (int s = 0; s < W_STAGES; ++s) {
+      float4* ones = reinterpret_cast<float4*>(smem + p.stage_off + s * STAGE_BYTES + 3 * W_ATOM);
+      for (int i = threadIdx.x; i < (int)(W_ATOM / 16); i += blockDim.x) ones[i] = make_float4(1.f, 1.f, 1.f, 1.f);
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   tc_fence_before();
@@ -425,89 +434,102 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  // this CTA's contiguous range of output rows (K-blocks)
-  const int blk0 = (int)(((long long)blockIdx.x * p.nblk) / gridDim.x);
-  const int blk1 = (int)(((long long)(blockIdx.x + 1) * p.nblk) / gridDim.x);
+  // this CTA's contiguous range of output rows
+  const int u0 = (int)(((long long)blockIdx.x * p.units) / gridDim.x);
+  const int u1 = (int)(((long long)(blockIdx.x + 1) * p.units) / gridDim.x);
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)p.atoms_a * p.kb * 128u + 2u * (uint32_t)p.win_rows * 128u;
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int blk = blk0; blk < blk1; ++blk) {
-        const int img = blk / p.m, h = blk - (blk / p.m) * p.m;
-        const int q0 = img * p.n2sq + h * p.n2;
-        mbar_wait(empty_bar(stage), phase ^ 1);
-        mbar_expect_tx(full_bar(stage), bytes);
-        const uint32_t a = sbase + stage * p.stage_bytes;
-        const uint32_t bw = a + p.a_bytes;
-        for (int j = 0; j < p.atoms_a; ++j) tma_load_3d(&tmG, a + j * p.atom_a, full_bar(stage), 32 * j, 0, blk);
-        tma_load_2d(&tmX, bw, full_bar(stage), 0, q0);
-        tma_load_2d(&tmX, bw + p.atom_b, full_bar(stage), 32, q0);
-        if (++stage == p.stages) {
-          stage = 0;
-          phase ^= 1;
+      int loads = 0;     // s2d rows loaded so far (ring slot = loads % W_RING)
+      for (int u = u0; u < u1; ++u) {
+        const int i = u - u0, stage = i % W_STAGES;
+        const int img = u / p.m, h = u - (u / p.m) * p.m;
+        const bool fresh = (i == 0) || (h == 0);
+        mbar_wait(empty_bar(stage), ((i / W_STAGES) & 1) ^ 1);
+        if (fresh && i > 0)   // a new image: its 3 rows overwrite slots the previous row still reads
+          mbar_wait(empty_bar((i - 1) % W_STAGES), ((i - 1) / W_STAGES) & 1);
+        const int nnew = fresh ? 3 : 1;
+        mbar_expect_tx(full_bar(stage), (uint32_t)(nnew * 4 + 3 + natoms_z) * W_ATOM);
+        const int rbase = img * p.n2;
+        for (int j = 0; j < nnew; ++j) {
+          const int r = fresh ? h + j : h + 2;
+          const uint32_t slot = ring + (uint32_t)(loads % W_RING) * 4u * W_ATOM;
+          ++loads;
+          for (int a = 0; a < 4; ++a)
+            tma_load_2d(&tmX, slot + a * W_ATOM, full_bar(stage), 32 * a, (rbase + r) * p.n2);
         }
+        const uint32_t stg = stg0 + stage * STAGE_BYTES;
+        for (int kx = 0; kx < 3; ++kx)
+          tma_load_2d(&tmX, stg + kx * W_ATOM, full_bar(stage), 128, (rbase + h + kx) * p.n2);
+        for (int j = 0; j < natoms_z; ++j)
+          tma_load_3d(&tmG, stg + (4 + j) * W_ATOM, full_bar(stage), 32 * j, 0, u);
       }
     }
   } else if (warp == 1) {
     // ---- MMA issuer (whole warp, one elected thread issues) --------------
-    const uint32_t id48 = instr_desc_rt(48, true, true, 128);
-    const uint32_t id32 = instr_desc_rt(32, true, true, 128);
-    const uint32_t id16 = instr_desc_rt(16, true, true, 128);
-    const uint64_t onesd = make_desc(sbase + p.ones_off, 8192, 512, 1);
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int blk = blk0; blk < blk1; ++blk) {
-      mbar_wait(full_bar(stage), phase);
+    const uint32_t idm = instr_desc_rt(p.d_out, true, true, 128);
+    int loads = 0, sl0 = 0, sl1 = 0, sl2 = 0;   // ring slots of rows h, h+1, h+2
+    for (int u = u0; u < u1; ++u) {
+      const int i = u - u0, stage = i % W_STAGES;
+      const int h = u - (u / p.m) * p.m;
+      if (i == 0 || h == 0) {
+        sl0 = loads % W_RING;
+        sl1 = (loads + 1) % W_RING;
+        sl2 = (loads + 2) % W_RING;
+        loads += 3;
+      } else {
+        sl0 = sl1;
+        sl1 = sl2;
+        sl2 = loads % W_RING;
+        loads += 1;
+      }
+      mbar_wait(full_bar(stage), (i / W_STAGES) & 1);
       tc_fence_after();
-      const uint32_t a = sbase + stage * p.stage_bytes;
-      const uint64_t ad0 = make_desc(a, p.atom_a, 512, 1);
-      const uint64_t bd0 = make_desc(a + p.a_bytes, p.atom_b, 512, 1);
-      const uint64_t bd1 = make_desc(a + p.a_bytes + p.atom_b, p.atom_b, 512, 1);
-      for (int kk = 0; kk < p.kb / 8; ++kk) {
-        const uint32_t accf = (blk > blk0 || kk > 0) ? 1u : 0u;
-        const uint64_t ad = ad0 + (uint64_t)(kk * 64u);       // 8 K rows = 1024 B
+      const uint32_t stg = stg0 + stage * STAGE_BYTES;
+      const uint32_t ra[3] = {ring + (uint32_t)sl0 * 4u * W_ATOM, ring + (uint32_t)sl1 * 4u * W_ATOM,
+                              ring + (uint32_t)sl2 * 4u * W_ATOM};
+#pragma unroll 1
+      for (int kk = 0; kk < W_KB / 8; ++kk) {
+        const uint32_t accf = (i > 0 || kk > 0) ? 1u : 0u;
+        const uint32_t ko = (uint32_t)kk * 1024u;   // 8 K rows x 128 B
+        const uint64_t bz = make_desc(stg + 4 * W_ATOM + ko, W_ATOM, 512, 1);
 #pragma unroll
-        for (int t = 0; t < MAX_TAPS; ++t) {
-          const uint64_t roff = (uint64_t)(((t / K2) * p.n2 + t % K2 + kk * 8) * 8u);   // rows x 128 B >> 4
-          const uint32_t dcol = tmem_base + (uint32_t)(t * CP);
-          if (!p.tap_split) {
-            tc_mma_tf32_elect(dcol, ad, bd0 + roff, id48, accf);
-          } else {
-            tc_mma_tf32_elect(dcol, ad, bd0 + roff, id32, accf);
-            tc_mma_tf32_elect(dcol + C0, ad, bd1 + roff, id16, accf);
-          }
-        }
-        // bias gradient: dZ^T times an all-ones operand (16 identical columns)
-        tc_mma_tf32_elect(tmem_base + (uint32_t)(MAX_TAPS * CP), ad, onesd + (uint64_t)(kk * 64u), id16, accf);
+        for (int t = 0; t < 3; ++t)
+          tc_mma_tf32_elect(tmem_base + (uint32_t)(t * p.d_out), make_desc(ra[t] + ko, W_ATOM, 512, 1), bz,
+                            idm, accf);
+        tc_mma_tf32_elect(tmem_base + (uint32_t)(3 * p.d_out), make_desc(stg + ko, W_ATOM, 512, 1), bz, idm,
+                          accf);
       }
       tc_commit_elect(empty_bar(stage));
-      if (++stage == p.stages) {
-        stage = 0;
-        phase ^= 1;
-      }
     }
     tc_commit_elect(acc_full);
   } else if (warp >= 4) {
-    // ---- epilogue: the CTA's partial dW (d_out x ncols) -> workspace -----
+    // ---- epilogue: the CTA's partial dW (d_out x W_COLS) -> workspace ----
     const int ew = warp - 4;
-    const int o = ew * 32 + lane;
+    const int L = ew * 32 + lane;            // TMEM lane = M row of every tile
     mbar_wait(acc_full, 0);
     tc_fence_after();
     const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16);
-    float* dst = p.ws + ((long long)blockIdx.x * p.d_out + o) * p.ncols;
+    float* dst = p.ws + (long long)blockIdx.x * p.d_out * W_COLS;
 #pragma unroll 1
-    for (int c0 = 0; c0 < p.ncols; c0 += 16) {
-      uint32_t rr[16];
-      tmem_ld16(t_row + (uint32_t)c0, rr);
-      tmem_wait_ld();
-      if (o < p.d_out) {
-        float4* d4 = reinterpret_cast<float4*>(dst + c0);
+    for (int t = 0; t < 4; ++t) {
+      // tiles 0-2: (kx = t, J = L); tile 3: (kx = L / 32, J = 128 + L % 32), J < 144 real
+      const int col = t < 3 ? t * 144 + L : (L >> 5) * 144 + 128 + (L & 31);
+      const bool ok = t < 3 || ((L >> 5) < 3 && (L & 31) < 16);
+#pragma unroll 1
+      for (int o0 = 0; o0 < p.d_out; o0 += 16) {
+        uint32_t rr[16];
+        tmem_ld16(t_row + (uint32_t)(t * p.d_out + o0), rr);
+        tmem_wait_ld();
+        if (ok) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          d4[j] = make_float4(__uint_as_float(rr[4 * j]), __uint_as_float(rr[4 * j + 1]),
-                              __uint_as_float(rr[4 * j + 2]), __uint_as_float(rr[4 * j + 3]));
+          for (int j = 0; j < 16; ++j) dst[(long long)(o0 + j) * W_COLS + col] = __uint_as_float(rr[j]);
+        } else if (t == 3 && L == 96) {   // an all-ones row: the bias gradient, + 3 pad columns
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            *reinterpret_cast<float4*>(dst + (long long)(o0 + j) * W_COLS + 432) =
+                make_float4(__uint_as_float(rr[j]), 0.f, 0.f, 0.f);
+        }
       }
     }
   }
@@ -544,7 +566,7 @@ __global__ void __launch_bounds__(256) window_reduce_kernel(const float* __restr
 
 // ------------------------------------------------------------- host -----
 struct Geo {
-  int m, taps, win_f, kb, win_w;
+  int m, taps, win_f;
 };
 
 int geometry(int b, int n2, int cp, int k2, int d_out, Geo* g) {
@@ -554,9 +576,7 @@ int geometry(int b, int n2, int cp, int k2, int d_out, Geo* g) {
   g->m = n2 - k2 + 1;
   g->taps = k2 * k2;
   g->win_f = 128 + (k2 - 1) * (n2 + 1);
-  g->kb = (g->m + 7) / 8 * 8;
-  g->win_w = g->kb + (k2 - 1) * (n2 + 1);
-  OMNI_REQUIRE(g->win_f <= WIN_MAX && g->win_w <= WIN_MAX && g->kb <= 64,
+  OMNI_REQUIRE(g->win_f <= WIN_MAX,
                "conv window: image too wide for one window (n2 = %d)", n2);
   OMNI_REQUIRE((long long)b * n2 * n2 < (1LL << 31), "conv window: too many pixels");
   return OMNI_OK;
@@ -607,10 +627,8 @@ long long omni_conv_window_plan(int op, int b, int n2, int cp, int k2, int d_out
   cwin::Geo g;
   if (cwin::geometry(b, n2, cp, k2, d_out, &g)) return -1;
   if (op == OMNI_CONV_FPROP) return (d_out == 32 || d_out == 64 || d_out == 96 || d_out == 128) ? 0 : -1;
-  if (op != OMNI_CONV_WGRAD_BIAS || d_out > 128) return -1;
-  const int ncols = g.taps * cwin::CP + 16;
-  if (ncols > cwin::W_TMEM_COLS) return -1;
-  return (long long)cwin::wgrad_splits(b * g.m) * d_out * ncols * 4;
+  if (op != OMNI_CONV_WGRAD_BIAS || d_out % 32 != 0 || d_out > 96 || g.m > cwin::W_KB) return -1;
+  return (long long)cwin::wgrad_splits(b * g.m) * d_out * cwin::W_COLS * 4;
 }
 
 int omni_conv_window_f32(int op, const float* Xs, int b, int n2, int cp, int k2, int d_out, const float* G,
@@ -668,47 +686,38 @@ int omni_conv_window_f32(int op, const float* Xs, int b, int n2, int cp, int k2,
     }
   }
   OMNI_REQUIRE(op == OMNI_CONV_WGRAD_BIAS, "conv window: op must be FPROP or WGRAD_BIAS");
-  OMNI_REQUIRE(d_out <= 128, "conv window wgrad: d_out <= 128 (got %d)", d_out);
-  const int ncols = taps * cwin::CP + 16;
-  OMNI_REQUIRE(ncols <= cwin::W_TMEM_COLS, "conv window wgrad: too many taps");
-  OMNI_REQUIRE(ldg >= d_out && ldy >= ncols, "conv window wgrad: leading dimension too small (ldy >= %d)", ncols);
-  const int nblk = b * g.m;
-  const int S = cwin::wgrad_splits(nblk);
-  const long long need = (long long)S * d_out * ncols * 4;
+  OMNI_REQUIRE(d_out % 32 == 0 && d_out <= 96, "conv window wgrad: d_out must be 32, 64 or 96 (got %d)", d_out);
+  OMNI_REQUIRE(g.m <= cwin::W_KB, "conv window wgrad: output rows wider than %d pixels", cwin::W_KB);
+  const int ncols = taps * cwin::CP + 1;
+  OMNI_REQUIRE(ldg >= d_out && ldy >= cwin::W_COLS,
+               "conv window wgrad: leading dimension too small (ldg >= d_out, ldy >= %d)", cwin::W_COLS);
+  (void)ncols;
+  const int units = b * g.m;
+  const int S = cwin::wgrad_splits(units);
+  const long long need = (long long)S * d_out * cwin::W_COLS * 4;
   OMNI_REQUIRE(workspace && ws_bytes >= need && ((uintptr_t)workspace & 15) == 0,
                "conv window wgrad: workspace of %lld bytes required (got %lld)", need, ws_bytes);
   cwin::WParams p{};
-  p.b = b;
   p.n2 = n2;
   p.m = g.m;
-  p.k2 = k2;
-  p.n2sq = n2 * n2;
-  p.kb = g.kb;
-  p.win_rows = g.win_w;
+  p.units = units;
   p.d_out = d_out;
-  p.nblk = nblk;
-  p.taps = taps;
-  p.ncols = ncols;
-  p.atoms_a = (d_out + 31) / 32;
-  p.atom_a = (uint32_t)((g.kb * 128 + 511) / 512 * 512);
-  p.atom_b = (uint32_t)((g.win_w * 128 + 511) / 512 * 512);
-  p.a_bytes = 4 * p.atom_a;
-  p.stage_bytes = (p.a_bytes + 2 * p.atom_b + 1023) / 1024 * 1024;
-  const uint32_t budget = 232448 - 1024 - 256 - 8192;
-  p.stages = (int)(budget / p.stage_bytes);
-  if (p.stages > 4) p.stages = 4;
-  OMNI_REQUIRE(p.stages >= 2, "conv window wgrad: stages do not fit in shared memory");
-  p.ones_off = p.stages * p.stage_bytes;
-  p.bar_off = p.ones_off + 8192;
-  p.tap_split = getenv("OMNI_WINDOW_TAP_SPLIT") ? 1 : 0;
+  p.ring_off = 0;
+  p.stage_off = cwin::W_RING * 4 * cwin::W_ATOM;
+  p.bar_off = p.stage_off + cwin::W_STAGES * 7 * cwin::W_ATOM;
   p.ws = workspace;
   CUtensorMap tg, tx;
-  const cuuint64_t gd[3] = {(cuuint64_t)d_out, (cuuint64_t)g.m, (cuuint64_t)b * g.m};
+  // dZ rows of one output row: (o, w < m, unit); w = m .. W_KB-1 zero-filled
+  const cuuint64_t gd[3] = {(cuuint64_t)d_out, (cuuint64_t)g.m, (cuuint64_t)units};
   const cuuint64_t gs[2] = {(cuuint64_t)ldg * 4, (cuuint64_t)g.m * ldg * 4};
-  const cuuint32_t gb[3] = {32, (cuuint32_t)g.kb, 1};
-  const cuuint64_t xd[2] = {(cuuint64_t)cwin::CP, (cuuint64_t)rows};
+  const cuuint32_t gb[3] = {32, (cuuint32_t)cwin::W_KB, 1};
+  // the s2d image as overlapping 160-float rows at the 48-float pixel pitch:
+  // row q, column J = X[q * 48 + J] (J < 144: the three ky taps' channels).
+  // The last two pixels are out of bounds (read as zeros); the last in-bounds
+  // row reads 64 bytes past the image (caller-provided slack, junk M rows).
+  const cuuint64_t xd[2] = {160, (cuuint64_t)(rows - 2)};
   const cuuint64_t xs[1] = {(cuuint64_t)cwin::CP * 4};
-  const cuuint32_t xb[2] = {32, (cuuint32_t)g.win_w};
+  const cuuint32_t xb[2] = {32, (cuuint32_t)cwin::W_KB};
   if ((rc = cwin::tmap(&tg, G, 3, gd, gs, gb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))) return rc;
   if ((rc = cwin::tmap(&tx, Xs, 2, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))) return rc;
   const int bytes = (int)(p.bar_off + 256 + 1024);
@@ -717,14 +726,15 @@ int omni_conv_window_f32(int op, const float* Xs, int b, int n2, int cp, int k2,
   cudaGetDevice(&dev);
   if (!(configured & (1ull << (dev & 63)))) {
     OMNI_CUDA_TRY(cudaFuncSetAttribute(cwin::conv_window_wgrad_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     configured |= 1ull << (dev & 63);
   }
   cwin::conv_window_wgrad_kernel<<<S, 256, bytes, st>>>(tg, tx, p);
   rc = omni::check_launch("conv_window_wgrad");
   if (rc) return rc;
-  const int total = d_out * (ncols / 4);
-  cwin::window_reduce_kernel<<<omni::grid_for(total, 256), 256, 0, st>>>(workspace, S, d_out, ncols, Y, ldy);
+  const int total = d_out * (cwin::W_COLS / 4);
+  cwin::window_reduce_kernel<<<omni::grid_for(total, 256), 256, 0, st>>>(workspace, S, d_out, cwin::W_COLS, Y,
+                                                                         ldy);
   return omni::check_launch("conv_window_reduce");
 }
 

@@ -163,7 +163,10 @@ class GpuNet:
                         op.s2d = (st, k2, p2, n2, cp)
                         op.implicit = True
                         op.window = window
-                        op.s2d_buf = z(self.b, n2, n2, cp)
+                        # 64 floats of slack: the window wgrad's overlapping-row view
+                        # of the image reads 16 floats past its last pixel
+                        npx = self.b * n2 * n2 * cp
+                        op.s2d_buf = z(npx + 64)[:npx].view(self.b, n2, n2, cp)
                 if op.s2d is not None:
                     st, k2, p2, n2, cp = op.s2d
                     op.Kc = op.Kf = k2 * k2 * cp
@@ -183,12 +186,11 @@ class GpuNet:
                 op.wstage = z(d, op.ldK)
                 op.ldW = op.ldK
                 if op.window:
-                    # weight gradient on the generic implicit GEMM over the same
-                    # 48-channel image: 64-wide channel blocks per tap (16 zero-read),
-                    # the bias as the folded extra row
+                    # weight + bias gradient on the window wgrad kernel: 48-wide tap
+                    # rows, the bias in column k2*k2*48
                     st, k2, p2, n2, cp = op.s2d
                     op.wgrad_op = _abi.CONV_WGRAD_BIAS
-                    op.ldW = K.round_up(k2 * k2 * 64 + 1, 32)
+                    op.ldW = K.round_up(k2 * k2 * cp + 4, 32)
                 elif op.implicit and op.boff >= 0 and not os.environ.get("OMNI_NO_WGRAD_BIAS"):
                     # bias gradient as one more row of the implicit wgrad GEMM (column Kf)
                     op.wgrad_op = _abi.CONV_WGRAD_BIAS
@@ -281,6 +283,9 @@ class GpuNet:
                 geo = (b, op.inp.n, op.c_in, op.k, op.s, op.p, d)
             need = max(K.conv_implicit_workspace_bytes(self.prec, _abi.CONV_FPROP, *geo),
                        K.conv_implicit_workspace_bytes(self.prec, op.wgrad_op, *geo))
+            if op.window:
+                st, k2, p2, n2, cp = op.s2d
+                need = max(need, K.conv_window_plan(_abi.CONV_WGRAD_BIAS, b, n2, cp, k2, d))
             if not op.first_param_layer:
                 need = max(need, K.conv_implicit_workspace_bytes(
                     self.prec, _abi.CONV_FPROP, b, op.m, d, op.k, 1, op.k - 1 - op.p, op.c_in))
@@ -582,14 +587,20 @@ class GpuNet:
                 if op.implicit:
                     with wgrad_stream():
                         X, c_, k_, s_, p_ = self._conv_input(op, b, transform=False)
-                        self._conv(op.wgrad_op, X, c_, k_, s_, p_, d, dZ, op.out.cs,
-                                   op.dwstage, op.ldW)
+                        if op.window:
+                            self._timed(d, c_ * k_ * k_, Mr, "conv", lambda: K.conv_window(
+                                _abi.CONV_WGRAD_BIAS, X, k_, d, dZ, op.out.cs, op.dwstage, op.ldW,
+                                workspace=self._ws_active))
+                        else:
+                            self._conv(op.wgrad_op, X, c_, k_, s_, p_, d, dZ, op.out.cs,
+                                       op.dwstage, op.ldW)
                         fold = op.wgrad_op == _abi.CONV_WGRAD_BIAS
                         gb = G[op.boff:op.boff + d] if fold else None
                         if op.s2d is not None:
-                            # wgrad rows are round_up(cp, 32) wide per tap (64 for the window form)
+                            # wgrad rows are cp (window kernel) or round_up(cp, 32) wide per tap
+                            cpw = op.s2d[4] if op.window else K.round_up(op.s2d[4], 32)
                             K.conv_weight_s2d(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k,
-                                              op.s2d[0], K.round_up(op.s2d[4], 32), op.dwstage, op.ldW,
+                                              op.s2d[0], cpw, op.dwstage, op.ldW,
                                               inverse=True, bias=gb)
                         else:
                             K.conv_weight_to_tap(G[op.woff:op.woff + op.wsz], d, op.c_in, op.k,

@@ -242,7 +242,11 @@ def conv_window(op: int, Xs: torch.Tensor, k2: int, d_out: int, G: torch.Tensor,
         _fits(Y, (pixels - 1) * ldy + d_out, "Y")
     else:
         _fits(G, (pixels - 1) * ldg + d_out, "G")
-        _fits(Y, (d_out - 1) * ldy + taps + 16, "Y")
+        _fits(Y, (d_out - 1) * ldy + taps + 4, "Y")
+        # the overlapping-row view of Xs reads 16 floats past its last pixel
+        slack = Xs.untyped_storage().nbytes() // 4 - Xs.storage_offset() - Xs.numel()
+        if not Xs.is_contiguous() or slack < 16:
+            raise ValueError("conv_window wgrad: Xs must be contiguous with >= 16 readable floats after it")
     if bias is not None:
         _fits(bias, d_out, "bias")
     need = conv_window_plan(op, b, n2, cp, k2, d_out)
