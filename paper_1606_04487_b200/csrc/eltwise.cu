@@ -54,6 +54,40 @@ __global__ void __launch_bounds__(kThreads) pool_fwd_kernel(
       arg[v] = hs * w + ws;
     }
     bool first = true;
+    if constexpr (KS > 0 && V == 4) {
+      // every window element loaded up front in one basic block (an element
+      // outside the clipped window reads the window's first element and is
+      // skipped by the fold), then folded in (dy, dx) order exactly as below:
+      // one exposed load latency per output instead of one per element
+      const int ny = he - hs, nx = we - ws;
+      float4 t[KS][KS];
+#pragma unroll
+      for (int dy = 0; dy < KS; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < KS; ++dx) {
+          const int iy = hs + (dy < ny ? dy : 0), ix = ws + (dx < nx ? dx : 0);
+          t[dy][dx] = __ldg(reinterpret_cast<const float4*>(Xi + (iy * w + ix) * cs_in));
+        }
+#pragma unroll
+      for (int dy = 0; dy < KS; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < KS; ++dx) {
+          if (dy >= ny || dx >= nx) continue;
+          const float val[4] = {t[dy][dx].x, t[dy][dx].y, t[dy][dx].z, t[dy][dx].w};
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            if (MODE == 0) {
+              if (first || val[v] > best[v]) {
+                best[v] = val[v];
+                arg[v] = (hs + dy) * w + (ws + dx);
+              }
+            } else {
+              acc[v] += val[v];
+            }
+          }
+          first = false;
+        }
+    } else {
 #pragma unroll
     for (int dy = 0; dy < (KS ? KS : 1); ++dy) {
       for (int iy = (KS ? hs + dy : hs); iy < (KS ? min(hs + dy + 1, he) : he); ++iy)
@@ -82,6 +116,7 @@ __global__ void __launch_bounds__(kThreads) pool_fwd_kernel(
             first = false;
           }
         }
+    }
     }
     float* dst = Y + (long long)opix * cs_out + ch;
     if (MODE == 0) {
@@ -221,22 +256,37 @@ __global__ void __launch_bounds__(kThreads) pool_bwd_s2_kernel(
         for (int v = 0; v < 4; ++v) acc[a][e][v] = 0.f;
     const int obase = img * oh * ow;
     // at stride 2 with k <= 3 (or k = 4, even pad) at most 2 x 2 windows cover an
-    // aligned 2x2 block: iterate a fixed, unrolled candidate set (all loads in flight)
+    // aligned 2x2 block: a fixed, unrolled candidate set whose loads are all
+    // issued up front (a candidate outside [oy0, oy1) x [ox0, ox1) reads a
+    // clamped in-range window and is skipped below)
+    float4 gq[2][2], yq[2][2];
+    int4 aq[2][2];
+#pragma unroll
+    for (int ty = 0; ty < 2; ++ty)
+#pragma unroll
+      for (int tx = 0; tx < 2; ++tx) {
+        const int o = obase + min(oy0 + ty, oh - 1) * ow + min(ox0 + tx, ow - 1);
+        gq[ty][tx] = __ldg(reinterpret_cast<const float4*>(dY + (long long)o * cs_out + ch));
+        if (MODE == 0) {
+          aq[ty][tx] = __ldg(reinterpret_cast<const int4*>(argmax + (long long)o * c + ch));
+          if (relu_mask_x == 2)
+            yq[ty][tx] = __ldg(reinterpret_cast<const float4*>(X + (long long)o * cs_out + ch));
+        }
+      }
 #pragma unroll
     for (int ty = 0; ty < 2; ++ty)
 #pragma unroll
       for (int tx = 0; tx < 2; ++tx) {
         const int oy = oy0 + ty, ox = ox0 + tx;
         if (oy >= oy1 || ox >= ox1) continue;
-        const int o = obase + oy * ow + ox;
-        const float4 g = __ldg(reinterpret_cast<const float4*>(dY + (long long)o * cs_out + ch));
+        const float4 g = gq[ty][tx];
         const float gv[4] = {g.x, g.y, g.z, g.w};
         if (MODE == 0) {
-          const int4 t = __ldg(reinterpret_cast<const int4*>(argmax + (long long)o * c + ch));
+          const int4 t = aq[ty][tx];
           const int av[4] = {t.x, t.y, t.z, t.w};
           float gm[4] = {gv[0], gv[1], gv[2], gv[3]};
           if (relu_mask_x == 2) {  // X holds the pooled output: mask by the window max
-            const float4 y = __ldg(reinterpret_cast<const float4*>(X + (long long)o * cs_out + ch));
+            const float4 y = yq[ty][tx];
             gm[0] = y.x > 0.f ? gm[0] : 0.f;
             gm[1] = y.y > 0.f ? gm[1] : 0.f;
             gm[2] = y.z > 0.f ? gm[2] : 0.f;

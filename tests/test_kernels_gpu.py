@@ -523,6 +523,30 @@ def test_conv_implicit_dgrad_via_flipped_weights(geom):
     assert rel_err(dX.cpu(), Xd.grad.permute(0, 2, 3, 1)) < 5e-6 * max(1.0, (d * k * k / 1000) ** 0.5)
 
 
+@pytest.mark.parametrize("b,n,c,s,cp", [(3, 227, 3, 4, 48), (2, 227, 3, 4, 64), (2, 30, 4, 2, 16),
+                                         (2, 16, 5, 2, 32), (1, 9, 3, 4, 48)])
+def test_space_to_depth_exact(b, n, c, s, cp):
+    """Y[img, X, Y, (dx*s + dy)*c + ch] = X[img, s*X + dx, s*Y + dy, ch], zero past
+    the image and in the padded channels -- bit-exact against a torch re-layout
+    (staged and unstaged kernels; the gathered form with a permuted batch)."""
+    gen = torch.Generator().manual_seed(5 + n)
+    X = torch.randn(b, n, n, c, generator=gen)
+    n2 = -(-n // s)
+    Xp = torch.zeros(b, n2 * s, n2 * s, c)
+    Xp[:, :n, :n] = X
+    ref = Xp.view(b, n2, s, n2, s, c).permute(0, 1, 3, 2, 4, 5).reshape(b, n2, n2, s * s * c)
+    want = torch.zeros(b, n2, n2, cp)
+    want[..., :s * s * c] = ref
+    Y = torch.full((b, n2, n2, cp), float("nan"), device=DEV)
+    K.space_to_depth(X.to(DEV), c, s, Y)
+    idx = torch.arange(b - 1, -1, -1, dtype=torch.int64)
+    Yg = torch.full((b, n2, n2, cp), float("nan"), device=DEV)
+    K.space_to_depth_gather(X.to(DEV), idx.to(DEV), c, s, Yg)
+    torch.cuda.synchronize()
+    assert torch.equal(Y.cpu(), want)
+    assert torch.equal(Yg.cpu(), want[idx])
+
+
 @pytest.mark.parametrize("geom", [(2, 27, 3, 11, 4, 0, 96), (2, 227, 3, 11, 4, 0, 96), (3, 16, 5, 4, 2, 0, 32)])
 def test_space_to_depth_conv_equals_strided_conv(geom):
     """A stride-s k x k conv == the stride-1 ceil(k/s)^2 implicit conv of the
