@@ -146,7 +146,10 @@ int omni_conv_implicit_f32(int precision, int op, const float* X, int b, int n, 
  * relu_mask_x == 2 (max pool only): X is the pooled OUTPUT (b, oh, ow, cs_out)
  * and each window's gradient is masked by (Y > 0) -- the same result, since
  * gradient reaches only the argmax element and Y equals it, at 1/k^2-ish of
- * the bytes.                                                                   */
+ * the bytes.  Forward mode 2 = max with that mask folded into the indices:
+ * windows whose maximum is not > 0 get the argmax sign bit set (argmax &
+ * 0x7fffffff is mode 0's), so backward mode 0 with relu_mask_x = 0 routes
+ * exactly what relu_mask_x = 2 does without reading Y.                      */
 int omni_pool_out_size(int n, int k, int stride, int pad, int ceil_mode);
 int omni_pool_fwd_nhwc_f32(int mode, const float* X, int b, int h, int w, int c, int cs_in,
                            int k, int stride, int pad, int ceil_mode, float* Y, int cs_out,

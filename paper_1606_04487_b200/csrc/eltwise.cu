@@ -24,10 +24,12 @@ __host__ __device__ inline int pool_out(int n, int k, int s, int p, int ceil_mod
 // One thread per (img, oy, ox, channel group of V).  Max: first maximum in
 // (dy, dx) order, argmax = iy*w + ix (problems.py:213-216).  Avg: Caffe
 // divisor.  V = 4 uses float4/int4 accesses (c, cs_in, cs_out multiples of 4).
+// mark (max): windows whose maximum is not > 0 get the argmax sign bit set,
+// so a backward without a ReLU mask routes nothing there (mode 2 below).
 template <int MODE, int V, int KS = 0>
 __global__ void __launch_bounds__(kThreads) pool_fwd_kernel(
     const float* __restrict__ X, int b, int h, int w, int c, int cs_in, int k_rt, int s, int p,
-    int oh, int ow, float* __restrict__ Y, int cs_out, int32_t* __restrict__ argmax) {
+    int oh, int ow, float* __restrict__ Y, int cs_out, int32_t* __restrict__ argmax, int mark) {
   const int k = KS ? KS : k_rt;   // KS > 0: fully unrolled window, all loads in flight
   const int cv = c / V;
   const int total = b * oh * ow * cv;
@@ -119,6 +121,11 @@ __global__ void __launch_bounds__(kThreads) pool_fwd_kernel(
     }
     }
     float* dst = Y + (long long)opix * cs_out + ch;
+    if (MODE == 0 && mark) {
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if (!(best[v] > 0.f)) arg[v] |= (int)0x80000000;
+    }
     if (MODE == 0) {
       if (V == 4) {
         *reinterpret_cast<float4*>(dst) = make_float4(best[0], best[1 % V], best[2 % V], best[3 % V]);
@@ -227,11 +234,13 @@ __global__ void __launch_bounds__(kThreads) pool_bwd_kernel(
 // so each window's dY and argmax are read once per block instead of once per
 // pixel.  Per pixel the windows are still summed in ascending (oy, ox) order:
 // bit-identical to pool_bwd_kernel.
-template <int MODE>
+// RM = relu_mask_x (compile time: the register budget follows the loads it needs).
+template <int MODE, int RM>
 __global__ void __launch_bounds__(kThreads) pool_bwd_s2_kernel(
     const float* __restrict__ dY, int b, int h, int w, int c, int cs_in, int k, int p, int oh,
     int ow, int cs_out, const int32_t* __restrict__ argmax, const float* __restrict__ X,
-    int relu_mask_x, float* __restrict__ dX) {
+    float* __restrict__ dX) {
+  constexpr int relu_mask_x = RM;
   const int cv = c / 4;
   const int bh = (h + 1) / 2, bw = (w + 1) / 2;
   const int total = b * bh * bw * cv;
@@ -662,10 +671,12 @@ int omni_pool_out_size(int n, int k, int stride, int pad, int ceil_mode) {
 int omni_pool_fwd_nhwc_f32(int mode, const float* X, int b, int h, int w, int c, int cs_in, int k,
                            int stride, int pad, int ceil_mode, float* Y, int cs_out,
                            int32_t* argmax, void* stream) {
-  OMNI_REQUIRE(mode == 0 || mode == 1, "pool: mode must be 0 (max) or 1 (avg)");
+  OMNI_REQUIRE(mode >= 0 && mode <= 2, "pool: mode must be 0 (max), 1 (avg) or 2 (max, marked argmax)");
   OMNI_REQUIRE(b >= 0 && h >= 1 && w >= 1 && c >= 1 && k >= 1 && stride >= 1 && pad >= 0 &&
                    pad < k && k <= h + 2 * pad && k <= w + 2 * pad && cs_in >= c && cs_out >= c,
                "pool: bad geometry");
+  const int mark = mode == 2 ? 1 : 0;
+  if (mode == 2) mode = 0;
   OMNI_REQUIRE(mode == 1 || argmax != nullptr, "pool: max mode needs an argmax buffer");
   const int oh = pool_out(h, k, stride, pad, ceil_mode), ow = pool_out(w, k, stride, pad, ceil_mode);
   const long long work = (long long)b * oh * ow * c;
@@ -677,7 +688,7 @@ int omni_pool_fwd_nhwc_f32(int mode, const float* X, int b, int h, int w, int c,
                   (mode == 1 || aligned16(argmax));
   const int grid = omni::grid_for(v4 ? work / 4 : work, kThreads);
 #define OMNI_POOL_FWD(M, V, KS) \
-  pool_fwd_kernel<M, V, KS><<<grid, kThreads, 0, st>>>(X, b, h, w, c, cs_in, k, stride, pad, oh, ow, Y, cs_out, argmax)
+  pool_fwd_kernel<M, V, KS><<<grid, kThreads, 0, st>>>(X, b, h, w, c, cs_in, k, stride, pad, oh, ow, Y, cs_out, argmax, mark)
   if (mode == 0) {
     if (v4 && k == 3) OMNI_POOL_FWD(0, 4, 3);
     else if (v4) OMNI_POOL_FWD(0, 4, 0);
@@ -715,12 +726,18 @@ int omni_pool_bwd_nhwc_f32(int mode, const float* dY, int b, int h, int w, int c
   if (v4 && stride == 2 && (k <= 3 || (k == 4 && pad % 2 == 0)) && !getenv("OMNI_POOL_BWD_PIXEL")) {
     const long long blocks = (long long)b * ((h + 1) / 2) * ((w + 1) / 2) * (c / 4);
     const int g2 = omni::grid_for(blocks, kThreads);
-    if (mode == 0)
-      pool_bwd_s2_kernel<0><<<g2, kThreads, 0, st>>>(dY, b, h, w, c, cs_in, k, pad, oh, ow, cs_out,
-                                                     argmax, X, relu_mask_x, dX);
-    else
-      pool_bwd_s2_kernel<1><<<g2, kThreads, 0, st>>>(dY, b, h, w, c, cs_in, k, pad, oh, ow, cs_out,
-                                                     argmax, X, relu_mask_x, dX);
+#define OMNI_POOL_BWD_S2(M, R)                                                                    \
+  pool_bwd_s2_kernel<M, R><<<g2, kThreads, 0, st>>>(dY, b, h, w, c, cs_in, k, pad, oh, ow, cs_out, argmax, \
+                                                    X, dX)
+    if (mode == 0) {
+      if (relu_mask_x == 2) OMNI_POOL_BWD_S2(0, 2);
+      else if (relu_mask_x == 1) OMNI_POOL_BWD_S2(0, 1);
+      else OMNI_POOL_BWD_S2(0, 0);
+    } else {
+      if (relu_mask_x == 1) OMNI_POOL_BWD_S2(1, 1);
+      else OMNI_POOL_BWD_S2(1, 0);
+    }
+#undef OMNI_POOL_BWD_S2
     return omni::check_launch("pool_bwd_s2");
   }
   const int grid = omni::grid_for(v4 ? work / 4 : work, kThreads);

@@ -268,6 +268,8 @@ class GpuNet:
         self.timer = None   # list -> (M, N, K, kind, ev0, ev1) per GEMM launch
         # False: weight gradients on the main stream (isolated kernel timing / debugging)
         self.overlap = not os.environ.get("OMNI_NO_SIDE_STREAM")
+        # max pools over a fused-ReLU activation: mask folded into the argmax (mode 2)
+        self.mark_pool = not os.environ.get("OMNI_NO_POOL_MARK")
 
     # ------------------------------------------------------------ shapes --
     def _workspace_need(self, op: Op, b: int) -> int:
@@ -437,6 +439,8 @@ class GpuNet:
                            op.out.value, op.out.cs, epi, kind="conv")
             elif op.kind == "pool":
                 mode = 0 if L.mode == "max" else 1
+                if mode == 0 and op.inp.fused_relu and self.mark_pool:
+                    mode = 2   # the ReLU mask of the routed element folded into the argmax
                 K.pool_fwd(mode, op.inp.value[:b], op.inp.c, op.k, op.s, op.p, L.ceil,
                            op.out.value[:b], op.argmax)
             elif op.kind == "relu":
@@ -637,7 +641,10 @@ class GpuNet:
                 if op.inp.grad is None:
                     continue
                 mode = 0 if L.mode == "max" else 1
-                if mode == 0 and op.inp.fused_relu:
+                if mode == 0 and op.inp.fused_relu and self.mark_pool:
+                    # max pool: forward mode 2 marked the windows whose max is not > 0
+                    xm, rm = None, 0
+                elif mode == 0 and op.inp.fused_relu:
                     # max pool: the ReLU mask of the routed element is (pooled value > 0)
                     xm, rm = op.out.value[:b], 2
                 else:

@@ -277,6 +277,32 @@ def test_maxpool_bwd_output_mask_equals_input_mask(geom):
     assert torch.equal(d1.cpu(), d2.cpu())
 
 
+@pytest.mark.parametrize("geom", [(2, 55, 55, 96, 3, 2, 0, True), (2, 13, 13, 20, 2, 2, 0, True),
+                                  (2, 9, 9, 8, 3, 2, 1, False), (1, 7, 7, 3, 3, 3, 1, True)])
+def test_maxpool_marked_argmax_equals_output_mask(geom):
+    """Forward mode 2 (argmax sign bit set where the window max is not > 0) +
+    backward without a mask == mode 0 + the relu_mask_x = 2 backward, bit for
+    bit; argmax & 0x7fffffff == mode 0's argmax; pooled values identical."""
+    b, h, w, c, k, s, p, ceil_mode = geom
+    gen = torch.Generator().manual_seed(23)
+    X = torch.randn(b, h, w, c, generator=gen).clamp_min(0).to(DEV)
+    X[0, : h // 2] = 0.0                                   # whole windows of zeros
+    oh, ow = K.pool_out_size(h, k, s, p, ceil_mode), K.pool_out_size(w, k, s, p, ceil_mode)
+    Y0, Y2 = torch.empty(b, oh, ow, c, device=DEV), torch.empty(b, oh, ow, c, device=DEV)
+    a0 = torch.empty(b * oh * ow * c, dtype=torch.int32, device=DEV)
+    a2 = torch.empty_like(a0)
+    K.pool_fwd(0, X, c, k, s, p, ceil_mode, Y0, a0)
+    K.pool_fwd(2, X, c, k, s, p, ceil_mode, Y2, a2)
+    dY = torch.randn(b, oh, ow, c, generator=gen).to(DEV)
+    d0, d2 = torch.empty_like(X), torch.empty_like(X)
+    K.pool_bwd(0, dY, X.shape, c, k, s, p, ceil_mode, a0, Y0, 2, d0)
+    K.pool_bwd(0, dY, X.shape, c, k, s, p, ceil_mode, a2, None, 0, d2)
+    torch.cuda.synchronize()
+    assert torch.equal(Y0, Y2) and torch.equal(a2 & 0x7FFFFFFF, a0)
+    assert bool((a2 < 0).any()) and torch.equal(a2 < 0, ~(Y0.view(-1) > 0))
+    assert torch.equal(d0, d2)
+
+
 def test_softmax_xent():
     b, C = 37, 1000
     gen = torch.Generator().manual_seed(2)
