@@ -954,14 +954,16 @@ Plan make_plan(int M, int N, int K, int sms, int bkt = BK, bool cta2 = false, bo
   return pl;
 }
 
-// CTA pairs (M = 256 tiles, half of B per CTA) for TF32 GEMMs with more than
-// one 128-row tile; the transposed conv form (im2col B, M = d_out <= 128) and
-// 3xTF32 stay on single CTAs (the kernel's split-K/converter protocol for
-// 3xTF32 pairs is written -- OWN_FULL -- but its low-order products came out
-// missing on the B200, tests/test_kernels_gpu.py; not enabled).
+// CTA pairs (M = 256 tiles, half of B per CTA) for GEMMs with more than one
+// 128-row tile: TF32 everywhere but the transposed conv form (im2col B,
+// M = d_out <= 128); 3xTF32 on plain GEMMs only (OWN_FULL protocol: each
+// CTA's converter warps split its own stage, CTA 0's MMA issuer waits for
+// both; bit-identical to single CTAs, 4096^3 0.742 -> 0.644 ms) -- its conv
+// forms measured slower on pairs (profiles/r02_3xtf32_pairs_ab.json).
 // OMNI_NO_2CTA=1 disables pairs.
 bool pair_ok(int precision, int M, int im2col) {
   static const bool off = getenv("OMNI_NO_2CTA") != nullptr;
+  if (precision == OMNI_PREC_3XTF32) return !off && M > BM && im2col == 0;
   return !off && precision == OMNI_PREC_TF32 && M > BM && im2col != 4;
 }
 
@@ -1114,6 +1116,10 @@ int dispatch_bn(const Plan& pl, const float* A, long long lda, const float* B, l
   if constexpr (!SPLIT3 && IM2COL != 4) {
     if (pl.cta2)
       return dispatch_bn_t<A_MN, B_MN, false, IM2COL, BKT, true>(pl, A, lda, B, ldb, p, st, cg, ones);
+  }
+  if constexpr (SPLIT3 && IM2COL == 0) {
+    if (pl.cta2)
+      return dispatch_bn_t<A_MN, B_MN, true, IM2COL, BKT, true>(pl, A, lda, B, ldb, p, st, cg, ones);
   }
   return dispatch_bn_t<A_MN, B_MN, SPLIT3, IM2COL, BKT, false>(pl, A, lda, B, ldb, p, st, cg, ones);
 }
