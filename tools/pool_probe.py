@@ -35,8 +35,12 @@ def main():
         dX = torch.empty(b, n, n, c, device=dev)
         fwd = lambda: K.pool_fwd(0, X, c, 3, 2, 0, False, Y, am)  # noqa: E731
         bwd = lambda: K.pool_bwd(0, dY, X.shape, c, 3, 2, 0, False, am, Y, 2, dX)  # noqa: E731
+        # the engine's form: forward mode 2 (ReLU mask in the argmax sign bit), unmasked backward
+        fwd2 = lambda: K.pool_fwd(2, X, c, 3, 2, 0, False, Y, am)  # noqa: E731
+        bwd2 = lambda: K.pool_bwd(0, dY, X.shape, c, 3, 2, 0, False, am, None, 0, dX)  # noqa: E731
         xin, yout = 4 * b * n * n * c, 4 * b * m * m * c
-        for kind, fn, nbytes in (("fwd", fwd, xin + 2 * yout), ("bwd", bwd, 3 * yout + xin)):
+        for kind, fn, nbytes in (("fwd", fwd, xin + 2 * yout), ("bwd", bwd, 3 * yout + xin),
+                                 ("fwd_marked", fwd2, xin + 2 * yout), ("bwd_marked", bwd2, 2 * yout + xin)):
             fn()
             torch.cuda.synchronize()
             if a.once:
