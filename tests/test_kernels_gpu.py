@@ -370,6 +370,27 @@ def test_group_updates_equals_eager_rounds(g, k, n, off):
     assert torch.equal(W[:off], W0[:off])
 
 
+@pytest.mark.parametrize("rows,cols,lds,ldd", [(36, 256, 256, 36), (256, 36, 36, 260), (49, 50, 52, 49),
+                                             (9, 1000, 1000, 12)])
+def test_transpose_batched_strided(rows, cols, lds, ldd):
+    """Batched transposes of the shapes the engine uses (the pool5 -> fc6
+    flatten and its gradient, 36 x 256 per image) and ragged ones: exact,
+    strided rows on both sides, nothing written outside the transposed block."""
+    gen = torch.Generator().manual_seed(rows * cols)
+    batch = 70
+    sb, db = rows * lds + 3, cols * ldd + 5
+    src = torch.randn(batch * sb, generator=gen)
+    dst = torch.full((batch * db,), float("nan"), device=DEV)
+    K.transpose(src.to(DEV), lds, sb, rows, cols, dst, ldd, db, batch)
+    torch.cuda.synchronize()
+    S = torch.as_strided(src, (batch, rows, cols), (sb, lds, 1))
+    D = torch.as_strided(dst.cpu(), (batch, cols, rows), (db, ldd, 1))
+    assert torch.equal(D, S.transpose(1, 2))
+    written = torch.zeros(batch * db, dtype=torch.bool)
+    torch.as_strided(written, (batch, cols, rows), (db, ldd, 1)).fill_(True)
+    assert torch.isnan(dst.cpu()[~written]).all()
+
+
 @pytest.mark.parametrize("o,c,k", [(7, 3, 5), (96, 3, 11), (256, 96, 5), (384, 256, 3), (512, 512, 3),
                                    (50, 20, 5)])
 def test_conv_weight_tap_roundtrip(o, c, k):
