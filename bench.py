@@ -643,6 +643,7 @@ def run_groups(args, net, dev, world, rank, local):
             "staleness_mean": float(np.mean(st_)) if st_ else 0.0,
             "gpu_launches": None, "clocks": clk, "e2e": None, "cpu_baseline": None,
             "roofline": None})
+    rt.close()
     dist.destroy_process_group()
 
 

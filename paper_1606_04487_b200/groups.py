@@ -348,6 +348,15 @@ class GroupRuntime:
         for _ in range(rounds):
             self.round()
 
+    def close(self) -> None:
+        """Release the communicators and peer mappings (collective: every rank)."""
+        if self._x is not None and hasattr(self._x, "close"):
+            self._x.close()
+            self._x = None
+        if self._p2p and getattr(self, "_peer", None) is not None:
+            self._peer.close()
+            self._peer = None
+
     def round(self) -> None:
         """One round = g master updates, one per group, in group order."""
         if self._p2p:

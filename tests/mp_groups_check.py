@@ -66,6 +66,7 @@ def main():
                 [tuple(e[:4]) for e in ev]
         print(json.dumps({"world": world, "g": args.g, "k": plan.k, "updates": rt.t,
                           "weights_rel_err": err, "events_match": ev_ok, "pass": ev_ok and err < 1e-4}))
+    rt.close()
     dist.destroy_process_group()
 
 
