@@ -693,7 +693,20 @@ __global__ void __launch_bounds__(256) splitk_reduce_v4_kernel(const float* __re
     const int col = (i - row * n4) << 2;
     const float* src = ws + (long long)row * N + col;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);  // 0 + sum, as the generic kernel
-    for (int sp = 0; sp < S; ++sp) {
+    int sp = 0;
+    for (; sp + 4 <= S; sp += 4) {   // 4 split loads in flight, then the ordered adds
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(src + (sp + u) * MN));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc.x += v[u].x;
+        acc.y += v[u].y;
+        acc.z += v[u].z;
+        acc.w += v[u].w;
+      }
+    }
+    for (; sp < S; ++sp) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(src + sp * MN));
       acc.x += v.x;
       acc.y += v.y;
