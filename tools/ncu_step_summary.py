@@ -60,16 +60,32 @@ def main():
     if len(gemm) == len(roles):
         for o, role in zip(gemm, roles):
             o["role"] = role
+    # algorithmic DRAM bytes of the CaffeNet b = 256 GEMMs (each operand read once,
+    # the result written once; MB): the floor the measured DRAM MB compare to
+    b = 256
+    act = {"x1": b * 57 * 57 * 48, "y1": b * 55 * 55 * 96, "p1": b * 27 * 27 * 96, "y2": b * 27 * 27 * 256,
+           "p2": b * 13 * 13 * 256, "y3": b * 13 * 13 * 384, "y4": b * 13 * 13 * 384, "y5": b * 13 * 13 * 256,
+           "f6": b * 9216, "f7": b * 4096, "f8": b * 4096, "z8": b * 1000}
+    wts = {"conv1": 96 * 432, "conv2": 256 * 2400, "conv3": 384 * 2304, "conv4": 384 * 3456,
+           "conv5": 256 * 3456, "fc6": 9216 * 4096, "fc7": 4096 * 4096, "fc8": 4096 * 1000}
+    io = {"conv1": ("x1", "y1"), "conv2": ("p1", "y2"), "conv3": ("p2", "y3"), "conv4": ("y3", "y4"),
+          "conv5": ("y4", "y5"), "fc6": ("f6", "f7"), "fc7": ("f7", "f8"), "fc8": ("f8", "z8")}
+    for o in out:
+        if "role" in o:
+            layer = o["role"].split()[0]
+            i, y = io[layer]
+            o["algorithmic_MB"] = 4e-6 * (act[i] + act[y] + wts[layer])
     tot = sum(o["us"] for o in out)
     res = {"launches": len(out), "sum_us": tot, "hbm_peak_GBps": hbm, "per_launch": out}
     json.dump(res, open(args[1], "w"), indent=1)
     if len(args) > 2:
         with open(args[2], "w") as fh:
-            fh.write(f"| # | kernel | role | us | DRAM MB | GB/s | % of HBM {hbm:.0f} | tensor % |\n")
-            fh.write("|---|---|---|---|---|---|---|---|\n")
+            fh.write(f"| # | kernel | role | us | DRAM MB | algorithmic MB | GB/s | % of HBM {hbm:.0f} | tensor % |\n")
+            fh.write("|---|---|---|---|---|---|---|---|---|\n")
             for i, o in enumerate(out):
+                alg = f"{o['algorithmic_MB']:.1f}" if "algorithmic_MB" in o else ""
                 fh.write(f"| {i} | {o['kernel'][:48]} | {o.get('role', '')} | {o['us']:.1f} | "
-                         f"{o['dram_MB']:.1f} | {o['dram_GBps'] or 0:.0f} | "
+                         f"{o['dram_MB']:.1f} | {alg} | {o['dram_GBps'] or 0:.0f} | "
                          f"{100 * (o['frac_of_hbm'] or 0):.0f} | {o['tensor_active_pct'] or 0:.0f} |\n")
             fh.write(f"\nsum of launch times {tot:.0f} us (serialised, cold-cache ncu replays)\n")
 
