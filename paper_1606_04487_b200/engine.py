@@ -48,6 +48,7 @@ class Act:
     fused_relu: bool = False
     value: torch.Tensor | None = None
     grad: torch.Tensor | None = None
+    ones: bool = False  # flat: column c holds 1.0 (the FC weight-gradient GEMM's bias row)
 
     def shape(self, b):
         return (b, self.n, self.n, self.cs) if self.spatial else (b, self.cs)
@@ -200,18 +201,21 @@ class GpuNet:
                 i += 2 if nxt_relu else 1
             elif L.kind == "fc":
                 f = int(torch.tensor(g.in_shape).prod())
-                out = Act(False, L.d_out, 0, ru4(L.d_out), fused_relu=nxt_relu)
+                # row pitch with room for a ones column (the next FC layer's bias gradient)
+                out = Act(False, L.d_out, 0, ru4(L.d_out + 1), fused_relu=nxt_relu)
                 op = Op("fc", L, cur, out, woff=g.param_offsets[0], wsz=g.param_sizes[0],
                         boff=g.param_offsets[1], relu=nxt_relu, first_param_layer=first_param, f_in=f)
                 if cur.spatial:
-                    op.flat = Act(False, f, 0, ru4(f), fused_relu=cur.fused_relu)
-                    op.flat.value = z(self.b, ru4(f))
+                    op.flat = Act(False, f, 0, ru4(f + 1), fused_relu=cur.fused_relu)
+                    op.flat.value = z(self.b, op.flat.cs)
+                    op.flat.value[:, f] = 1.0
+                    op.flat.ones = True
                 else:
                     op.flat = cur
                 # FC weights (in, out) serve directly as the GEMM's B operand
                 # (MN-major forward, K-major data gradient) when TMA can read them.
                 op.w_inplace = L.d_out % 4 == 0 and g.param_offsets[0] % 4 == 0
-                op.wstage = None if op.w_inplace else z(L.d_out, ru4(f))
+                op.wstage = None if op.w_inplace else z(L.d_out, op.flat.cs)
                 first_param = False
                 i += 2 if nxt_relu else 1
             elif L.kind == "pool":
@@ -229,6 +233,9 @@ class GpuNet:
             else:  # pragma: no cover
                 raise ValueError(L)
             out.value = z(*out.shape(self.b))
+            if not out.spatial and out.cs > out.c:
+                out.value[:, out.c] = 1.0   # never written by the GEMMs (N = c); ReLU keeps it 1
+                out.ones = True
             self.ops.append(op)
             cur = out
         self.logits = cur
@@ -270,6 +277,8 @@ class GpuNet:
         self.overlap = not os.environ.get("OMNI_NO_SIDE_STREAM")
         # max pools over a fused-ReLU activation: mask folded into the argmax (mode 2)
         self.mark_pool = not os.environ.get("OMNI_NO_POOL_MARK")
+        # FC bias gradients as one more row of the weight-gradient GEMM (the ones column)
+        self.fc_bias_row = not os.environ.get("OMNI_NO_FC_BIAS_ROW")
 
     # ------------------------------------------------------------ shapes --
     def _workspace_need(self, op: Op, b: int) -> int:
@@ -309,7 +318,7 @@ class GpuNet:
             return out
         if op.kind == "fc":
             d = op.layer.d_out
-            out = [(b, d, op.f_in), (op.f_in, d, b)]
+            out = [(b, d, op.f_in), (op.f_in, d, b), (op.f_in + 1, d, b)]
             if not op.first_param_layer:
                 out.append((b, op.f_in, d))
             return out
@@ -554,11 +563,17 @@ class GpuNet:
                 d = L.d_out
                 dZ = op.out.grad
                 with wgrad_stream():
-                    # weight gradient straight into the flat (in, out) slice
-                    self._gemm(op.f_in, d, b, op.flat.value, op.flat.cs, True, dZ, op.out.cs, True,
-                               G[op.woff:op.woff + op.wsz], d)
-                    if op.boff >= 0:
-                        K.bias_grad(dZ, op.out.cs, b, d, G[op.boff:op.boff + d], self.bias_ws)
+                    if op.boff == op.woff + op.wsz and op.flat.ones and self.fc_bias_row:
+                        # weight + bias gradient in one GEMM: the input's ones column is
+                        # row f of X^T, and the bias follows the (in, out) weights in G
+                        self._gemm(op.f_in + 1, d, b, op.flat.value, op.flat.cs, True, dZ, op.out.cs,
+                                   True, G[op.woff:op.boff + d], d)
+                    else:
+                        # weight gradient straight into the flat (in, out) slice
+                        self._gemm(op.f_in, d, b, op.flat.value, op.flat.cs, True, dZ, op.out.cs, True,
+                                   G[op.woff:op.woff + op.wsz], d)
+                        if op.boff >= 0:
+                            K.bias_grad(dZ, op.out.cs, b, d, G[op.boff:op.boff + d], self.bias_ws)
                     done(op)
                 if op.first_param_layer:
                     continue
