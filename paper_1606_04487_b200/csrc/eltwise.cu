@@ -13,6 +13,27 @@ constexpr int kThreads = 256;
 
 inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
+// n / d for 0 <= n < 2^32 by one wide multiply: m = ceil(2^(32+s) / d) with
+// s = ceil(log2 d); the rounding error stays below 1/d, so the quotient is
+// exact (index math of the issue-bound pooling backward).
+struct FastDiv {
+  unsigned long long m;
+  int shift;
+  int d;
+};
+inline FastDiv fast_div(int d) {
+  int s = 0;
+  while ((1ll << s) < d) ++s;
+  FastDiv f;
+  f.m = (unsigned long long)((((unsigned __int128)1 << (32 + s)) + d - 1) / d);
+  f.shift = 32 + s;
+  f.d = d;
+  return f;
+}
+__device__ __forceinline__ int fdiv(int n, const FastDiv& f) {
+  return (int)(((unsigned __int128)(unsigned)n * f.m) >> f.shift);
+}
+
 __host__ __device__ inline int pool_out(int n, int k, int s, int p, int ceil_mode) {
   const int span = n + 2 * p - k;
   int out = (ceil_mode ? (span + s - 1) / s : span / s) + 1;
@@ -239,17 +260,17 @@ template <int MODE, int RM>
 __global__ void __launch_bounds__(kThreads) pool_bwd_s2_kernel(
     const float* __restrict__ dY, int b, int h, int w, int c, int cs_in, int k, int p, int oh,
     int ow, int cs_out, const int32_t* __restrict__ argmax, const float* __restrict__ X,
-    float* __restrict__ dX) {
+    float* __restrict__ dX, FastDiv dcv, FastDiv dbhw, FastDiv dbw) {
   constexpr int relu_mask_x = RM;
   const int cv = c / 4;
   const int bh = (h + 1) / 2, bw = (w + 1) / 2;
   const int total = b * bh * bw * cv;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-    const int blk = idx / cv;
+    const int blk = fdiv(idx, dcv);
     const int ch = (idx - blk * cv) * 4;
-    const int img = blk / (bh * bw);
+    const int img = fdiv(blk, dbhw);
     const int r = blk - img * bh * bw;
-    const int by = r / bw, bx = r - (r / bw) * bw;
+    const int by = fdiv(r, dbw), bx = r - by * bw;
     const int y0 = 2 * by, x0 = 2 * bx;
     const int y1 = min(y0 + 1, h - 1), x1 = min(x0 + 1, w - 1);
     const int oy0 = (y0 + p < k) ? 0 : (y0 + p - k) / 2 + 1;
@@ -726,9 +747,11 @@ int omni_pool_bwd_nhwc_f32(int mode, const float* dY, int b, int h, int w, int c
   if (v4 && stride == 2 && (k <= 3 || (k == 4 && pad % 2 == 0)) && !getenv("OMNI_POOL_BWD_PIXEL")) {
     const long long blocks = (long long)b * ((h + 1) / 2) * ((w + 1) / 2) * (c / 4);
     const int g2 = omni::grid_for(blocks, kThreads);
+    const FastDiv dcv = fast_div(c / 4), dbhw = fast_div(((h + 1) / 2) * ((w + 1) / 2)),
+                  dbw = fast_div((w + 1) / 2);
 #define OMNI_POOL_BWD_S2(M, R)                                                                    \
   pool_bwd_s2_kernel<M, R><<<g2, kThreads, 0, st>>>(dY, b, h, w, c, cs_in, k, pad, oh, ow, cs_out, argmax, \
-                                                    X, dX)
+                                                    X, dX, dcv, dbhw, dbw)
     if (mode == 0) {
       if (relu_mask_x == 2) OMNI_POOL_BWD_S2(0, 2);
       else if (relu_mask_x == 1) OMNI_POOL_BWD_S2(0, 1);
